@@ -1,0 +1,110 @@
+/*
+ * hybridpar_b200_denoiser.h — C ABI of the denoiser kernels behind the seam.
+ *
+ * The reference has no neural network: its only denoiser is the analytic
+ * Gaussian mixture eps_prediction (/root/reference/pkg/src/hybridpar/
+ * mixture.py:152-158), reached from engine.py:171-184 (_branches /
+ * _conditional_branch). These entry points are what a random-init
+ * SDXL-shaped U-Net or SD3-shaped MMDiT needs to stand in at that seam on
+ * B200: tcgen05/TMA GEMM and implicit-GEMM 3x3 convolution with fused
+ * epilogues, fused multi-head attention, and the memory-bound norm /
+ * resampling ops. All tensors are bf16 NHWC / row-major unless noted, all
+ * calls are stream-ordered, never allocate, and are CUDA-graph capturable.
+ */
+#ifndef HYBRIDPAR_B200_DENOISER_H
+#define HYBRIDPAR_B200_DENOISER_H
+
+#include <stdint.h>
+#include "hybridpar_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- GEMM / implicit-GEMM convolution (tcgen05 + TMA, TMEM accumulators) --- */
+#define HP_A_PLAIN        0   /* A is [M, K] row-major (lda elements)            */
+#define HP_A_CONV3X3      1   /* A is NHWC [n, h, w, c]; K = 9*c; pad 1, stride 1  */
+#define HP_A_CONV3X3_S2   2   /* same, stride 2 (output h/2 x w/2)                 */
+
+#define HP_ACT_NONE   0
+#define HP_ACT_GELU   1       /* exact erf GELU                                     */
+#define HP_ACT_SILU   2
+#define HP_ACT_GEGLU  3       /* weight rows interleaved per 2*BN/2 tile: out = a*gelu(b) */
+
+typedef struct hp_gemm_desc {
+    const void* a;     int64_t lda;            /* bf16                           */
+    int32_t a_mode;                            /* HP_A_*                         */
+    int32_t img_n, img_h, img_w, img_c;        /* conv input geometry            */
+    const void* b;     int64_t ldb;            /* bf16 weights [N, K] (K-major)  */
+    void* d;           int64_t ldd;            /* bf16 output [M, N_out]         */
+    int64_t M, N, K;
+    const float* bias;                         /* [N] or NULL                    */
+    const float* bias2; int64_t bias2_div;     /* bias2[(row/div)*N + col]       */
+    const void* residual; int64_t ldr;         /* bf16 [M, N_out] or NULL        */
+    int32_t act;                               /* HP_ACT_*                       */
+    int32_t block_n;                           /* 0 = auto                       */
+    float alpha;                               /* acc scale before bias          */
+} hp_gemm_desc;
+
+int hp_gemm(const hp_gemm_desc* d, void* stream);
+/* block_n the auto heuristic would choose (0 if unsupported shape) */
+int32_t hp_gemm_pick_block_n(int64_t M, int64_t N, int32_t act);
+
+/* ---- fused multi-head attention (tcgen05 S = QK^T and O = PV) -------------- */
+/* q: [B, Sq, ldq] with head h at column h*64 (+q_col0); k/v likewise with
+ * Skv rows; o: [B, Sq, ldo]. head_dim = 64. scale applied to QK^T.          */
+typedef struct hp_attn_desc {
+    const void* q; int64_t ldq; int64_t q_col0;
+    const void* k; int64_t ldk; int64_t k_col0;
+    const void* v; int64_t ldv; int64_t v_col0;
+    void* o;       int64_t ldo;
+    int32_t batch, heads, sq, skv;
+    float scale;
+} hp_attn_desc;
+int hp_attention(const hp_attn_desc* d, void* stream);
+
+/* ---- norms, activations, resampling (HBM-bound) --------------------------- */
+/* GroupNorm over NHWC bf16 (x1 channels c1, optional x2 concat channels c2),
+ * affine gamma/beta fp32, optional SiLU, writes y [n, hw, c1+c2] bf16.
+ * stats: workspace of >= 2*n*groups floats.                                  */
+int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_t n, int64_t hw,
+                  int32_t groups, float eps, const float* gamma, const float* beta, int32_t silu,
+                  void* y, float* stats, void* stream);
+/* LayerNorm over rows of bf16 [rows, c]; optional gamma/beta (fp32);
+ * optional adaLN modulation y = norm*(1+scale[b]) + shift[b] with
+ * b = row / rows_per_batch, scale/shift bf16 rows of length c (stride ldm). */
+int hp_layer_norm(const void* x, int64_t rows, int32_t c, float eps, const float* gamma,
+                  const float* beta, const void* shift, const void* scale, int64_t ldm,
+                  int64_t rows_per_batch, void* y, void* stream);
+/* y = silu(x) elementwise, bf16 */
+int hp_silu(const void* x, void* y, int64_t n, void* stream);
+/* nearest 2x upsample NHWC bf16: [n, h, w, c] -> [n, 2h, 2w, c] */
+int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, void* y, void* stream);
+/* channel concat NHWC: y[..., 0:c1] = a, y[..., c1:c1+c2] = b */
+int hp_concat_channels(const void* a, int32_t c1, const void* b, int32_t c2, int64_t pixels,
+                       void* y, void* stream);
+/* direct 3x3 conv for tiny channel counts (conv_in / conv_out): NHWC bf16 in,
+ * weights fp32 [cout, 3, 3, cin], bias fp32; out either bf16 NHWC or fp32  */
+int hp_conv3x3_small(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin,
+                     const float* wgt, const float* bias, int32_t cout, void* y,
+                     int32_t y_is_f32, void* stream);
+/* sinusoidal timestep embedding (flip_sin_to_cos, shift 0): out[b, dim] fp32 */
+int hp_timestep_embedding(const float* t, int32_t b, int32_t dim, float max_period, float* out,
+                          void* stream);
+/* small-M linear for embeddings: y[M, N] = act_out(act_in(x)[M, K] W[N, K]^T + bias), fp32 io,
+ * bf16 weights; act_* in {HP_ACT_NONE, HP_ACT_SILU}                         */
+int hp_linear_small(const float* x, int32_t M, int32_t K, const void* w, const float* bias,
+                    int32_t N, int32_t act_in, int32_t act_out, float* y, void* stream);
+/* patchify / unpatchify for the MMDiT (p = 2): NHWC latent <-> tokens        */
+int hp_patchify(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int32_t p, void* y,
+                void* stream);
+/* gated residual for adaLN-Zero: x[row, :] += gate[b, :] * y[row, :]        */
+int hp_gated_residual(void* x, const void* y, const void* gate, int64_t ldg, int64_t rows,
+                      int32_t c, int64_t rows_per_batch, void* stream);
+/* bf16 -> fp32 copy with layout change NHWC(c) -> flat latent (same order) */
+int hp_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYBRIDPAR_B200_DENOISER_H */

@@ -1,0 +1,419 @@
+// hp_gemm.cu — K4: persistent warp-specialised tcgen05 GEMM for the denoiser.
+//
+//   D[M, N] = epilogue( alpha * A[M, K] . B[N, K]^T )
+//
+// A is either a plain row-major activation matrix or, for 3x3 convolutions,
+// an NHWC activation read as an implicit GEMM: the K loop walks 9 taps x
+// (Cin/64) channel blocks and each A tile is one 4-D TMA box of the input
+// shifted by the tap offset (TMA zero-fills the padding halo; stride-2
+// convolutions use TMA element strides). B is the K-major weight [N, K]
+// (conv weights stored [Cout][3][3][Cin]). No im2col buffer exists.
+//
+// Roles (256 threads, 1 CTA/SM, persistent over output tiles):
+//   warp 0      TMA producer   (smem ring of STAGES {A 128x64, B BNx64} tiles, SW128)
+//   warp 1      MMA issuer     (tcgen05.mma M=128, N=BN, K=16; fp32 accumulators in TMEM)
+//   warp 2      TMEM allocator (2 x BN columns: accumulator double buffer)
+//   warps 4..7  epilogue       (tcgen05.ld 32x32b -> bias / per-image bias / residual /
+//                               GELU / SiLU / GEGLU -> bf16 stores)
+// The epilogue of tile i overlaps the MMAs of tile i+1 through the TMEM
+// double buffer; TMA runs STAGES k-blocks ahead of the tensor core.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string.h>
+#include <mutex>
+#include "hybridpar_b200_denoiser.h"
+#include "hp_tc.cuh"
+
+using namespace hptc;
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 256;
+constexpr uint32_t kABytes = BM * BK * 2;  // 16 KB
+
+struct GemmParams {
+  int M, N, K;
+  int num_kb;
+  int mode;          // HP_A_*
+  int cin_blocks;    // conv: Cin / 64
+  int out_h, out_w;  // conv output spatial size
+  int box_w, box_h;  // conv tile (output pixels)
+  int num_m_tiles, num_n_tiles;
+  __nv_bfloat16* d; long long ldd;
+  const float* bias;
+  const float* bias2; long long bias2_div;
+  const __nv_bfloat16* res; long long ldr;
+  int act;
+  float alpha;
+};
+
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+
+template <int BN>
+__device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
+                                              int lane) {
+  const int row = m0 + quarter * 32 + lane;
+  const bool row_ok = row < p.M;
+  const uint32_t lane_addr = tmem_acc + ((uint32_t)(quarter * 32) << 16);
+  if (p.act == HP_ACT_GEGLU) {
+    // tile columns [0, BN/2) are the linear halves, [BN/2, BN) the gates of
+    // the same BN/2 outputs (weights interleaved on the host)
+    const int out0 = n0 / 2;
+#pragma unroll 1
+    for (int c = 0; c < BN / 64; ++c) {
+      uint32_t ra[32], rg[32];
+      tmem_ld_32x32b_x32(lane_addr + c * 32, ra);
+      tmem_ld_32x32b_x32(lane_addr + BN / 2 + c * 32, rg);
+      tmem_ld_wait();
+      if (!row_ok) continue;
+      const int ocol = out0 + c * 32;
+      uint32_t packed[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        float a0 = __uint_as_float(ra[j]) * p.alpha, a1 = __uint_as_float(ra[j + 1]) * p.alpha;
+        float g0 = __uint_as_float(rg[j]) * p.alpha, g1 = __uint_as_float(rg[j + 1]) * p.alpha;
+        if (p.bias) {
+          a0 += p.bias[n0 + c * 32 + j];
+          a1 += p.bias[n0 + c * 32 + j + 1];
+          g0 += p.bias[n0 + BN / 2 + c * 32 + j];
+          g1 += p.bias[n0 + BN / 2 + c * 32 + j + 1];
+        }
+        packed[j / 2] = pack_bf16(a0 * gelu_erf(g0), a1 * gelu_erf(g1));
+      }
+      uint4* dst = reinterpret_cast<uint4*>(p.d + (long long)row * p.ldd + ocol);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+    }
+    return;
+  }
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(lane_addr + c * 32, r);
+    tmem_ld_wait();
+    if (!row_ok) continue;
+    const int col = n0 + c * 32;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+    if (p.bias) {
+      const float4* b4 = reinterpret_cast<const float4*>(p.bias + col);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 b = __ldg(b4 + q);
+        v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
+      }
+    }
+    if (p.bias2) {
+      const float4* b4 = reinterpret_cast<const float4*>(p.bias2 + (long long)(row / p.bias2_div) * p.N + col);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 b = __ldg(b4 + q);
+        v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
+      }
+    }
+    if (p.act == HP_ACT_GELU) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+    } else if (p.act == HP_ACT_SILU) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
+    }
+    if (p.res) {
+      const uint4* src = reinterpret_cast<const uint4*>(p.res + (long long)row * p.ldr + col);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u = src[q];
+        float2 f0 = unpack_bf16(u.x), f1 = unpack_bf16(u.y), f2 = unpack_bf16(u.z), f3 = unpack_bf16(u.w);
+        v[8 * q + 0] += f0.x; v[8 * q + 1] += f0.y; v[8 * q + 2] += f1.x; v[8 * q + 3] += f1.y;
+        v[8 * q + 4] += f2.x; v[8 * q + 5] += f2.y; v[8 * q + 6] += f3.x; v[8 * q + 7] += f3.y;
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(p.d + (long long)row * p.ldd + col);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      dst[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                          pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+  }
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  constexpr uint32_t kBBytes = BN * BK * 2;
+  constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  constexpr uint32_t kIdesc = idesc_bf16_f32(BM, BN);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------ TMA producer ------------------------------
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % p.num_m_tiles) * BM;
+        const int n0 = (tile / p.num_m_tiles) * BN;
+        int img = 0, y0 = 0, x0 = 0;
+        if (p.mode != HP_A_PLAIN) {
+          const int hw = p.out_h * p.out_w;
+          img = m0 / hw;
+          const int rem = m0 - img * hw;
+          y0 = rem / p.out_w;
+          x0 = rem - y0 * p.out_w;
+        }
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], kStageBytes);
+          uint8_t* a_dst = smA + s * kABytes;
+          if (p.mode == HP_A_PLAIN) {
+            tma_load_2d(a_dst, &tmA, &full[s], kb * BK, m0);
+          } else {
+            const int tap = kb / p.cin_blocks;
+            const int cb = kb - tap * p.cin_blocks;
+            const int dy = tap / 3, dx = tap - dy * 3;
+            if (p.mode == HP_A_CONV3X3) {
+              tma_load_4d(a_dst, &tmA, &full[s], cb * BK, x0 + dx - 1, y0 + dy - 1, img);
+            } else {
+              tma_load_4d(a_dst, &tmA, &full[s], cb * BK, 2 * x0 + dx - 1, 2 * y0 + dy - 1, img);
+            }
+          }
+          tma_load_2d(smB + s * kBBytes, &tmB, &full[s], kb * BK, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------ MMA issuer ------------------------------
+      uint32_t it = 0, local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const uint32_t acc = local & 1;
+        const uint32_t use = local >> 1;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t da = sdesc_sw128_kmajor(smA + s * kABytes);
+          const uint64_t db = sdesc_sw128_kmajor(smB + s * kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // +32 bytes along K inside the 128-byte swizzle atom = +2 in the address field
+            umma_bf16(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb | k) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------ epilogue ------------------------------
+    const int quarter = warp & 3;
+    uint32_t local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const uint32_t acc = local & 1;
+      const uint32_t use = local >> 1;
+      const int m0 = (tile % p.num_m_tiles) * BM;
+      const int n0 = (tile / p.num_m_tiles) * BN;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      epilogue_tile<BN>(p, tmem_base + acc * BN, m0, n0, quarter, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps (driver entry point, no -lcuda link dependency)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+              const uint32_t* box, const uint32_t* estride) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; e[i] = estride ? estride[i] : 1; }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, b, e,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int BN, int STAGES>
+int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
+  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + BN * BK * 2) + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return HP_ERR_CUDA;
+    attr_set = true;
+  }
+  const int tiles = p.num_m_tiles * p.num_n_tiles;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_kernel<BN, STAGES><<<grid, kThreads, smem, st>>>(ta, tb, p);
+  return cudaGetLastError() == cudaSuccess ? HP_OK : HP_ERR_CUDA;
+}
+
+int pick_bn(int64_t M, int64_t N, int act) {
+  const int cands[4] = {256, 160, 128, 64};
+  int best = 0;
+  double best_cost = 1e30;
+  const int64_t mt = (M + BM - 1) / BM;
+  const int sms = g_num_sms ? g_num_sms : 148;
+  for (int bn : cands) {
+    if (N % bn) continue;
+    if (act == HP_ACT_GEGLU && bn != 256 && bn != 128) continue;
+    const int64_t tiles = mt * (N / bn);
+    const int64_t waves = (tiles + sms - 1) / sms;
+    const double cost = (double)waves * (bn + 48);
+    if (cost < best_cost - 1e-9) { best_cost = cost; best = bn; }
+  }
+  return best;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t hp_gemm_pick_block_n(int64_t M, int64_t N, int32_t act) { return pick_bn(M, N, act); }
+
+int hp_gemm(const hp_gemm_desc* d, void* stream) {
+  if (!d || !d->a || !d->b || !d->d) return HP_ERR_PARAMETER;
+  if (d->M <= 0 || d->N <= 0 || d->K <= 0) return HP_ERR_SHAPE;
+  if ((d->K % 8) || (d->ldb % 8)) return HP_ERR_UNSUPPORTED;   // 16-byte TMA strides
+  if ((reinterpret_cast<uintptr_t>(d->a) | reinterpret_cast<uintptr_t>(d->b)) & 15) return HP_ERR_UNSUPPORTED;
+  num_sms();
+  const int bn = d->block_n ? d->block_n : pick_bn(d->M, d->N, d->act);
+  if (bn == 0 || d->N % bn) return HP_ERR_UNSUPPORTED;
+  if (d->act == HP_ACT_GEGLU && (bn % 64)) return HP_ERR_UNSUPPORTED;
+  const int64_t n_out = d->act == HP_ACT_GEGLU ? d->N / 2 : d->N;
+  if ((d->ldd % 8) || (d->residual && (d->ldr % 8)) || (n_out % 32)) return HP_ERR_UNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(d->d) & 15) || (d->bias && (reinterpret_cast<uintptr_t>(d->bias) & 15)))
+    return HP_ERR_UNSUPPORTED;
+
+  GemmParams p{};
+  p.M = (int)d->M; p.N = (int)d->N; p.K = (int)d->K;
+  p.mode = d->a_mode;
+  p.d = static_cast<__nv_bfloat16*>(d->d); p.ldd = d->ldd;
+  p.bias = d->bias; p.bias2 = d->bias2; p.bias2_div = d->bias2_div > 0 ? d->bias2_div : 1;
+  p.res = static_cast<const __nv_bfloat16*>(d->residual); p.ldr = d->ldr;
+  p.act = d->act;
+  p.alpha = d->alpha == 0.0f ? 1.0f : d->alpha;
+  p.num_m_tiles = (int)((d->M + BM - 1) / BM);
+  p.num_n_tiles = (int)(d->N / bn);
+
+  CUtensorMap ta, tb;
+  if (d->a_mode == HP_A_PLAIN) {
+    if (d->lda % 8) return HP_ERR_UNSUPPORTED;
+    p.num_kb = (int)((d->K + BK - 1) / BK);
+    const uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)d->M};
+    const uint64_t str[1] = {(uint64_t)d->lda * 2};
+    const uint32_t box[2] = {BK, BM};
+    if (!make_map(&ta, d->a, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;
+  } else if (d->a_mode == HP_A_CONV3X3 || d->a_mode == HP_A_CONV3X3_S2) {
+    const int s = d->a_mode == HP_A_CONV3X3_S2 ? 2 : 1;
+    const int c = d->img_c;
+    if (c % BK || d->K != 9LL * c) return HP_ERR_SHAPE;
+    p.out_h = d->img_h / s;
+    p.out_w = d->img_w / s;
+    if ((int64_t)d->img_n * p.out_h * p.out_w != d->M) return HP_ERR_SHAPE;
+    p.box_w = p.out_w < BM ? p.out_w : BM;
+    p.box_h = BM / p.box_w;
+    if (BM % p.box_w || p.out_w % p.box_w || p.out_h % p.box_h) return HP_ERR_UNSUPPORTED;
+    p.cin_blocks = c / BK;
+    p.num_kb = 9 * p.cin_blocks;
+    const uint64_t dims[4] = {(uint64_t)c, (uint64_t)d->img_w, (uint64_t)d->img_h, (uint64_t)d->img_n};
+    const uint64_t str[3] = {(uint64_t)c * 2, (uint64_t)d->img_w * c * 2, (uint64_t)d->img_h * d->img_w * c * 2};
+    const uint32_t box[4] = {BK, (uint32_t)(p.box_w * s), (uint32_t)(p.box_h * s), 1};
+    const uint32_t es[4] = {1, (uint32_t)s, (uint32_t)s, 1};
+    if (!make_map(&ta, d->a, 4, dims, str, box, es)) return HP_ERR_CUDA;
+  } else {
+    return HP_ERR_PARAMETER;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)d->N};
+    const uint64_t str[1] = {(uint64_t)d->ldb * 2};
+    const uint32_t box[2] = {BK, (uint32_t)bn};
+    if (!make_map(&tb, d->b, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (bn) {
+    case 256: return launch_gemm<256, 4>(ta, tb, p, st);
+    case 160: return launch_gemm<160, 5>(ta, tb, p, st);
+    case 128: return launch_gemm<128, 6>(ta, tb, p, st);
+    case 64: return launch_gemm<64, 8>(ta, tb, p, st);
+    default: return HP_ERR_UNSUPPORTED;
+  }
+}
+
+}  // extern "C"

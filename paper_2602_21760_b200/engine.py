@@ -256,7 +256,7 @@ class _StepRunner:
         K.sampler_step(x=x, eps_c=eps_c, eps_u=eps_u, x_out=out, x_out_bf16=outb,
                        update=self.update, t=t, w=self.plan.guidance.w,
                        dt=1.0 / self.plan.schedule.T, ws=self.ws, discrepancy=discrepancy,
-                       ctrl=self.ctrl, ctrl_op=ctrl_op, mirror_ptr=self.mirror.ptr)
+                       ctrl=self.ctrl, ctrl_op=ctrl_op, mirror_ptr=self.mirror.ptr, **kw)
         return out, outb
 
     def measured(self, x, xb, t, ctrl_op):
