@@ -95,9 +95,13 @@ int hp_timestep_embedding(const float* t, int32_t b, int32_t dim, float max_peri
  * bf16 weights; act_* in {HP_ACT_NONE, HP_ACT_SILU}                         */
 int hp_linear_small(const float* x, int32_t M, int32_t K, const void* w, const float* bias,
                     int32_t N, int32_t act_in, int32_t act_out, float* y, void* stream);
-/* patchify / unpatchify for the MMDiT (p = 2): NHWC latent <-> tokens        */
-int hp_patchify(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int32_t p, void* y,
-                void* stream);
+/* patchify (inverse = 0): NHWC latent [n,h,w,c] -> tokens [n, (h/p)(w/p), p*p*c]
+ * ordered (py, px, c); inverse = 1 maps tokens back to the latent.           */
+int hp_patchify(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int32_t p,
+                int32_t inverse, void* y, void* stream);
+/* y[row, :] = x[row, :] + add[row % add_rows, :]  (positional embedding), bf16 */
+int hp_add_rows(const void* x, const void* add, int64_t rows, int64_t add_rows, int32_t c,
+                void* y, void* stream);
 /* gated residual for adaLN-Zero: x[row, :] += gate[b, :] * y[row, :]        */
 int hp_gated_residual(void* x, const void* y, const void* gate, int64_t ldg, int64_t rows,
                       int32_t c, int64_t rows_per_batch, void* stream);

@@ -1,0 +1,548 @@
+// hp_norm.cu — K6: the denoiser's memory-bound ops on bf16 NHWC / row tensors.
+//
+// GroupNorm(+SiLU) is two passes (per-image partial statistics over pixel
+// chunks, then a normalise pass that folds the partials in fixed order), so
+// it is deterministic and batch-invariant: image b's statistics never depend
+// on the other images in the batch. LayerNorm is one warp per row with an
+// exact two-pass mean/variance from registers and optional adaLN modulation.
+// Everything else is a 16-byte-vectorised streaming kernel.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <math.h>
+#include "hybridpar_b200_denoiser.h"
+#include "hp_common.cuh"
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ void load8(const bf16* p, float* v) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void store8(bf16* p, const float* v) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+inline int nblocks(int64_t work, int per_block, int cap = 148 * 16) {
+  int64_t b = (work + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+inline bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------------------
+// GroupNorm pass 1: grid (splits, n). Thread t owns 8-channel vector j = t % V
+// of pixels t / V, t / V + R, ... within the block's pixel chunk.
+constexpr int kGnThreads = 256;
+constexpr int kMaxC = 2560;
+
+__global__ void __launch_bounds__(kGnThreads)
+gn_stats_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
+                int groups, int splits, float* __restrict__ part) {
+  __shared__ float s_sum[kMaxC], s_sq[kMaxC];
+  const int C = c1 + c2;
+  const int V = C / 8;
+  const int n = blockIdx.y, split = blockIdx.x;
+  for (int c = threadIdx.x; c < C; c += kGnThreads) { s_sum[c] = 0.f; s_sq[c] = 0.f; }
+  __syncthreads();
+  const int64_t p_begin = hw * split / splits, p_end = hw * (split + 1) / splits;
+  for (int j0 = 0; j0 < V; j0 += kGnThreads) {
+    const int vecs = min(V - j0, kGnThreads);
+    const int rows = kGnThreads / vecs;
+    const int j = j0 + threadIdx.x % vecs;
+    const int r = threadIdx.x / vecs;
+    if (r >= rows) continue;
+    float sum[8] = {0}, sq[8] = {0};
+    const int ch = j * 8;
+    for (int64_t p = p_begin + r; p < p_end; p += rows) {
+      float v[8];
+      if (ch < c1) load8(x1 + ((int64_t)n * hw + p) * c1 + ch, v);
+      else load8(x2 + ((int64_t)n * hw + p) * c2 + (ch - c1), v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { sum[i] += v[i]; sq[i] += v[i] * v[i]; }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { atomicAdd(&s_sum[ch + i], sum[i]); atomicAdd(&s_sq[ch + i], sq[i]); }
+  }
+  __syncthreads();
+  const int cg = C / groups;
+  for (int g = threadIdx.x; g < groups; g += kGnThreads) {
+    float a = 0.f, b = 0.f;
+    for (int c = g * cg; c < (g + 1) * cg; ++c) { a += s_sum[c]; b += s_sq[c]; }
+    float* o = part + (((int64_t)n * splits + split) * groups + g) * 2;
+    o[0] = a;
+    o[1] = b;
+  }
+}
+
+// GroupNorm pass 2: grid (chunks, n); stats folded per block in fixed order.
+__global__ void __launch_bounds__(kGnThreads)
+gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
+                int groups, int splits, const float* __restrict__ part, float eps,
+                const float* __restrict__ gamma, const float* __restrict__ beta, int do_silu,
+                bf16* __restrict__ y) {
+  __shared__ float s_mean[64], s_rstd[64];
+  const int C = c1 + c2;
+  const int V = C / 8;
+  const int n = blockIdx.y;
+  const int cg = C / groups;
+  if (threadIdx.x < groups) {
+    double a = 0.0, b = 0.0;
+    for (int s = 0; s < splits; ++s) {
+      const float* o = part + (((int64_t)n * splits + s) * groups + threadIdx.x) * 2;
+      a += (double)o[0];
+      b += (double)o[1];
+    }
+    const double cnt = (double)hw * cg;
+    const double mean = a / cnt;
+    double var = b / cnt - mean * mean;
+    if (var < 0) var = 0;
+    s_mean[threadIdx.x] = (float)mean;
+    s_rstd[threadIdx.x] = (float)(1.0 / sqrt(var + (double)eps));
+  }
+  __syncthreads();
+  const int64_t total = hw * V;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / V;
+    const int j = (int)(i - p * V);
+    const int ch = j * 8;
+    float v[8];
+    if (ch < c1) load8(x1 + ((int64_t)n * hw + p) * c1 + ch, v);
+    else load8(x2 + ((int64_t)n * hw + p) * c2 + (ch - c1), v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = ch + k;
+      const int g = c / cg;
+      float o = (v[k] - s_mean[g]) * s_rstd[g];
+      o = o * gamma[c] + beta[c];
+      v[k] = do_silu ? silu(o) : o;
+    }
+    store8(y + ((int64_t)n * hw + p) * C + ch, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LayerNorm: one warp per row, c <= 32 * 8 * kLnVec
+constexpr int kLnVec = 8;
+__global__ void __launch_bounds__(256)
+ln_kernel(const bf16* __restrict__ x, int64_t rows, int c, float eps, const float* __restrict__ gamma,
+          const float* __restrict__ beta, const bf16* __restrict__ shift, const bf16* __restrict__ scale,
+          int64_t ldm, int64_t rows_per_batch, bf16* __restrict__ y) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
+  if (row >= rows) return;
+  const int V = c / 8;
+  const bf16* xr = x + row * c;
+  float v[kLnVec][8];
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < kLnVec; ++k) {
+    const int j = lane + 32 * k;
+    if (j < V) {
+      load8(xr + j * 8, v[k]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum += v[k][i];
+    }
+  }
+  sum = hp_warp_sum_f(sum);
+  const float mean = sum / c;
+  float sq = 0.f;
+#pragma unroll
+  for (int k = 0; k < kLnVec; ++k) {
+    const int j = lane + 32 * k;
+    if (j < V) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { const float d = v[k][i] - mean; sq += d * d; }
+    }
+  }
+  sq = hp_warp_sum_f(sq);
+  const float rstd = rsqrtf(sq / c + eps);
+  const int64_t b = rows_per_batch > 0 ? row / rows_per_batch : 0;
+#pragma unroll
+  for (int k = 0; k < kLnVec; ++k) {
+    const int j = lane + 32 * k;
+    if (j >= V) continue;
+    float o[8], sh[8], sc[8];
+    if (shift) load8(shift + b * ldm + j * 8, sh);
+    if (scale) load8(scale + b * ldm + j * 8, sc);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int ch = j * 8 + i;
+      float t = (v[k][i] - mean) * rstd;
+      if (gamma) t = t * gamma[ch];
+      if (beta) t = t + beta[ch];
+      if (scale) t = t * (1.0f + sc[i]);
+      if (shift) t = t + sh[i];
+      o[i] = t;
+    }
+    store8(y + row * c + j * 8, o);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void silu_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, int64_t n8) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float v[8];
+    load8(x + i * 8, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = silu(v[k]);
+    store8(y + i * 8, v);
+  }
+}
+
+__global__ void upsample2x_kernel(const bf16* __restrict__ x, int n, int h, int w, int c, bf16* __restrict__ y) {
+  const int V = c / 8;
+  const int64_t total = (int64_t)n * 2 * h * 2 * w * V;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % V);
+    int64_t pix = i / V;
+    const int ox = (int)(pix % (2 * w));
+    pix /= (2 * w);
+    const int oy = (int)(pix % (2 * h));
+    const int b = (int)(pix / (2 * h));
+    const uint4 u = *reinterpret_cast<const uint4*>(x + (((int64_t)b * h + oy / 2) * w + ox / 2) * c + j * 8);
+    *reinterpret_cast<uint4*>(y + i * 8) = u;
+  }
+}
+
+__global__ void concat_kernel(const bf16* __restrict__ a, int c1, const bf16* __restrict__ b, int c2,
+                              int64_t pixels, bf16* __restrict__ y) {
+  const int V1 = c1 / 8, V = (c1 + c2) / 8;
+  const int64_t total = pixels * V;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / V;
+    const int j = (int)(i - p * V);
+    uint4 u = j < V1 ? *reinterpret_cast<const uint4*>(a + p * c1 + j * 8)
+                     : *reinterpret_cast<const uint4*>(b + p * c2 + (j - V1) * 8);
+    *reinterpret_cast<uint4*>(y + i * 8) = u;
+  }
+}
+
+// conv_in style: cin small (<= 16), cout multiple of 8. Thread = (pixel, 8 cout).
+__global__ void conv_small_in_kernel(const bf16* __restrict__ x, int n, int h, int w, int cin,
+                                     const float* __restrict__ wgt, const float* __restrict__ bias, int cout,
+                                     bf16* __restrict__ y) {
+  extern __shared__ float s_w[];  // [cout][9*cin]
+  const int kk = 9 * cin;
+  for (int i = threadIdx.x; i < cout * kk; i += blockDim.x) s_w[i] = wgt[i];
+  __syncthreads();
+  const int G = cout / 8;
+  const int64_t total = (int64_t)n * h * w * G;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(i % G);
+    const int64_t pix = i / G;
+    const int xx = (int)(pix % w);
+    const int yy = (int)((pix / w) % h);
+    const int b = (int)(pix / ((int64_t)w * h));
+    float in[9 * 16];
+    for (int t = 0; t < 9; ++t) {
+      const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
+      const bool ok = sy >= 0 && sy < h && sx >= 0 && sx < w;
+      for (int ci = 0; ci < cin; ++ci)
+        in[t * cin + ci] = ok ? __bfloat162float(x[(((int64_t)b * h + sy) * w + sx) * cin + ci]) : 0.f;
+    }
+    float o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int co = g * 8 + k;
+      float acc = bias ? bias[co] : 0.f;
+      const float* wr = s_w + co * kk;
+      for (int q = 0; q < kk; ++q) acc = fmaf(in[q], wr[q], acc);
+      o[k] = acc;
+    }
+    store8(y + pix * cout + g * 8, o);
+  }
+}
+
+// conv_out style: cout small (<= 8), cin multiple of 8. One warp per output pixel.
+__global__ void conv_small_out_kernel(const bf16* __restrict__ x, int n, int h, int w, int cin,
+                                      const float* __restrict__ wgt, const float* __restrict__ bias, int cout,
+                                      void* __restrict__ y, int y_f32) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int64_t pixels = (int64_t)n * h * w;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int V = cin / 8;
+  for (int64_t pix = warp; pix < pixels; pix += nwarps) {
+    const int xx = (int)(pix % w);
+    const int yy = (int)((pix / w) % h);
+    const int b = (int)(pix / ((int64_t)w * h));
+    float acc[8] = {0};
+    for (int q = lane; q < 9 * V; q += 32) {
+      const int t = q / V, j = q - t * V;
+      const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
+      if (sy < 0 || sy >= h || sx < 0 || sx >= w) continue;
+      float v[8];
+      load8(x + (((int64_t)b * h + sy) * w + sx) * cin + j * 8, v);
+      for (int co = 0; co < cout; ++co) {
+        const float* wr = wgt + ((int64_t)co * 9 + t) * cin + j * 8;
+        float a = acc[co];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a = fmaf(v[i], wr[i], a);
+        acc[co] = a;
+      }
+    }
+    for (int co = 0; co < cout; ++co) acc[co] = hp_warp_sum_f(acc[co]);
+    if (lane < cout) {
+      float r = 0.f;
+      for (int co = 0; co < cout; ++co) if (co == lane) r = acc[co];
+      r += bias ? bias[lane] : 0.f;
+      if (y_f32) static_cast<float*>(y)[pix * cout + lane] = r;
+      else static_cast<bf16*>(y)[pix * cout + lane] = __float2bfloat16_rn(r);
+    }
+  }
+}
+
+__global__ void timestep_emb_kernel(const float* __restrict__ t, int b, int dim, float max_period,
+                                    float* __restrict__ out) {
+  const int half = dim / 2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < b * half; i += gridDim.x * blockDim.x) {
+    const int r = i / half, k = i - r * half;
+    const float freq = expf(-logf(max_period) * (float)k / (float)half);
+    const float arg = t[r] * freq;
+    out[(int64_t)r * dim + k] = cosf(arg);          // flip_sin_to_cos: [cos, sin]
+    out[(int64_t)r * dim + half + k] = sinf(arg);
+  }
+}
+
+// y[m, n] = act_out(sum_k act_in(x[m, k]) * W[n, k] + bias[n]); one warp per (n), all M rows
+constexpr int kSmallMaxM = 8;
+__global__ void linear_small_kernel(const float* __restrict__ x, int M, int K, const bf16* __restrict__ w,
+                                    const float* __restrict__ bias, int N, int act_in, int act_out,
+                                    float* __restrict__ y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int n = warp; n < N; n += nwarps) {
+    float acc[kSmallMaxM] = {0};
+    const bf16* wr = w + (int64_t)n * K;
+    for (int k = lane * 8; k < K; k += 256) {
+      float wv[8];
+      load8(wr + k, wv);
+      for (int m = 0; m < M; ++m) {
+        const float* xr = x + (int64_t)m * K + k;
+        float a = acc[m];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float xv = xr[i];
+          if (act_in == HP_ACT_SILU) xv = silu(xv);
+          a = fmaf(xv, wv[i], a);
+        }
+        acc[m] = a;
+      }
+    }
+    for (int m = 0; m < M; ++m) {
+      float r = hp_warp_sum_f(acc[m]);
+      if (lane == 0) {
+        r += bias ? bias[n] : 0.f;
+        if (act_out == HP_ACT_SILU) r = silu(r);
+        y[(int64_t)m * N + n] = r;
+      }
+    }
+  }
+}
+
+__global__ void patchify_kernel(const bf16* __restrict__ x, int n, int h, int w, int c, int p, int inverse,
+                                bf16* __restrict__ y) {
+  // token t = (ty, tx); feature f = (py * p + px) * c + ch
+  const int64_t total = (int64_t)n * h * w * c;
+  const int tw = w / p;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % c);
+    int64_t pix = i / c;
+    const int xx = (int)(pix % w);
+    const int yy = (int)((pix / w) % h);
+    const int b = (int)(pix / ((int64_t)w * h));
+    const int64_t tok = ((int64_t)b * (h / p) + yy / p) * tw + xx / p;
+    const int64_t f = ((int64_t)(yy % p) * p + (xx % p)) * c + ch;
+    const int64_t ti = tok * ((int64_t)p * p * c) + f;
+    if (!inverse) y[ti] = x[i];
+    else y[i] = x[ti];
+  }
+}
+
+__global__ void add_rows_kernel(const bf16* __restrict__ x, const bf16* __restrict__ add, int64_t rows,
+                                int64_t add_rows, int c, bf16* __restrict__ y) {
+  const int V = c / 8;
+  const int64_t total = rows * V;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / V;
+    const int j = (int)(i - r * V);
+    float a[8], b[8];
+    load8(x + r * c + j * 8, a);
+    load8(add + (r % add_rows) * c + j * 8, b);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] += b[k];
+    store8(y + r * c + j * 8, a);
+  }
+}
+
+__global__ void gated_residual_kernel(bf16* __restrict__ x, const bf16* __restrict__ yv,
+                                      const bf16* __restrict__ gate, int64_t ldg, int64_t rows, int c,
+                                      int64_t rows_per_batch) {
+  const int V = c / 8;
+  const int64_t total = rows * V;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / V;
+    const int j = (int)(i - r * V);
+    const int64_t b = r / rows_per_batch;
+    float a[8], v[8], g[8];
+    load8(x + r * c + j * 8, a);
+    load8(yv + r * c + j * 8, v);
+    load8(gate + b * ldg + j * 8, g);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] += g[k] * v[k];
+    store8(x + r * c + j * 8, a);
+  }
+}
+
+__global__ void cast_kernel(const bf16* __restrict__ x, float* __restrict__ y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __bfloat162float(x[i]);
+}
+
+inline int ok() { return cudaGetLastError() == cudaSuccess ? HP_OK : HP_ERR_CUDA; }
+
+}  // namespace
+
+extern "C" {
+
+int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_t n, int64_t hw, int32_t groups,
+                  float eps, const float* gamma, const float* beta, int32_t do_silu, void* y, float* stats,
+                  void* stream) {
+  const int C = c1 + (x2 ? c2 : 0);
+  if (!x1 || !y || !gamma || !beta || !stats) return HP_ERR_PARAMETER;
+  if (C % 8 || c1 % 8 || C > kMaxC || groups < 1 || groups > 64 || C % groups || n < 1 || hw < 1) return HP_ERR_SHAPE;
+  if (!a16(x1) || (x2 && !a16(x2)) || !a16(y)) return HP_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int splits = (296 + n - 1) / n;
+  if (splits > hw) splits = (int)hw;
+  if (splits > 64) splits = 64;
+  gn_stats_kernel<<<dim3(splits, n), kGnThreads, 0, st>>>(static_cast<const bf16*>(x1), c1,
+                                                          static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups,
+                                                          splits, stats);
+  const int64_t per_img = hw * (C / 8);
+  int chunks = nblocks(per_img, kGnThreads * 4, 4096);
+  gn_apply_kernel<<<dim3(chunks, n), kGnThreads, 0, st>>>(static_cast<const bf16*>(x1), c1,
+                                                          static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups,
+                                                          splits, stats, eps, gamma, beta, do_silu,
+                                                          static_cast<bf16*>(y));
+  return ok();
+}
+
+int hp_layer_norm(const void* x, int64_t rows, int32_t c, float eps, const float* gamma, const float* beta,
+                  const void* shift, const void* scale, int64_t ldm, int64_t rows_per_batch, void* y, void* stream) {
+  if (!x || !y) return HP_ERR_PARAMETER;
+  if (c % 8 || c > 32 * 8 * kLnVec || rows < 1) return HP_ERR_SHAPE;
+  if ((shift || scale) && (rows_per_batch < 1 || ldm % 8)) return HP_ERR_PARAMETER;
+  const int blocks = (int)((rows + 7) / 8);
+  ln_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(x), rows, c, eps, gamma, beta, static_cast<const bf16*>(shift),
+      static_cast<const bf16*>(scale), ldm, rows_per_batch, static_cast<bf16*>(y));
+  return ok();
+}
+
+int hp_silu(const void* x, void* y, int64_t n, void* stream) {
+  if (!x || !y || n % 8) return HP_ERR_PARAMETER;
+  silu_kernel<<<nblocks(n / 8, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const bf16*>(x),
+                                                                                   static_cast<bf16*>(y), n / 8);
+  return ok();
+}
+
+int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, void* y, void* stream) {
+  if (!x || !y || c % 8) return HP_ERR_PARAMETER;
+  const int64_t total = (int64_t)n * 4 * h * w * (c / 8);
+  upsample2x_kernel<<<nblocks(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(x), n, h, w, c, static_cast<bf16*>(y));
+  return ok();
+}
+
+int hp_concat_channels(const void* a, int32_t c1, const void* b, int32_t c2, int64_t pixels, void* y, void* stream) {
+  if (!a || !b || !y || c1 % 8 || c2 % 8) return HP_ERR_PARAMETER;
+  concat_kernel<<<nblocks(pixels * ((c1 + c2) / 8), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(a), c1, static_cast<const bf16*>(b), c2, pixels, static_cast<bf16*>(y));
+  return ok();
+}
+
+int hp_conv3x3_small(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin, const float* wgt,
+                     const float* bias, int32_t cout, void* y, int32_t y_is_f32, void* stream) {
+  if (!x || !wgt || !y) return HP_ERR_PARAMETER;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cin <= 16 && cout % 8 == 0 && !y_is_f32) {
+    const size_t smem = (size_t)cout * 9 * cin * sizeof(float);
+    if (smem > 200 * 1024) return HP_ERR_UNSUPPORTED;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(conv_small_in_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t total = (int64_t)n * h * w * (cout / 8);
+    conv_small_in_kernel<<<nblocks(total, 256, 148 * 4), 256, smem, st>>>(static_cast<const bf16*>(x), n, h, w, cin,
+                                                                           wgt, bias, cout, static_cast<bf16*>(y));
+    return ok();
+  }
+  if (cout <= 8 && cin % 8 == 0) {
+    const int64_t pixels = (int64_t)n * h * w;
+    conv_small_out_kernel<<<nblocks(pixels * 32, 256, 148 * 16), 256, 0, st>>>(static_cast<const bf16*>(x), n, h, w,
+                                                                                cin, wgt, bias, cout, y, y_is_f32);
+    return ok();
+  }
+  return HP_ERR_UNSUPPORTED;
+}
+
+int hp_timestep_embedding(const float* t, int32_t b, int32_t dim, float max_period, float* out, void* stream) {
+  if (!t || !out || dim % 2) return HP_ERR_PARAMETER;
+  timestep_emb_kernel<<<nblocks((int64_t)b * dim / 2, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      t, b, dim, max_period, out);
+  return ok();
+}
+
+int hp_linear_small(const float* x, int32_t M, int32_t K, const void* w, const float* bias, int32_t N,
+                    int32_t act_in, int32_t act_out, float* y, void* stream) {
+  if (!x || !w || !y) return HP_ERR_PARAMETER;
+  if (M < 1 || M > kSmallMaxM || K % 8) return HP_ERR_SHAPE;
+  linear_small_kernel<<<nblocks((int64_t)N * 32, 256, 148 * 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, M, K, static_cast<const bf16*>(w), bias, N, act_in, act_out, y);
+  return ok();
+}
+
+int hp_patchify(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int32_t p, int32_t inverse, void* y,
+                void* stream) {
+  if (!x || !y || p < 1 || h % p || w % p) return HP_ERR_PARAMETER;
+  patchify_kernel<<<nblocks((int64_t)n * h * w * c, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(x), n, h, w, c, p, inverse, static_cast<bf16*>(y));
+  return ok();
+}
+
+int hp_add_rows(const void* x, const void* add, int64_t rows, int64_t add_rows, int32_t c, void* y, void* stream) {
+  if (!x || !add || !y || c % 8 || add_rows < 1) return HP_ERR_PARAMETER;
+  add_rows_kernel<<<nblocks(rows * (c / 8), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(x), static_cast<const bf16*>(add), rows, add_rows, c, static_cast<bf16*>(y));
+  return ok();
+}
+
+int hp_gated_residual(void* x, const void* y, const void* gate, int64_t ldg, int64_t rows, int32_t c,
+                      int64_t rows_per_batch, void* stream) {
+  if (!x || !y || !gate || c % 8 || rows_per_batch < 1 || ldg % 8) return HP_ERR_PARAMETER;
+  gated_residual_kernel<<<nblocks(rows * (c / 8), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<bf16*>(x), static_cast<const bf16*>(y), static_cast<const bf16*>(gate), ldg, rows, c,
+      rows_per_batch);
+  return ok();
+}
+
+int hp_cast_bf16_f32(const void* x, float* y, int64_t n, void* stream) {
+  if (!x || !y) return HP_ERR_PARAMETER;
+  cast_kernel<<<nblocks(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const bf16*>(x), y, n);
+  return ok();
+}
+
+}  // extern "C"

@@ -1,7 +1,232 @@
-"""ctypes bindings of the denoiser kernels (include/hybridpar_b200_denoiser.h)."""
+"""ctypes bindings of the denoiser kernels (include/hybridpar_b200_denoiser.h).
+
+Thin torch-tensor wrappers: shapes/dtypes are checked here, pointers and the
+current stream cross the C ABI, results are written into caller-provided or
+freshly allocated bf16 tensors (the caching allocator makes the latter free
+inside captured CUDA graphs). No computation happens in Python.
+"""
 from __future__ import annotations
 
-from .. import _native as N
+import ctypes as C
 
-SIGNATURES: dict = {}
+import torch
+
+from .. import _native as N
+from ..errors import ShapeError, check
+
+_VP, _I32, _I64, _F32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+
+HP_A_PLAIN, HP_A_CONV3X3, HP_A_CONV3X3_S2 = 0, 1, 2
+ACT_NONE, ACT_GELU, ACT_SILU, ACT_GEGLU = 0, 1, 2, 3
+
+
+class HpGemmDesc(C.Structure):
+    _fields_ = [
+        ("a", _VP), ("lda", _I64), ("a_mode", _I32),
+        ("img_n", _I32), ("img_h", _I32), ("img_w", _I32), ("img_c", _I32),
+        ("b", _VP), ("ldb", _I64),
+        ("d", _VP), ("ldd", _I64),
+        ("M", _I64), ("N", _I64), ("K", _I64),
+        ("bias", _VP),
+        ("bias2", _VP), ("bias2_div", _I64),
+        ("residual", _VP), ("ldr", _I64),
+        ("act", _I32), ("block_n", _I32), ("alpha", _F32),
+    ]
+
+
+class HpAttnDesc(C.Structure):
+    _fields_ = [
+        ("q", _VP), ("ldq", _I64), ("q_col0", _I64),
+        ("k", _VP), ("ldk", _I64), ("k_col0", _I64),
+        ("v", _VP), ("ldv", _I64), ("v_col0", _I64),
+        ("o", _VP), ("ldo", _I64),
+        ("batch", _I32), ("heads", _I32), ("sq", _I32), ("skv", _I32),
+        ("scale", _F32),
+    ]
+
+
+SIGNATURES = {
+    "hp_gemm": (C.c_int, [C.POINTER(HpGemmDesc), _VP]),
+    "hp_gemm_pick_block_n": (_I32, [_I64, _I64, _I32]),
+    "hp_attention": (C.c_int, [C.POINTER(HpAttnDesc), _VP]),
+    "hp_group_norm": (C.c_int, [_VP, _I32, _VP, _I32, _I32, _I64, _I32, _F32, _VP, _VP, _I32, _VP, _VP, _VP]),
+    "hp_layer_norm": (C.c_int, [_VP, _I64, _I32, _F32, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
+    "hp_silu": (C.c_int, [_VP, _VP, _I64, _VP]),
+    "hp_upsample2x": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP]),
+    "hp_concat_channels": (C.c_int, [_VP, _I32, _VP, _I32, _I64, _VP, _VP]),
+    "hp_conv3x3_small": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP, _I32, _VP, _I32, _VP]),
+    "hp_timestep_embedding": (C.c_int, [_VP, _I32, _I32, _F32, _VP, _VP]),
+    "hp_linear_small": (C.c_int, [_VP, _I32, _I32, _VP, _VP, _I32, _I32, _I32, _VP, _VP]),
+    "hp_patchify": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _I32, _I32, _VP, _VP]),
+    "hp_add_rows": (C.c_int, [_VP, _VP, _I64, _I64, _I32, _VP, _VP]),
+    "hp_gated_residual": (C.c_int, [_VP, _VP, _VP, _I64, _I64, _I32, _I64, _VP]),
+    "hp_cast_bf16_f32": (C.c_int, [_VP, _VP, _I64, _VP]),
+}
 N.register_signatures(SIGNATURES)
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _s():
+    return C.c_void_p(N.stream_ptr())
+
+
+def _bf16(t, name):
+    if t.dtype != torch.bfloat16 or not t.is_cuda:
+        raise ShapeError(f"{name} must be a bf16 CUDA tensor, got {t.dtype} on {t.device}")
+
+
+def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, act=ACT_NONE,
+         alpha=1.0, block_n=0, conv=None):
+    """out[M, N'] = epi(alpha * A @ W^T). ``conv=(n, h, w, c, stride)`` reads A as NHWC."""
+    lib = N.load()
+    _bf16(a, "A")
+    _bf16(w, "W")
+    Nn, K = w.shape
+    d = HpGemmDesc()
+    d.a = _p(a)
+    if conv is None:
+        M = a.numel() // a.shape[-1]
+        if a.shape[-1] != K:
+            raise ShapeError(f"gemm K mismatch: A {tuple(a.shape)} vs W {tuple(w.shape)}")
+        d.lda = a.stride(-2) if a.dim() >= 2 else K
+        d.a_mode = HP_A_PLAIN
+    else:
+        n, h, wd, c, stride = conv
+        if K != 9 * c:
+            raise ShapeError(f"conv weight K={K} != 9*{c}")
+        M = n * (h // stride) * (wd // stride)
+        d.lda = c
+        d.a_mode = HP_A_CONV3X3 if stride == 1 else HP_A_CONV3X3_S2
+        d.img_n, d.img_h, d.img_w, d.img_c = n, h, wd, c
+    n_out = Nn // 2 if act == ACT_GEGLU else Nn
+    if out is None:
+        out = torch.empty((M, n_out), dtype=torch.bfloat16, device=a.device)
+    d.b, d.ldb = _p(w), w.stride(0)
+    d.d, d.ldd = _p(out), out.stride(-2) if out.dim() >= 2 else n_out
+    d.M, d.N, d.K = M, Nn, K
+    d.bias = _p(bias)
+    d.bias2, d.bias2_div = _p(bias2), int(bias2_div)
+    d.residual = _p(residual)
+    d.ldr = residual.stride(-2) if residual is not None else 0
+    d.act, d.block_n, d.alpha = int(act), int(block_n), float(alpha)
+    check(lib.hp_gemm(C.byref(d), _s()), f"hp_gemm M={M} N={Nn} K={K}")
+    return out
+
+
+def attention(q, k, v, out, *, batch, heads, sq, skv, scale, q_col0=0, k_col0=0, v_col0=0):
+    """Multi-head attention, head_dim 64; q/k/v/out are 2-D [batch*rows, ld] views."""
+    lib = N.load()
+    d = HpAttnDesc()
+    d.q, d.ldq, d.q_col0 = _p(q), q.stride(0), q_col0
+    d.k, d.ldk, d.k_col0 = _p(k), k.stride(0), k_col0
+    d.v, d.ldv, d.v_col0 = _p(v), v.stride(0), v_col0
+    d.o, d.ldo = _p(out), out.stride(0)
+    d.batch, d.heads, d.sq, d.skv, d.scale = batch, heads, sq, skv, float(scale)
+    check(lib.hp_attention(C.byref(d), _s()), "hp_attention")
+    return out
+
+
+def group_norm(x, n, hw, c, gamma, beta, *, groups=32, eps=1e-5, silu=False, x2=None, c2=0, out=None,
+               stats=None):
+    lib = N.load()
+    C_ = c + (c2 if x2 is not None else 0)
+    if out is None:
+        out = torch.empty((n * hw, C_), dtype=torch.bfloat16, device=x.device)
+    if stats is None:
+        stats = torch.empty(2 * n * groups * 64, dtype=torch.float32, device=x.device)
+    check(lib.hp_group_norm(_p(x), c, _p(x2), c2, n, hw, groups, eps, _p(gamma), _p(beta), int(silu),
+                            _p(out), _p(stats), _s()), "hp_group_norm")
+    return out
+
+
+def layer_norm(x, c, *, eps=1e-6, gamma=None, beta=None, shift=None, scale=None, ldm=0, rows_per_batch=0,
+               out=None):
+    lib = N.load()
+    rows = x.numel() // c
+    if out is None:
+        out = torch.empty((rows, c), dtype=torch.bfloat16, device=x.device)
+    check(lib.hp_layer_norm(_p(x), rows, c, eps, _p(gamma), _p(beta), _p(shift), _p(scale), int(ldm),
+                            int(rows_per_batch), _p(out), _s()), "hp_layer_norm")
+    return out
+
+
+def silu(x, out=None):
+    lib = N.load()
+    out = torch.empty_like(x) if out is None else out
+    check(lib.hp_silu(_p(x), _p(out), x.numel(), _s()), "hp_silu")
+    return out
+
+
+def upsample2x(x, n, h, w, c):
+    lib = N.load()
+    out = torch.empty((n * 4 * h * w, c), dtype=torch.bfloat16, device=x.device)
+    check(lib.hp_upsample2x(_p(x), n, h, w, c, _p(out), _s()), "hp_upsample2x")
+    return out
+
+
+def concat_channels(a, c1, b, c2, pixels):
+    lib = N.load()
+    out = torch.empty((pixels, c1 + c2), dtype=torch.bfloat16, device=a.device)
+    check(lib.hp_concat_channels(_p(a), c1, _p(b), c2, pixels, _p(out), _s()), "hp_concat_channels")
+    return out
+
+
+def conv3x3_small(x, n, h, w, cin, wgt, bias, cout, *, out=None, out_f32=False):
+    lib = N.load()
+    if out is None:
+        out = torch.empty((n * h * w, cout), dtype=torch.float32 if out_f32 else torch.bfloat16,
+                          device=x.device)
+    check(lib.hp_conv3x3_small(_p(x), n, h, w, cin, _p(wgt), _p(bias), cout, _p(out), int(out_f32), _s()),
+          "hp_conv3x3_small")
+    return out
+
+
+def timestep_embedding(t, dim, max_period=10000.0):
+    lib = N.load()
+    out = torch.empty((t.numel(), dim), dtype=torch.float32, device=t.device)
+    check(lib.hp_timestep_embedding(_p(t), t.numel(), dim, float(max_period), _p(out), _s()),
+          "hp_timestep_embedding")
+    return out
+
+
+def linear_small(x, w, bias=None, *, act_in=ACT_NONE, act_out=ACT_NONE, out=None):
+    lib = N.load()
+    M, K = x.shape
+    Nn = w.shape[0]
+    if out is None:
+        out = torch.empty((M, Nn), dtype=torch.float32, device=x.device)
+    check(lib.hp_linear_small(_p(x), M, K, _p(w), _p(bias), Nn, act_in, act_out, _p(out), _s()),
+          "hp_linear_small")
+    return out
+
+
+def patchify(x, n, h, w, c, p, inverse=False, out=None):
+    lib = N.load()
+    if out is None:
+        out = torch.empty(n * h * w * c, dtype=torch.bfloat16, device=x.device)
+    check(lib.hp_patchify(_p(x), n, h, w, c, p, int(inverse), _p(out), _s()), "hp_patchify")
+    return out
+
+
+def add_rows(x, add, c, out=None):
+    lib = N.load()
+    rows = x.numel() // c
+    out = torch.empty_like(x) if out is None else out
+    check(lib.hp_add_rows(_p(x), _p(add), rows, add.numel() // c, c, _p(out), _s()), "hp_add_rows")
+    return out
+
+
+def gated_residual(x, y, gate, ldg, c, rows_per_batch):
+    lib = N.load()
+    check(lib.hp_gated_residual(_p(x), _p(y), _p(gate), ldg, x.numel() // c, c, rows_per_batch, _s()),
+          "hp_gated_residual")
+    return x
+
+
+def cast_bf16_f32(x, out):
+    lib = N.load()
+    check(lib.hp_cast_bf16_f32(_p(x), _p(out), x.numel(), _s()), "hp_cast_bf16_f32")
+    return out

@@ -1,0 +1,185 @@
+"""GPU: denoiser kernels (tcgen05 GEMM / conv, attention, norms) vs plain torch fp32.
+
+Tolerances: outputs are bf16, so each check is max-abs error <= tol * max|ref|
+with tol = 1e-2 (one bf16 ulp is 2^-8 = 3.9e-3 relative) unless stated.
+"""
+import math
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2602_21760_b200.denoiser import kernels as K
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+
+
+def close(out, ref, tol=TOL):
+    out = out.float()
+    err = (out - ref).abs().max().item()
+    scale = ref.abs().max().item() + 1e-6
+    assert err <= tol * scale, f"max err {err:.4g} vs scale {scale:.4g} ({err / scale:.3g})"
+
+
+def rnd(*shape, s=1.0):
+    return (torch.randn(*shape, device="cuda") * s).bfloat16()
+
+
+@pytest.mark.parametrize("M,N,Kd,bn", [(128, 64, 64, 0), (256, 256, 128, 0), (2048, 1280, 1280, 0),
+                                       (154, 640, 2048, 0), (8192, 320, 640, 0), (300, 128, 72, 0),
+                                       (1024, 512, 256, 64), (1024, 512, 256, 128), (1024, 512, 256, 256),
+                                       (640, 320, 320, 160)])
+def test_gemm_plain(M, N, Kd, bn):
+    torch.manual_seed(M + N + Kd)
+    a, w = rnd(M, Kd), rnd(N, Kd, s=Kd ** -0.5)
+    bias = torch.randn(N, device="cuda")
+    out = K.gemm(a, w, bias=bias, block_n=bn)
+    ref = a.float() @ w.float().t() + bias
+    close(out, ref)
+
+
+def test_gemm_epilogues():
+    torch.manual_seed(1)
+    M, N, Kd = 512, 256, 320
+    a, w = rnd(M, Kd), rnd(N, Kd, s=Kd ** -0.5)
+    bias = torch.randn(N, device="cuda")
+    res = rnd(M, N)
+    b2 = torch.randn(2, N, device="cuda")
+    close(K.gemm(a, w, bias=bias, act=K.ACT_GELU), F.gelu(a.float() @ w.float().t() + bias))
+    close(K.gemm(a, w, bias=bias, act=K.ACT_SILU), F.silu(a.float() @ w.float().t() + bias))
+    close(K.gemm(a, w, bias=bias, residual=res), a.float() @ w.float().t() + bias + res.float())
+    close(K.gemm(a, w, bias=bias, bias2=b2, bias2_div=M // 2),
+          a.float() @ w.float().t() + bias + b2.repeat_interleave(M // 2, 0))
+    close(K.gemm(a, w, alpha=0.5), 0.5 * (a.float() @ w.float().t()))
+
+
+@pytest.mark.parametrize("bn", [128, 256])
+def test_gemm_geglu(bn):
+    torch.manual_seed(2)
+    M, F_, Kd = 256, 512, 320
+    a = rnd(M, Kd)
+    w = rnd(2 * F_, Kd, s=Kd ** -0.5)
+    bias = torch.randn(2 * F_, device="cuda")
+    # interleave: each tile of bn rows = bn/2 "a" rows followed by the matching bn/2 gate rows
+    h = bn // 2
+    idx = torch.cat([torch.cat([torch.arange(i, i + h), torch.arange(F_ + i, F_ + i + h)])
+                     for i in range(0, F_, h)]).cuda()
+    out = K.gemm(a, w[idx].contiguous(), bias=bias[idx].contiguous(), act=K.ACT_GEGLU, block_n=bn)
+    full = a.float() @ w.float().t() + bias
+    ref = full[:, :F_] * F.gelu(full[:, F_:])
+    close(out, ref)
+
+
+@pytest.mark.parametrize("n,h,w,c,co,stride", [(2, 32, 32, 64, 128, 1), (1, 128, 128, 64, 64, 1),
+                                               (2, 64, 64, 128, 256, 1), (1, 256, 256, 64, 64, 1),
+                                               (2, 64, 64, 64, 64, 2), (2, 128, 128, 64, 128, 2),
+                                               (1, 16, 16, 192, 320, 1)])
+def test_conv3x3_implicit_gemm(n, h, w, c, co, stride):
+    torch.manual_seed(h + c)
+    x = rnd(n, h, w, c)
+    wt = rnd(co, c, 3, 3, s=(9 * c) ** -0.5)
+    bias = torch.randn(co, device="cuda")
+    wk = wt.permute(0, 2, 3, 1).reshape(co, 9 * c).contiguous()
+    out = K.gemm(x, wk, bias=bias, conv=(n, h, w, c, stride))
+    ref = F.conv2d(x.float().permute(0, 3, 1, 2), wt.float(), bias, stride=stride, padding=1)
+    close(out.view(n, h // stride, w // stride, co), ref.permute(0, 2, 3, 1))
+
+
+@pytest.mark.parametrize("B,H,sq,skv", [(1, 1, 128, 128), (2, 3, 256, 256), (2, 2, 333, 333),
+                                        (2, 4, 256, 77), (1, 2, 1024, 1024), (2, 1, 130, 500)])
+def test_attention(B, H, sq, skv):
+    torch.manual_seed(sq + skv)
+    q = rnd(B * sq, H * 64)
+    k = rnd(B * skv, H * 64)
+    v = rnd(B * skv, H * 64)
+    o = torch.empty_like(q)
+    K.attention(q, k, v, o, batch=B, heads=H, sq=sq, skv=skv, scale=1 / 8)
+    qf = q.float().view(B, sq, H, 64).transpose(1, 2)
+    kf = k.float().view(B, skv, H, 64).transpose(1, 2)
+    vf = v.float().view(B, skv, H, 64).transpose(1, 2)
+    ref = F.scaled_dot_product_attention(qf, kf, vf, scale=1 / 8).transpose(1, 2).reshape(B * sq, H * 64)
+    close(o, ref, tol=2e-2)
+
+
+def test_attention_fused_qkv_columns():
+    B, S, H = 2, 256, 2
+    qkv = rnd(B * S, 3 * H * 64)
+    o = torch.empty(B * S, H * 64, dtype=torch.bfloat16, device="cuda")
+    K.attention(qkv, qkv, qkv, o, batch=B, heads=H, sq=S, skv=S, scale=0.125, q_col0=0, k_col0=H * 64,
+                v_col0=2 * H * 64)
+    q, k, v = qkv.float().view(B, S, 3, H, 64).unbind(2)
+    ref = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), scale=0.125)
+    close(o, ref.transpose(1, 2).reshape(B * S, H * 64), tol=2e-2)
+
+
+@pytest.mark.parametrize("n,hw,c,c2,silu", [(2, 4096, 320, 0, True), (2, 1024, 1280, 640, False),
+                                            (1, 256, 960, 0, True)])
+def test_group_norm(n, hw, c, c2, silu):
+    x = rnd(n * hw, c, s=2.0) + 0.5
+    x2 = rnd(n * hw, c2) if c2 else None
+    C = c + c2
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda")
+    out = K.group_norm(x, n, hw, c, g, b, silu=silu, x2=x2, c2=c2)
+    full = x.float() if x2 is None else torch.cat([x.float(), x2.float()], 1)
+    ref = F.group_norm(full.view(n, hw, C).permute(0, 2, 1), 32, g, b, eps=1e-5).permute(0, 2, 1).reshape(n * hw, C)
+    if silu:
+        ref = F.silu(ref)
+    close(out, ref)
+
+
+def test_group_norm_batch_invariant():
+    x = rnd(2 * 1024, 640)
+    g, b = torch.ones(640, device="cuda"), torch.zeros(640, device="cuda")
+    both = K.group_norm(x, 2, 1024, 640, g, b)
+    one = K.group_norm(x[1024:].contiguous(), 1, 1024, 640, g, b)
+    assert torch.equal(both[1024:], one)
+
+
+@pytest.mark.parametrize("c", [640, 1280, 1536])
+def test_layer_norm(c):
+    x = rnd(700, c) + 1.0
+    g, b = torch.randn(c, device="cuda"), torch.randn(c, device="cuda")
+    close(K.layer_norm(x, c, gamma=g, beta=b, eps=1e-5), F.layer_norm(x.float(), (c,), g, b, eps=1e-5))
+    sh, sc = rnd(2, c), rnd(2, c)
+    out = K.layer_norm(x[:600], c, shift=sh, scale=sc, ldm=c, rows_per_batch=300)
+    ref = F.layer_norm(x[:600].float(), (c,), eps=1e-6)
+    ref = ref * (1 + sc.float().repeat_interleave(300, 0)) + sh.float().repeat_interleave(300, 0)
+    close(out, ref)
+
+
+def test_small_ops():
+    n, h, w = 2, 16, 16
+    x4 = rnd(n, h, w, 4)
+    wt = torch.randn(320, 4, 3, 3, device="cuda") * 0.3
+    bias = torch.randn(320, device="cuda")
+    out = K.conv3x3_small(x4, n, h, w, 4, wt.permute(0, 2, 3, 1).contiguous(), bias, 320)
+    ref = F.conv2d(x4.float().permute(0, 3, 1, 2), wt, bias, padding=1).permute(0, 2, 3, 1)
+    close(out.view(n, h, w, 320), ref)
+    x320 = rnd(n, h, w, 320)
+    wo = torch.randn(4, 320, 3, 3, device="cuda") * 0.05
+    bo = torch.randn(4, device="cuda")
+    out = K.conv3x3_small(x320, n, h, w, 320, wo.permute(0, 2, 3, 1).contiguous(), bo, 4)
+    ref = F.conv2d(x320.float().permute(0, 3, 1, 2), wo, bo, padding=1).permute(0, 2, 3, 1)
+    close(out.view(n, h, w, 4), ref)
+    up = K.upsample2x(x320, n, h, w, 320)
+    assert torch.equal(up.view(n, 2 * h, 2 * w, 320),
+                       x320.repeat_interleave(2, 1).repeat_interleave(2, 2))
+    cat = K.concat_channels(x320.view(-1, 320), 320, x4.view(-1, 4).repeat(1, 2), 8, n * h * w)
+    assert torch.equal(cat[:, :320], x320.view(-1, 320))
+    t = torch.tensor([999.0, 1.0], device="cuda")
+    emb = K.timestep_embedding(t, 320)
+    half = 160
+    fr = torch.exp(-math.log(10000.0) * torch.arange(half, device="cuda") / half)
+    ref = torch.cat([torch.cos(t[:, None] * fr), torch.sin(t[:, None] * fr)], 1)
+    assert (emb - ref).abs().max().item() < 2e-3
+    xs = torch.randn(2, 320, device="cuda")
+    ws = rnd(1280, 320, s=0.05)
+    bs = torch.randn(1280, device="cuda")
+    ys = K.linear_small(xs, ws, bs, act_in=K.ACT_SILU)
+    assert (ys - (F.silu(xs) @ ws.float().t() + bs)).abs().max().item() < 1e-3
+    lat = rnd(2, 8, 8, 16)
+    tok = K.patchify(lat, 2, 8, 8, 16, 2)
+    ref = lat.view(2, 4, 2, 4, 2, 16).permute(0, 1, 3, 2, 4, 5).reshape(-1)
+    assert torch.equal(tok, ref)
+    assert torch.equal(K.patchify(tok, 2, 8, 8, 16, 2, inverse=True), lat.reshape(-1))
