@@ -1,0 +1,116 @@
+"""Seam adapter: a neural denoiser as the engine's branch evaluator.
+
+Replaces the reference's per-condition-group ``eps_prediction`` fan-out
+(engine.py:164-184) for neural networks:
+
+* ``branches(x, t)`` runs ONE batched forward over [uncond rows; cond rows]
+  (classifier-free guidance batched on one GPU; the rows are independent, so
+  the result is bit-identical to two separate forwards) and returns
+  (eps_c, eps_u) as views of the graph's static output;
+* ``conditional(x, t)`` runs the conditional rows only (pipelined window).
+
+Each distinct batch layout is captured once into a CUDA graph; a step is then
+``t`` upload + graph replay. The fused sampler kernel writes the next bf16
+latent straight into the graph's static input (``input_slot``), so no copy
+sits between two steps.
+"""
+from __future__ import annotations
+
+import torch
+
+from .. import _native as N
+
+
+def net_timestep(t: int, T: int) -> float:
+    return float(round(t * 1000 / T) - 1)
+
+
+class _Graphed:
+    def __init__(self, fn, x_static, t_static, use_graph: bool):
+        self.fn, self.x, self.t = fn, x_static, t_static
+        self.graph = None
+        self.out = None
+        self.use_graph = use_graph
+
+    def run(self):
+        if self.graph is not None:
+            self.graph.replay()
+            return self.out
+        if not self.use_graph:
+            self.out = self.fn(self.x, self.t)
+            return self.out
+        # warm-up eagerly (kernel attributes, TMA encoder, allocator), then capture
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.fn(self.x, self.t)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.out = self.fn(self.x, self.t)
+        self.graph = g
+        g.replay()
+        return self.out
+
+
+class NetDenoiser:
+    """Neural branch evaluator behind the seam (UNet or MMDiT)."""
+
+    latent_dtype = torch.float32
+    eps_dtype = torch.bfloat16
+    wants_bf16_input = True
+
+    def __init__(self, net, conditioning, conditions, schedule, latent_shape, use_graph=True):
+        N.require_cuda()
+        self.net, self.sched = net, schedule
+        self.shape = tuple(latent_shape)             # (H, W, C) NHWC per image
+        self.numel = self.shape[0] * self.shape[1] * self.shape[2]
+        self.B = len(conditions)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        prompts = [c.indices[0] for c in conditions]
+        ctx_c = conditioning.context[prompts]
+        pool_c = conditioning.pooled[prompts]
+        ctx_u = conditioning.null_context.expand(self.B, -1, -1)
+        pool_u = conditioning.null_pooled.expand(self.B, -1)
+        net.prepare(torch.cat([ctx_u, ctx_c]).to(dev), torch.cat([pool_u, pool_c]).to(dev), key="both")
+        net.prepare(ctx_c.to(dev), pool_c.to(dev), key="cond")
+        B2 = 2 * self.B
+        self.x_both = torch.zeros((B2,) + self.shape, dtype=torch.bfloat16, device=dev)
+        self.t_both = torch.zeros(B2, dtype=torch.float32, device=dev)
+        self.x_cond = torch.zeros((self.B,) + self.shape, dtype=torch.bfloat16, device=dev)
+        self.t_cond = torch.zeros(self.B, dtype=torch.float32, device=dev)
+        half = self.x_both[: self.B]
+
+        def both(x, t):
+            x[self.B:].copy_(x[: self.B])
+            return net.forward(x, t, key="both")
+
+        def cond(x, t):
+            return net.forward(x, t, key="cond")
+
+        self.g_both = _Graphed(both, self.x_both, self.t_both, use_graph)
+        self.g_cond = _Graphed(cond, self.x_cond, self.t_cond, use_graph)
+        self._slot = half.view(self.B, self.numel)
+
+    def input_slot(self):
+        """bf16 [B, N] buffer the sampler kernel writes the next latent into."""
+        return self._slot
+
+    def load_input(self, x: torch.Tensor) -> None:
+        self._slot.copy_(x.to(torch.bfloat16).view(self.B, self.numel))
+
+    def _set_t(self, buf, t):
+        buf.fill_(net_timestep(t, self.sched.T))
+
+    def branches(self, x, t, x_bf16=None):
+        if x_bf16 is None or x_bf16.data_ptr() != self._slot.data_ptr():
+            self.load_input(x)
+        self._set_t(self.t_both, t)
+        out = self.g_both.run().reshape(2 * self.B, self.numel)
+        return out[self.B:], out[: self.B]            # eps_c, eps_u
+
+    def conditional(self, x, t, x_bf16=None):
+        self.x_cond.view(self.B, self.numel).copy_(x.to(torch.bfloat16).view(self.B, self.numel))
+        self._set_t(self.t_cond, t)
+        return self.g_cond.run().reshape(self.B, self.numel)

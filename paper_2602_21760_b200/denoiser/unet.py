@@ -1,0 +1,317 @@
+"""SDXL-shaped U-Net on the package's sm_100a kernels (the denoiser seam).
+
+Activations are bf16 NHWC (pixels x channels, row-major), weights bf16 in the
+kernels' layouts, accumulation fp32 in TMEM. Every op is one of our kernels:
+
+  ResBlock      GN+SiLU -> conv3x3 (implicit GEMM; epilogue: bias + per-image
+                time-embedding bias) -> GN+SiLU -> conv3x3 (epilogue: bias +
+                residual = identity or 1x1-conv shortcut)
+  Transformer   GN -> proj_in GEMM -> [LN -> fused QKV GEMM -> attention ->
+                out GEMM(+residual) -> LN -> Q GEMM -> cross-attention over
+                per-run cached K/V -> out GEMM(+residual) -> LN -> GEGLU GEMM
+                (gate fused in the epilogue) -> GEMM(+residual)] -> proj_out
+                GEMM(+residual)
+  Down / Up     stride-2 conv3x3 via TMA element strides / nearest 2x + conv3x3
+
+Step-invariant work (text-time embedding, cross-attention K/V of the fixed
+prompt context) is computed once per run in ``prepare``; ``forward`` is pure
+kernel launches on fixed buffers, so it is captured in a CUDA graph.
+Batch-invariant by construction (per-row GEMM tiles, per-image norms,
+per-(image, head) attention): image b's output never depends on the other
+rows of the batch, which makes serial (batched CFG), condition-partitioned
+and empty-window hybrid runs bit-identical.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import kernels as K
+from .weights import UNetSpec, unet_param_specs, unet_skip_channels
+
+
+def _bf(t):
+    return t.to(torch.bfloat16).contiguous()
+
+
+def _f32(t):
+    return t.to(torch.float32).contiguous()
+
+
+class _Lin:
+    def __init__(self, W, name, bias=True, dev="cuda"):
+        self.w = _bf(W[name + ".weight"].to(dev))
+        self.b = _f32(W[name + ".bias"].to(dev)) if bias and (name + ".bias") in W else None
+
+    def __call__(self, x, **kw):
+        return K.gemm(x, self.w, bias=self.b, **kw)
+
+
+class _Conv:
+    def __init__(self, W, name, dev="cuda"):
+        w = W[name + ".weight"].to(dev)
+        co, ci, kh, kw = w.shape
+        self.co, self.ci, self.k = co, ci, kh
+        self.w = _bf(w.permute(0, 2, 3, 1).reshape(co, kh * kw * ci))
+        self.b = _f32(W[name + ".bias"].to(dev))
+
+    def __call__(self, x, n, h, w, stride=1, **kw):
+        if self.k == 1:
+            return K.gemm(x, self.w, bias=self.b, **kw)
+        return K.gemm(x, self.w, bias=self.b, conv=(n, h, w, self.ci, stride), **kw)
+
+
+class _Norm:
+    def __init__(self, W, name, dev="cuda"):
+        self.g = _f32(W[name + ".weight"].to(dev))
+        self.b = _f32(W[name + ".bias"].to(dev))
+
+
+class _ResBlock:
+    def __init__(self, W, name, temb_dim, dev):
+        self.n1, self.n2 = _Norm(W, name + ".norm1", dev), _Norm(W, name + ".norm2", dev)
+        self.c1, self.c2 = _Conv(W, name + ".conv1", dev), _Conv(W, name + ".conv2", dev)
+        self.tproj = _Lin(W, name + ".time_emb_proj", dev=dev)
+        self.short = _Conv(W, name + ".conv_shortcut", dev) if (name + ".conv_shortcut.weight") in W else None
+
+    def __call__(self, x, n, h, w, temb, groups, stats):
+        ci, co = self.c1.ci, self.c1.co
+        hw = h * w
+        tb = K.linear_small(temb, self.tproj.w, self.tproj.b, act_in=K.ACT_SILU)   # [n, co]
+        y = K.group_norm(x, n, hw, ci, self.n1.g, self.n1.b, groups=groups, silu=True, stats=stats)
+        y = self.c1(y, n, h, w, bias2=tb, bias2_div=hw)
+        y = K.group_norm(y, n, hw, co, self.n2.g, self.n2.b, groups=groups, silu=True, stats=stats)
+        res = self.short(x, n, h, w) if self.short is not None else x
+        return self.c2(y, n, h, w, residual=res)
+
+
+class _Block:
+    def __init__(self, W, name, c, heads, dev):
+        self.c, self.heads = c, heads
+        self.n1, self.n2, self.n3 = (_Norm(W, f"{name}.norm{i}", dev) for i in (1, 2, 3))
+        a1 = f"{name}.attn1"
+        self.qkv = _bf(torch.cat([W[f"{a1}.to_q.weight"], W[f"{a1}.to_k.weight"], W[f"{a1}.to_v.weight"]]).to(dev))
+        self.o1 = _Lin(W, f"{a1}.to_out.0", dev=dev)
+        a2 = f"{name}.attn2"
+        self.q2 = _bf(W[f"{a2}.to_q.weight"].to(dev))
+        self.kv2 = _bf(torch.cat([W[f"{a2}.to_k.weight"], W[f"{a2}.to_v.weight"]]).to(dev))
+        self.o2 = _Lin(W, f"{a2}.to_out.0", dev=dev)
+        # GEGLU: interleave hidden/gate rows per 256-wide output tile (128 + 128)
+        pw, pb = W[f"{name}.ff.net.0.proj.weight"].to(dev), W[f"{name}.ff.net.0.proj.bias"].to(dev)
+        F_ = pw.shape[0] // 2
+        half = 128
+        idx = torch.cat([torch.cat([torch.arange(i, i + half), torch.arange(F_ + i, F_ + i + half)])
+                         for i in range(0, F_, half)]).to(dev)
+        self.ff1_w, self.ff1_b = _bf(pw[idx]), _f32(pb[idx])
+        self.ff2 = _Lin(W, f"{name}.ff.net.2", dev=dev)
+        self.kv_cache = {}
+
+    def prepare(self, ctx2d, key):
+        self.kv_cache[key] = K.gemm(ctx2d, self.kv2)        # [rows*L, 2C]
+
+    def __call__(self, h, n, S, ctx_len, key):
+        c = self.c
+        scale = 1.0 / math.sqrt(64)
+        y = K.layer_norm(h, c, gamma=self.n1.g, beta=self.n1.b, eps=1e-5)
+        qkv = K.gemm(y, self.qkv)
+        att = torch.empty_like(y)
+        K.attention(qkv, qkv, qkv, att, batch=n, heads=self.heads, sq=S, skv=S, scale=scale,
+                    q_col0=0, k_col0=c, v_col0=2 * c)
+        h = self.o1(att, residual=h, out=h)
+        y = K.layer_norm(h, c, gamma=self.n2.g, beta=self.n2.b, eps=1e-5)
+        q = K.gemm(y, self.q2)
+        kv = self.kv_cache[key]
+        K.attention(q, kv, kv, att, batch=n, heads=self.heads, sq=S, skv=ctx_len, scale=scale,
+                    q_col0=0, k_col0=0, v_col0=c)
+        h = self.o2(att, residual=h, out=h)
+        y = K.layer_norm(h, c, gamma=self.n3.g, beta=self.n3.b, eps=1e-5)
+        f = K.gemm(y, self.ff1_w, bias=self.ff1_b, act=K.ACT_GEGLU, block_n=256)
+        return self.ff2(f, residual=h, out=h)
+
+
+class _Transformer:
+    def __init__(self, W, name, c, depth, head_dim, dev):
+        self.c = c
+        self.norm = _Norm(W, name + ".norm", dev)
+        self.pin, self.pout = _Lin(W, name + ".proj_in", dev=dev), _Lin(W, name + ".proj_out", dev=dev)
+        self.blocks = [_Block(W, f"{name}.transformer_blocks.{d}", c, c // head_dim, dev) for d in range(depth)]
+
+    def prepare(self, ctx2d, key):
+        for b in self.blocks:
+            b.prepare(ctx2d, key)
+
+    def __call__(self, x, n, hw, groups, stats, ctx_len, key):
+        y = K.group_norm(x, n, hw, self.c, self.norm.g, self.norm.b, groups=groups, eps=1e-6, stats=stats)
+        h = self.pin(y)
+        for b in self.blocks:
+            h = b(h, n, hw, ctx_len, key)
+        return self.pout(h, residual=x)
+
+
+class UNet:
+    """Random-init SDXL-shaped U-Net; ``forward`` maps bf16 NHWC latents to eps."""
+
+    def __init__(self, spec: UNetSpec, W: dict, device="cuda"):
+        self.spec = s = spec
+        dev = torch.device(device)
+        self.dev = dev
+        ch = s.block_out
+        self.conv_in_w = _f32(W["conv_in.weight"].to(dev).permute(0, 2, 3, 1))
+        self.conv_in_b = _f32(W["conv_in.bias"].to(dev))
+        self.t1, self.t2 = _Lin(W, "time_embedding.linear_1", dev=dev), _Lin(W, "time_embedding.linear_2", dev=dev)
+        self.a1, self.a2 = _Lin(W, "add_embedding.linear_1", dev=dev), _Lin(W, "add_embedding.linear_2", dev=dev)
+        self.down = []
+        for lvl, co in enumerate(ch):
+            res = [_ResBlock(W, f"down_blocks.{lvl}.resnets.{j}", s.temb_dim, dev) for j in range(s.layers_per_block)]
+            att = [(_Transformer(W, f"down_blocks.{lvl}.attentions.{j}", co, s.transformer_depth[lvl], s.head_dim, dev)
+                    if s.transformer_depth[lvl] else None) for j in range(s.layers_per_block)]
+            ds = _Conv(W, f"down_blocks.{lvl}.downsamplers.0.conv", dev) if lvl < len(ch) - 1 else None
+            self.down.append((res, att, ds))
+        self.mid = (_ResBlock(W, "mid_block.resnets.0", s.temb_dim, dev),
+                    _Transformer(W, "mid_block.attentions.0", ch[-1], s.mid_depth, s.head_dim, dev),
+                    _ResBlock(W, "mid_block.resnets.1", s.temb_dim, dev))
+        self.up = []
+        for u in range(len(ch)):
+            lvl = len(ch) - 1 - u
+            co = ch[lvl]
+            res = [_ResBlock(W, f"up_blocks.{u}.resnets.{j}", s.temb_dim, dev) for j in range(s.layers_per_block + 1)]
+            att = [(_Transformer(W, f"up_blocks.{u}.attentions.{j}", co, s.transformer_depth[lvl], s.head_dim, dev)
+                    if s.transformer_depth[lvl] else None) for j in range(s.layers_per_block + 1)]
+            us = _Conv(W, f"up_blocks.{u}.upsamplers.0.conv", dev) if u < len(ch) - 1 else None
+            self.up.append((res, att, us))
+        self.norm_out = _Norm(W, "conv_norm_out", dev)
+        self.conv_out_w = _f32(W["conv_out.weight"].to(dev).permute(0, 2, 3, 1))
+        self.conv_out_b = _f32(W["conv_out.bias"].to(dev))
+        self.stats = torch.empty(2 * 64 * 64 * 32, dtype=torch.float32, device=dev)
+        self.aug = {}
+        self.ctx_len = s.context_len
+
+    def _transformers(self):
+        for res, att, _ in self.down + self.up:
+            for a in att:
+                if a is not None:
+                    yield a
+        yield self.mid[1]
+
+    def prepare(self, context: torch.Tensor, pooled: torch.Tensor, key="default"):
+        """Per-run, step-invariant work: text-time embedding and cross-attention K/V.
+
+        context [n, L, cross_dim], pooled [n, pooled_dim] (fp32 or bf16), one row per
+        image of the forward batch."""
+        s = self.spec
+        n = context.shape[0]
+        ctx2d = _bf(context.to(self.dev).reshape(n * s.context_len, s.cross_dim))
+        for t in self._transformers():
+            t.prepare(ctx2d, key)
+        # add_embedding(text_embeds ++ time_ids embedding); SDXL time ids for 1024^2
+        size = 8.0 * s.latent_hw
+        ids = torch.tensor([size, size, 0.0, 0.0, size, size], device=self.dev).repeat(n, 1)
+        tid = K.timestep_embedding(ids.reshape(-1).contiguous(), s.time_id_dim).reshape(n, -1)
+        add_in = torch.cat([_f32(pooled.to(self.dev)), tid], dim=1).contiguous()
+        a = K.linear_small(add_in, self.a1.w, self.a1.b, act_out=K.ACT_SILU)
+        self.aug[key] = K.linear_small(a, self.a2.w, self.a2.b)
+
+    def forward(self, x: torch.Tensor, t: torch.Tensor, key="default") -> torch.Tensor:
+        """x: [n, H, W, in_ch] bf16 NHWC; t: [n] fp32 timesteps -> eps [n, H, W, out_ch] bf16."""
+        s = self.spec
+        n, H, Wd = x.shape[0], x.shape[1], x.shape[2]
+        st, g = self.stats, s.groups
+        te = K.timestep_embedding(t, s.block_out[0])
+        te = K.linear_small(te, self.t1.w, self.t1.b, act_out=K.ACT_SILU)
+        temb = K.linear_small(te, self.t2.w, self.t2.b)
+        temb = temb + self.aug[key]                    # tiny [n, 1280] add
+        h = K.conv3x3_small(x, n, H, Wd, s.in_channels, self.conv_in_w, self.conv_in_b, s.block_out[0])
+        skips = [h]
+        hh, ww = H, Wd
+        for res, att, ds in self.down:
+            for r, a in zip(res, att):
+                h = r(h, n, hh, ww, temb, g, st)
+                if a is not None:
+                    h = a(h, n, hh * ww, g, st, self.ctx_len, key)
+                skips.append(h)
+            if ds is not None:
+                h = ds(h, n, hh, ww, stride=2)
+                hh, ww = hh // 2, ww // 2
+                skips.append(h)
+        r0, tr, r1 = self.mid
+        h = r0(h, n, hh, ww, temb, g, st)
+        h = tr(h, n, hh * ww, g, st, self.ctx_len, key)
+        h = r1(h, n, hh, ww, temb, g, st)
+        for res, att, us in self.up:
+            for r, a in zip(res, att):
+                sk = skips.pop()
+                cat = K.concat_channels(h, h.shape[1], sk, sk.shape[1], n * hh * ww)
+                h = r(cat, n, hh, ww, temb, g, st)
+                if a is not None:
+                    h = a(h, n, hh * ww, g, st, self.ctx_len, key)
+            if us is not None:
+                h = K.upsample2x(h, n, hh, ww, h.shape[1])
+                hh, ww = hh * 2, ww * 2
+                h = us(h, n, hh, ww)
+        y = K.group_norm(h, n, hh * ww, s.block_out[0], self.norm_out.g, self.norm_out.b, groups=g, silu=True, stats=st)
+        eps = K.conv3x3_small(y, n, hh, ww, s.block_out[0], self.conv_out_w, self.conv_out_b, s.out_channels)
+        return eps.view(n, hh, ww, s.out_channels)
+
+
+def build_unet(spec: UNetSpec, seed: int = 0, device="cuda", weights: dict | None = None) -> UNet:
+    if weights is None:
+        from .weights import init_weights
+        weights = init_weights(unet_param_specs(spec), seed=seed, device=device)
+    return UNet(spec, weights, device=device)
+
+
+def unet_flops(spec: UNetSpec, n: int) -> float:
+    """Analytic forward FLOPs (2*MACs of every GEMM/conv + 4*S*S*C attention) for n images."""
+    s = spec
+    ch = s.block_out
+    H = s.latent_hw
+    fl = 0.0
+    L = s.context_len
+
+    def conv(hw, ci, co, k=3):
+        return 2.0 * n * hw * ci * co * k * k
+
+    def res(hw, ci, co):
+        f = conv(hw, ci, co) + conv(hw, co, co)
+        if ci != co:
+            f += conv(hw, ci, co, 1)
+        return f
+
+    def tr(hw, c, depth):
+        f = 2 * 2.0 * n * hw * c * c                        # proj in/out
+        per = (2.0 * n * hw * c * 3 * c + 2.0 * n * hw * c * c      # qkv + out
+               + 4.0 * n * hw * hw * c                              # self attention
+               + 2.0 * n * hw * c * c * 2                           # q2 + out2
+               + 4.0 * n * hw * L * c                               # cross attention
+               + 2.0 * n * hw * c * 8 * c + 2.0 * n * hw * 4 * c * c)  # GEGLU + ff2
+        return f + depth * per
+
+    fl += 2.0 * n * H * H * s.in_channels * ch[0] * 9
+    hw = H * H
+    prev = ch[0]
+    for lvl, co in enumerate(ch):
+        for j in range(s.layers_per_block):
+            fl += res(hw, prev if j == 0 else co, co)
+            if s.transformer_depth[lvl]:
+                fl += tr(hw, co, s.transformer_depth[lvl])
+        prev = co
+        if lvl < len(ch) - 1:
+            fl += conv(hw // 4, co, co)
+            hw //= 4
+    fl += 2 * res(hw, ch[-1], ch[-1]) + tr(hw, ch[-1], s.mid_depth)
+    skips = unet_skip_channels(s)
+    prev = ch[-1]
+    for u in range(len(ch)):
+        lvl = len(ch) - 1 - u
+        co = ch[lvl]
+        for j in range(s.layers_per_block + 1):
+            fl += res(hw, prev + skips.pop(), co)
+            prev = co
+            if s.transformer_depth[lvl]:
+                fl += tr(hw, co, s.transformer_depth[lvl])
+        if u < len(ch) - 1:
+            hw *= 4
+            fl += conv(hw, co, co)
+    fl += 2.0 * n * H * H * ch[0] * s.out_channels * 9
+    return fl

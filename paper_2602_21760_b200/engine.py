@@ -197,6 +197,12 @@ class MixtureDenoiser:
         self.gm, self.sched, self.sampler = plan.mixture, plan.schedule, plan.sampler
         self.groups = [(c, torch.as_tensor(r)) for c, r in condition_groups(plan.conditions)]
 
+    def input_slot(self):
+        return None
+
+    def load_input(self, x):
+        return None
+
     def _one(self, cond, x, t):
         if self.sampler == "euler":
             return fm_velocity(self.gm, cond, x, t / self.sched.T)
@@ -239,15 +245,22 @@ class _StepRunner:
             self.coef = {t: StepCoefficients.ddim(plan.schedule, t) for t in range(1, T + 1)}
         self.update = N.HP_UPDATE_EULER if plan.sampler == "euler" else N.HP_UPDATE_DDIM
 
-    def upload(self, x_host: np.ndarray):
-        x = torch.from_numpy(np.ascontiguousarray(x_host)).to(self.dev, non_blocking=True)
+    def upload(self, x_host):
+        if isinstance(x_host, torch.Tensor):
+            x = x_host.to(self.dev, non_blocking=True)
+        else:
+            x = torch.from_numpy(np.ascontiguousarray(x_host)).to(self.dev, non_blocking=True)
         x = x.to(self.den.latent_dtype)
-        xb = x.to(torch.bfloat16) if self.den.wants_bf16_input else None
+        xb = None
+        if self.den.wants_bf16_input:
+            self.den.load_input(x)
+            xb = self.den.input_slot()
         return x, xb
 
     def _advance(self, x, xb, eps_c, eps_u, t, ctrl_op, discrepancy=True):
         out = torch.empty_like(x)
-        outb = torch.empty_like(xb) if xb is not None else None
+        # the next bf16 latent goes straight into the denoiser's (graph) input
+        outb = self.den.input_slot() if self.den.wants_bf16_input else None
         c = self.coef[t]
         kw = {}
         if c is not None:
@@ -268,8 +281,8 @@ class _StepRunner:
         x, xb = history[0]
         acc = None
         for d, f in enumerate(fractions):
-            hx, hxb = history[min(d, len(history) - 1)]
-            e = self.den.conditional(hx, t, hxb)
+            hx, _ = history[min(d, len(history) - 1)]
+            e = self.den.conditional(hx, t)
             if acc is None:
                 acc = torch.empty(e.shape, dtype=x.dtype, device=x.device)
             K.blend_accumulate(acc, e, f, first=(d == 0))

@@ -1,0 +1,114 @@
+"""GPU: the SDXL-shaped U-Net on our kernels, and full denoising runs through the
+drop-in engine, against the fp32 torch reference network and against the
+REFERENCE ENGINE run with the same network at its seam (golden fixtures from
+oracle/gen_golden_unet.py, BASELINE config 1).
+
+Tolerances (stated, bf16 compute / fp32 latent): one forward: max-abs <= 5e-2
+of max|eps_ref| and mean-abs <= 1e-2 of mean|eps_ref|; 20-step x0 vs the
+reference engine: max-abs <= 5e-2, mean-abs <= 1e-2 (latents are O(1)).
+Schedules (tau1, tau2, stage labels, series keys) must be identical.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_21760_b200 as hp
+from paper_2602_21760_b200 import pipelines
+from paper_2602_21760_b200.denoiser.unet import UNet
+from paper_2602_21760_b200.denoiser.weights import TINY, init_weights, synthetic_conditioning, unet_param_specs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    W = init_weights(unet_param_specs(TINY), seed=0, device="cpu")
+    cond = synthetic_conditioning(1, TINY.context_len, TINY.cross_dim, TINY.pooled_dim)
+    return W, cond
+
+
+def _ref_net(W):
+    from oracle.unet_ref import UNetRef
+    return UNetRef(TINY, {k: v.cuda() for k, v in W.items()})
+
+
+def test_forward_matches_fp32_reference(tiny):
+    W, cond = tiny
+    net = UNet(TINY, W)
+    n, Hh = 2, TINY.latent_hw
+    ctx = torch.cat([cond.null_context, cond.context]).cuda()
+    pooled = torch.cat([cond.null_pooled, cond.pooled]).cuda()
+    net.prepare(ctx, pooled, key="k")
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(n, Hh, Hh, 4, device="cuda", generator=g)
+    t = torch.tensor([981.0, 981.0], device="cuda")
+    eps = net.forward(x.bfloat16(), t, key="k").float()
+    ref = _ref_net(W)(x.permute(0, 3, 1, 2), t, ctx, pooled).permute(0, 2, 3, 1)
+    err = (eps - ref).abs()
+    assert err.max().item() <= 5e-2 * ref.abs().max().item()
+    assert err.mean().item() <= 1e-2 * ref.abs().mean().item()
+
+
+def test_batch_invariance_bitwise(tiny):
+    W, cond = tiny
+    net = UNet(TINY, W)
+    ctx = torch.cat([cond.null_context, cond.context]).cuda()
+    pooled = torch.cat([cond.null_pooled, cond.pooled]).cuda()
+    net.prepare(ctx, pooled, key="both")
+    net.prepare(ctx[1:], pooled[1:], key="one")
+    x = torch.randn(2, TINY.latent_hw, TINY.latent_hw, 4, device="cuda").bfloat16()
+    t = torch.tensor([500.0, 500.0], device="cuda")
+    both = net.forward(x, t, key="both")
+    one = net.forward(x[1:].contiguous(), t[1:].contiguous(), key="one")
+    assert torch.equal(both[1:], one)
+
+
+@pytest.fixture(scope="module")
+def golden(golden_dir):
+    with open(os.path.join(golden_dir, "unet_tiny.json")) as fh:
+        meta = json.load(fh)
+    return meta, np.load(os.path.join(golden_dir, "unet_tiny.npz"))
+
+
+@pytest.mark.parametrize("case", ["serial", "hybrid_cap", "hybrid_k0"])
+def test_engine_matches_reference_engine_with_seam(tiny, golden, case):
+    W, cond = tiny
+    meta, arrays = golden
+    c = meta["cases"][case]
+    den = pipelines.build_sdxl_denoiser(TINY, n_prompts=1, steps=meta["T"], weights=W, conditioning=cond)
+    plan = pipelines.sdxl_plan(TINY, variant=c["variant"], steps=meta["T"], seed=meta["seed"],
+                               guidance=meta["guidance"], denoiser=den, clock="model")
+    if "switch" in c:
+        from dataclasses import replace
+        plan = replace(plan, switch=hp.SwitchConfig(**c["switch"]))
+    res = hp.run_plan(plan)
+    assert (res.tau1, res.tau2) == (c["tau1"], c["tau2"])
+    assert [t for t, _ in res.series] == [t for t, _ in c["series"]]
+    ref = arrays[case]
+    err = np.abs(res.x0 - ref)
+    assert err.max() <= 5e-2, err.max()
+    assert err.mean() <= 1e-2, err.mean()
+    np.testing.assert_allclose([m for _, m in res.series], [m for _, m in c["series"]], rtol=2e-2)
+    # the switch schedule from the GPU-measured series equals the reference controller's
+    if "switch" in c:
+        st, labels = hp.replay_series([(t, m) for t, m in res.series], hp.SwitchConfig(**c["switch"])) \
+            if c["switch"]["k"] == 0 else (None, None)
+        if st is not None:
+            assert st.tau1 == res.tau1
+
+
+def test_serial_fcp_k0_bit_identical_on_gpu(tiny):
+    W, cond = tiny
+    den = pipelines.build_sdxl_denoiser(TINY, n_prompts=1, steps=20, weights=W, conditioning=cond)
+    outs = []
+    for variant, sw in (("serial", None), ("full_condition_partition", None),
+                        ("hybrid", dict(L=4, g_slope=1e-12, tau_cap=8, k=0))):
+        plan = pipelines.sdxl_plan(TINY, variant=variant, steps=20, seed=3, denoiser=den, clock="model")
+        if sw:
+            from dataclasses import replace
+            plan = replace(plan, switch=hp.SwitchConfig(**sw))
+        outs.append(hp.run_plan(plan).x0)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
