@@ -1,0 +1,368 @@
+"""Benchmark: SDXL 1024^2 50-step CFG latency (s/image) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One bench "step" is one complete 50-step classifier-free-guided generation of
+one 1024^2 image (128x128x4 latent) with a random-init SDXL-shaped U-Net
+(2.57 B parameters) on this package's sm_100a kernels, driven through the
+drop-in ``run_plan`` API. At N=1 the plan is ``serial`` (both guidance
+branches on one GPU, batched); at N>1 each GPU pair runs one image
+(``--mode pairs``, condition partitioning over NVLink) or every GPU runs its
+own image (``--mode replicas``, the default until the pair path has been
+validated on multi-GPU hardware).
+
+Printed JSON (rank 0, one line): ``value`` = device-resident seconds per image
+for the whole job (inputs resident, no host copies); ``e2e`` = the same metric
+through ``run_plan`` with host x_T in and host x0 out each run; ``roofline``
+= the denoiser forward (tensor-bound) against MEASURED_PEAKS.json;
+``sampler_roofline`` = the fused exchange+CFG+DDIM kernel (HBM-bound);
+``cpu_baseline`` = the oracle CPU path (fp32 torch U-Net + numpy sampler) on
+this host, bounded sample, extrapolated.
+
+``--impl reference`` times the reference's CPU implementation of the path
+(the oracle port: numpy fp64 sampler trio of schedules.py / monitor.py plus the
+fp32 torch network at the seam, all host threads) on the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SDXL 1024^2 50-step latency (s/image)"
+UNIT = "s/image"
+STEPS_T = 50
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([s.strip() for s in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _max_over_ranks(ws, v):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------------
+def cpu_reference_sample(spec, n_forwards: int = 1, threads: int | None = None, weights=None):
+    """Oracle CPU path on this host: fp32 torch U-Net forward (one branch, B=1) and
+    the numpy fp64 sampler trio at the latent size. Returns (s/image, details)."""
+    import torch
+    from oracle import sampler as osmp
+    from oracle.unet_ref import UNetRef
+    from paper_2602_21760_b200.denoiser.weights import init_weights, synthetic_conditioning, unet_param_specs
+    threads = threads or os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    t0 = time.perf_counter()
+    if weights is None:
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        weights = {k: v.cpu() for k, v in init_weights(unet_param_specs(spec), seed=0, device=dev).items()}
+    init_s = time.perf_counter() - t0
+    net = UNetRef(spec, weights)
+    cond = synthetic_conditioning(1, spec.context_len, spec.cross_dim, spec.pooled_dim)
+    hw = spec.latent_hw
+    x = torch.randn(1, spec.in_channels, hw, hw)
+    fwd = []
+    with torch.no_grad():
+        for _ in range(n_forwards):
+            t1 = time.perf_counter()
+            net(x, torch.tensor([500.0]), cond.context, cond.pooled)
+            fwd.append(time.perf_counter() - t1)
+    n = hw * hw * spec.in_channels
+    rng = np.random.default_rng(0)
+    ec, eu, xs = rng.standard_normal((1, n)), rng.standard_normal((1, n)), rng.standard_normal((1, n))
+    _, _, abar, sig = osmp.schedule_tables("scaled-linear", STEPS_T, 0.00085, 0.012)
+    t1 = time.perf_counter()
+    reps = 20
+    for _ in range(reps):
+        m = osmp.rel_mae(ec, eu)
+        e = osmp.cfg(ec, eu, 5.0)
+        xs = osmp.ddim(xs, e, 25, abar, sig)
+    trio = (time.perf_counter() - t1) / reps
+    f = min(fwd)
+    per_image = STEPS_T * (2 * f + trio)         # reference serial: rho = 2 branch evaluations / step
+    return per_image, {"forward_s": f, "sampler_trio_s": trio, "threads": threads, "weight_init_s": init_s,
+                       "m": m}
+
+
+def run_reference_arm(args):
+    ws, rank, local = _dist()
+    if rank != 0:
+        return 0
+    from paper_2602_21760_b200.denoiser.weights import SDXL
+    import torch
+    weights = None
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    from paper_2602_21760_b200.denoiser.weights import init_weights, unet_param_specs
+    weights = {k: v.cpu() for k, v in init_weights(unet_param_specs(SDXL), seed=0, device=dev).items()}
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, det = cpu_reference_sample(SDXL, 1, weights=weights)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    sample = (f"per step: one fp32 CPU forward of the SDXL-shaped U-Net at B=1 (one branch) + the numpy "
+              f"fp64 cfg/rel_mae/ddim trio at N=65536, extrapolated x{STEPS_T} steps x2 branches")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": {"workload": "sdxl-1024-50step-cfg", "latent": [128, 128, 4], "T": STEPS_T,
+                       "parallelism": "cpu"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": det["threads"], "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------------
+def sampler_roofline(hbm_peak):
+    """Time the fused CFG+DDIM+rel-MAE kernel at the SDXL latent size (both
+    branches of one image: 65,536 elements) and at 2^26 elements."""
+    import torch
+    import paper_2602_21760_b200 as hp
+    from paper_2602_21760_b200 import _kernels as K, _native as N
+    s = hp.build_schedule("scaled-linear", 50, 0.00085, 0.012)
+    c = hp.StepCoefficients.ddim(s, 30)
+    res = {}
+    for n in (65536, 1 << 22, 1 << 26):
+        x = torch.randn(n, device="cuda")
+        ec = torch.randn(n, device="cuda").bfloat16()
+        eu = torch.randn(n, device="cuda").bfloat16()
+        out = torch.empty_like(x)
+        ob = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        ws = K.workspace()
+
+        def launch():
+            K.sampler_step(x=x, eps_c=ec, eps_u=eu, x_out=out, x_out_bf16=ob, update=N.HP_UPDATE_DDIM, t=30,
+                           w=5.0, c_sigma=c.c_sigma, c_sqrt_ab=c.c_sqrt_ab, c_sqrt_ab_prev=c.c_sqrt_ab_prev,
+                           c_sqrt_1m_ab_prev=c.c_sqrt_1m_ab_prev, ws=ws)
+        for _ in range(5):
+            launch()
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        times = []
+        for _ in range(20):
+            flush.zero_()                                    # evict L2 (> 126 MB)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            launch()
+            b.record()
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b) / 1e3)
+        t = statistics.median(times)
+        bytes_ = 14 * n       # x f32 in + eps_c, eps_u bf16 + x f32 out + x bf16 out
+        res[n] = {"elements": n, "us": t * 1e6, "algorithmic_bytes": bytes_, "gbs": bytes_ / t / 1e9,
+                  "frac": bytes_ / t / 1e9 / hbm_peak}
+    return res
+
+
+def forward_roofline(den, spec, reps=20):
+    import torch
+    from paper_2602_21760_b200.denoiser.unet import unet_flops
+    x = torch.randn(1, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
+    den.load_input(x)
+    for _ in range(3):
+        den.branches(x, 30, den.input_slot())
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        den.branches(x, 30, den.input_slot())
+    b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / 1e3 / reps
+    return t, unet_flops(spec, 2)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "pairs"])
+    ap.add_argument("--spec", default="sdxl", choices=["sdxl", "tiny"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2602_21760_b200 as hp
+    from paper_2602_21760_b200 import pipelines
+    from paper_2602_21760_b200.denoiser import kernels as DK
+    from paper_2602_21760_b200.denoiser.weights import SDXL, TINY
+    spec = SDXL if args.spec == "sdxl" else TINY
+    hbm_peak, bf16_burst, bf16_sus, peak_src = _peaks()
+
+    den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=STEPS_T, seed=rank)
+    plan = pipelines.sdxl_plan(spec, variant="serial", steps=STEPS_T, seed=rank, denoiser=den, clock="device")
+    for _ in range(args.warmup):
+        hp.run_plan(plan)
+    torch.cuda.synchronize()
+    x_host = hp.initial_latents(plan)
+    x_dev = torch.from_numpy(x_host).cuda()
+
+    # ---- device-resident timed region ----
+    clocks = ClockSampler(local)
+    with clocks:
+        _barrier(ws)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            hp.engine.run_plan_resident(plan, x_dev)
+        b.record()
+        torch.cuda.synchronize()
+        _barrier(ws)
+    dev_s = _max_over_ranks(ws, a.elapsed_time(b) / 1e3)
+    images = args.steps * ws
+    value = dev_s / images
+
+    # ---- end-to-end through the public API (host x_T in, host x0 out) ----
+    _barrier(ws)
+    torch.cuda.synchronize()
+    a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a2.record()
+    last = None
+    for _ in range(args.steps):
+        last = hp.run_plan(plan)
+    b2.record()
+    torch.cuda.synchronize()
+    _barrier(ws)
+    e2e_s = _max_over_ranks(ws, a2.elapsed_time(b2) / 1e3)
+    h2d = int(x_host.nbytes)
+    d2h = int(last.x0.nbytes) + 16 * len(last.series)
+
+    fwd_s, fwd_flops = forward_roofline(den, spec)
+    launches_fwd = den.g_both.launches
+    samp = sampler_roofline(hbm_peak) if rank == 0 else {}
+
+    if rank != 0:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return 0
+    achieved = fwd_flops / fwd_s / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{spec.name}-1024-50step-cfg" if spec.name == "sdxl" else f"{spec.name}-50step",
+                   "latent": [spec.latent_hw, spec.latent_hw, spec.in_channels], "T": STEPS_T,
+                   "guidance_w": 5.0, "images_per_gpu": args.steps, "plan": "serial (CFG batched B=2)",
+                   "parallelism": f"{args.mode}x{ws}" if ws > 1 else "single",
+                   "params_b": 2.567 if spec.name == "sdxl" else None,
+                   "l2": "working set (5.1 GB of bf16 weights per step) >> 126 MB L2"},
+        "e2e": {"value": e2e_s / images, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(args.steps * STEPS_T * (launches_fwd + 1)),
+        "roofline": {"bound": "tensor", "kernel": "denoiser forward (tcgen05 GEMM/conv + attention), B=2",
+                     "achieved": achieved, "peak": bf16_sus, "unit": "TFLOP/s", "frac": achieved / bf16_sus,
+                     "peak_kind": f"{peak_src} sustained", "frac_of_burst": achieved / bf16_burst,
+                     "flops_per_launch": fwd_flops, "forward_ms": fwd_s * 1e3, "traffic": None},
+        "sampler_roofline": {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_src,
+                             "sizes": list(samp.values())},
+        "clocks": clocks.summary(),
+        "throughput_images_per_s": images / dev_s,
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        try:
+            v, det = cpu_reference_sample(spec, 1)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": det["threads"], "kind": "port",
+                                    "sample": "one fp32 CPU forward of the same-shape U-Net at B=1 + the numpy fp64 "
+                                              "cfg/rel_mae/ddim trio at the latent size; x50 steps x2 branches",
+                                    "forward_s": det["forward_s"], "sampler_trio_s": det["sampler_trio_s"]}
+        except Exception as exc:  # pragma: no cover
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                                    "sample": f"failed: {exc}"}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    _ = DK
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -53,32 +53,41 @@ constexpr int kMaxC = 2560;
 __global__ void __launch_bounds__(kGnThreads)
 gn_stats_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
                 int groups, int splits, float* __restrict__ part) {
+  // fixed-order reduction (no float atomics): deterministic, batch-invariant
   __shared__ float s_sum[kMaxC], s_sq[kMaxC];
+  __shared__ float p_sum[kGnThreads * 8], p_sq[kGnThreads * 8];
   const int C = c1 + c2;
   const int V = C / 8;
   const int n = blockIdx.y, split = blockIdx.x;
-  for (int c = threadIdx.x; c < C; c += kGnThreads) { s_sum[c] = 0.f; s_sq[c] = 0.f; }
-  __syncthreads();
   const int64_t p_begin = hw * split / splits, p_end = hw * (split + 1) / splits;
   for (int j0 = 0; j0 < V; j0 += kGnThreads) {
     const int vecs = min(V - j0, kGnThreads);
     const int rows = kGnThreads / vecs;
     const int j = j0 + threadIdx.x % vecs;
     const int r = threadIdx.x / vecs;
-    if (r >= rows) continue;
     float sum[8] = {0}, sq[8] = {0};
-    const int ch = j * 8;
-    for (int64_t p = p_begin + r; p < p_end; p += rows) {
-      float v[8];
-      if (ch < c1) load8(x1 + ((int64_t)n * hw + p) * c1 + ch, v);
-      else load8(x2 + ((int64_t)n * hw + p) * c2 + (ch - c1), v);
+    if (r < rows) {
+      const int ch = j * 8;
+      for (int64_t p = p_begin + r; p < p_end; p += rows) {
+        float v[8];
+        if (ch < c1) load8(x1 + ((int64_t)n * hw + p) * c1 + ch, v);
+        else load8(x2 + ((int64_t)n * hw + p) * c2 + (ch - c1), v);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) { sum[i] += v[i]; sq[i] += v[i] * v[i]; }
+        for (int i = 0; i < 8; ++i) { sum[i] += v[i]; sq[i] += v[i] * v[i]; }
+      }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { atomicAdd(&s_sum[ch + i], sum[i]); atomicAdd(&s_sq[ch + i], sq[i]); }
+    for (int i = 0; i < 8; ++i) { p_sum[threadIdx.x * 8 + i] = sum[i]; p_sq[threadIdx.x * 8 + i] = sq[i]; }
+    __syncthreads();
+    for (int q = threadIdx.x; q < vecs * 8; q += kGnThreads) {
+      const int jj = q / 8, i = q % 8;
+      float a = 0.f, b = 0.f;
+      for (int rr = 0; rr < rows; ++rr) { a += p_sum[(rr * vecs + jj) * 8 + i]; b += p_sq[(rr * vecs + jj) * 8 + i]; }
+      s_sum[(j0 + jj) * 8 + i] = a;
+      s_sq[(j0 + jj) * 8 + i] = b;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int cg = C / groups;
   for (int g = threadIdx.x; g < groups; g += kGnThreads) {
     float a = 0.f, b = 0.f;

@@ -19,6 +19,7 @@ from __future__ import annotations
 import torch
 
 from .. import _native as N
+from . import kernels as K
 
 
 def net_timestep(t: int, T: int) -> float:
@@ -31,6 +32,7 @@ class _Graphed:
         self.graph = None
         self.out = None
         self.use_graph = use_graph
+        self.launches = 0
 
     def run(self):
         if self.graph is not None:
@@ -46,8 +48,10 @@ class _Graphed:
             self.fn(self.x, self.t)
         torch.cuda.current_stream().wait_stream(s)
         g = torch.cuda.CUDAGraph()
+        before = K.LAUNCHES
         with torch.cuda.graph(g):
             self.out = self.fn(self.x, self.t)
+        self.launches = K.LAUNCHES - before
         self.graph = g
         g.replay()
         return self.out

@@ -294,13 +294,13 @@ class _StepRunner:
             raise from_status(mr.status, f"step at t={t}")
         return mr
 
-    def finish(self, x):
+    def finish(self, x, to_host=True):
         host = K.ctrl_read(self.ctrl)
         if host.status != 0:
             raise from_status(host.status, "denoising loop")
         series = tuple((t, float(host.m[t])) for t in range(self.plan.schedule.T, -1, -1)
                        if host.has[t])
-        x0 = x.to(torch.float64).cpu().numpy()
+        x0 = x.to(torch.float64).cpu().numpy() if to_host else None
         return x0, series
 
 
@@ -399,10 +399,10 @@ def _result(plan, x0, trace, series, tau1=None, tau2=None, stages=(), x_dev=None
                      x0_device=x_dev)
 
 
-def _run_exact(plan: ExecutionPlan, serial: bool) -> RunResult:
+def _run_exact(plan: ExecutionPlan, serial: bool, x_init=None, to_host=True) -> RunResult:
     st = _StepRunner(plan)
     clock = _Clock(plan)
-    x, xb = st.upload(initial_latents(plan))
+    x, xb = st.upload(initial_latents(plan) if x_init is None else x_init)
     T = plan.schedule.T
     for s in range(1, T + 1):
         t = T - s + 1
@@ -411,7 +411,7 @@ def _run_exact(plan: ExecutionPlan, serial: bool) -> RunResult:
             clock.serial_step(s)
         else:
             clock.measured_step(s, "")
-    x0, series = st.finish(x)
+    x0, series = st.finish(x, to_host)
     return _result(plan, x0, clock.result(), series, x_dev=x)
 
 
@@ -432,13 +432,13 @@ def run_full_condition_partition(plan: ExecutionPlan) -> RunResult:
     return _run_exact(plan, serial=False)
 
 
-def _run_staged(plan: ExecutionPlan, fractions) -> RunResult:
+def _run_staged(plan: ExecutionPlan, fractions, x_init=None, to_host=True) -> RunResult:
     st = _StepRunner(plan)
     clock = _Clock(plan)
     sw = plan.switch
     T = plan.schedule.T
     n = len(plan.devices)
-    x, xb = st.upload(initial_latents(plan))
+    x, xb = st.upload(initial_latents(plan) if x_init is None else x_init)
     host = StageState()
     no_series = DiscrepancySeries()
     first_poll = min(sw.L + 1, sw.tau_cap)   # the slope cannot fire earlier
@@ -467,7 +467,7 @@ def _run_staged(plan: ExecutionPlan, fractions) -> RunResult:
                 clock.measured_step(s, host.stage.value)
         stages.append(host.stage)
         prev = host.stage
-    x0, series = st.finish(x)
+    x0, series = st.finish(x, to_host)
     return _result(plan, x0, clock.result(), series, host.tau1, host.tau2, stages, x_dev=x)
 
 
@@ -517,3 +517,15 @@ _RUNNERS = {
 
 def run_plan(plan: ExecutionPlan) -> RunResult:
     return _RUNNERS[plan.variant](plan)
+
+
+def run_plan_resident(plan: ExecutionPlan, x_init: torch.Tensor) -> RunResult:
+    """``run_plan`` with x_T already resident on the device and x0 left there
+    (``RunResult.x0`` is None, ``x0_device`` holds it): the device-side cost of
+    a run with no host<->device traffic. Serial / FCP / hybrid / layer-wise."""
+    v = plan.variant
+    if v in (PlanVariant.SERIAL, PlanVariant.FULL_CONDITION_PARTITION):
+        return _run_exact(plan, serial=v is PlanVariant.SERIAL, x_init=x_init, to_host=False)
+    if v in (PlanVariant.HYBRID, PlanVariant.LAYER_WISE):
+        return _run_staged(plan, plan.segment_fractions, x_init=x_init, to_host=False)
+    raise PlanError(f"run_plan_resident does not run {v.value} plans")
