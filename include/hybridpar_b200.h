@@ -185,6 +185,11 @@ int hp_flag_wait(const volatile uint32_t* flag, uint32_t value,
 int hp_stage_send(void* dst, const void* src, int64_t nbytes, uint32_t* flag,
                   uint32_t value, void* stream);
 
+/* Zero-filled device allocation with an exact base pointer (IPC-exportable
+ * exchange buffers and flag words); hp_free releases it. Not for the hot loop. */
+int hp_alloc(int64_t nbytes, void** out_ptr);
+int hp_free(void* ptr);
+
 /* library version / build info */
 const char* hp_version(void);
 int hp_device_sm_count(int32_t* out);

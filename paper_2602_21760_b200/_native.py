@@ -85,6 +85,8 @@ SIGNATURES = {
     "hp_signal": (C.c_int, [_VP, _U32, _VP]),
     "hp_flag_wait": (C.c_int, [_VP, _U32, _VP, C.c_uint64, _VP]),
     "hp_stage_send": (C.c_int, [_VP, _VP, _I64, _VP, _U32, _VP]),
+    "hp_alloc": (C.c_int, [_I64, C.POINTER(C.c_void_p)]),
+    "hp_free": (C.c_int, [_VP]),
     "hp_version": (C.c_char_p, []),
     "hp_device_sm_count": (C.c_int, [_VP]),
 }

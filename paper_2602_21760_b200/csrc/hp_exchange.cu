@@ -112,6 +112,18 @@ int hp_stage_send(void* dst, const void* src, int64_t nbytes, uint32_t* flag, ui
   return HP_OK;
 }
 
+int hp_alloc(int64_t nbytes, void** out_ptr) {
+  if (nbytes <= 0 || !out_ptr) return HP_ERR_PARAMETER;
+  if (cudaMalloc(out_ptr, (size_t)nbytes) != cudaSuccess) return HP_ERR_CUDA;
+  if (cudaMemset(*out_ptr, 0, (size_t)nbytes) != cudaSuccess) return HP_ERR_CUDA;
+  return cudaDeviceSynchronize() == cudaSuccess ? HP_OK : HP_ERR_CUDA;
+}
+
+int hp_free(void* ptr) {
+  if (!ptr) return HP_ERR_PARAMETER;
+  return cudaFree(ptr) == cudaSuccess ? HP_OK : HP_ERR_CUDA;
+}
+
 const char* hp_version(void) { return "hybridpar_b200 0.1.0 (sm_100a)"; }
 
 int hp_device_sm_count(int32_t* out) {

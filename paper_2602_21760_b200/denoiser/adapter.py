@@ -77,6 +77,7 @@ class NetDenoiser:
         pool_c = conditioning.pooled[prompts]
         ctx_u = conditioning.null_context.expand(self.B, -1, -1)
         pool_u = conditioning.null_pooled.expand(self.B, -1)
+        self._ctx_u, self._pool_u = ctx_u.to(dev), pool_u.to(dev)
         net.prepare(torch.cat([ctx_u, ctx_c]).to(dev), torch.cat([pool_u, pool_c]).to(dev), key="both")
         net.prepare(ctx_c.to(dev), pool_c.to(dev), key="cond")
         B2 = 2 * self.B
@@ -118,3 +119,15 @@ class NetDenoiser:
         self.x_cond.view(self.B, self.numel).copy_(x.to(torch.bfloat16).view(self.B, self.numel))
         self._set_t(self.t_cond, t)
         return self.g_cond.run().reshape(self.B, self.numel)
+
+    def unconditional(self, x, t, x_bf16=None):
+        """Unconditional rows only (the uncond rank of a condition-partitioned pair)."""
+        if not hasattr(self, "g_uncond"):
+            self.net.prepare(self._ctx_u, self._pool_u, key="uncond")
+            self.x_unc = torch.zeros((self.B,) + self.shape, dtype=torch.bfloat16, device=self.dev)
+            self.t_unc = torch.zeros(self.B, dtype=torch.float32, device=self.dev)
+            self.g_uncond = _Graphed(lambda xx, tt: self.net.forward(xx, tt, key="uncond"), self.x_unc,
+                                     self.t_unc, self.g_cond.use_graph)
+        self.x_unc.view(self.B, self.numel).copy_(x.to(torch.bfloat16).view(self.B, self.numel))
+        self._set_t(self.t_unc, t)
+        return self.g_uncond.run().reshape(self.B, self.numel)

@@ -219,6 +219,9 @@ class MixtureDenoiser:
         eps_u = self._one(None, x, t)
         return self.conditional(x, t), eps_u
 
+    def unconditional(self, x, t, x_bf16=None):
+        return self._one(None, x, t)
+
 
 class _StepRunner:
     """Per-run GPU state: coefficient table, workspace, controller, mirror."""
