@@ -241,76 +241,97 @@ __global__ void concat_kernel(const bf16* __restrict__ a, int c1, const bf16* __
   }
 }
 
-// conv_in style: cin small (<= 16), cout multiple of 8. Thread = (pixel, 8 cout).
-__global__ void conv_small_in_kernel(const bf16* __restrict__ x, int n, int h, int w, int cin,
-                                     const float* __restrict__ wgt, const float* __restrict__ bias, int cout,
-                                     bf16* __restrict__ y) {
-  extern __shared__ float s_w[];  // [cout][9*cin]
-  const int kk = 9 * cin;
-  for (int i = threadIdx.x; i < cout * kk; i += blockDim.x) s_w[i] = wgt[i];
+// conv_in: cin = CIN (4), cout multiple of 32. Thread = (pixel, 32 output
+// channels); a warp holds 32 consecutive pixels of one channel group, so every
+// weight read is a shared-memory broadcast.
+template <int CIN>
+__global__ void __launch_bounds__(256)
+conv_small_in_kernel(const bf16* __restrict__ x, int n, int h, int w, const float* __restrict__ wgt,
+                     const float* __restrict__ bias, int cout, bf16* __restrict__ y) {
+  extern __shared__ float s_w[];  // [cout][9*CIN] then bias[cout]
+  constexpr int KK = 9 * CIN;
+  for (int i = threadIdx.x; i < cout * KK; i += blockDim.x) s_w[i] = wgt[i];
+  for (int i = threadIdx.x; i < cout; i += blockDim.x) s_w[cout * KK + i] = bias ? bias[i] : 0.f;
   __syncthreads();
-  const int G = cout / 8;
-  const int64_t total = (int64_t)n * h * w * G;
+  const int G = cout / 32;
+  const int64_t pixels = (int64_t)n * h * w;
+  const int64_t total = pixels * G;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int g = (int)(i % G);
-    const int64_t pix = i / G;
+    const int64_t pix = (i / 32 / G) * 32 + (i % 32);        // lanes = consecutive pixels
+    const int g = (int)((i / 32) % G);
+    if (pix >= pixels) continue;
     const int xx = (int)(pix % w);
     const int yy = (int)((pix / w) % h);
     const int b = (int)(pix / ((int64_t)w * h));
-    float in[9 * 16];
+    float in[KK];
+#pragma unroll
     for (int t = 0; t < 9; ++t) {
       const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
       const bool ok = sy >= 0 && sy < h && sx >= 0 && sx < w;
-      for (int ci = 0; ci < cin; ++ci)
-        in[t * cin + ci] = ok ? __bfloat162float(x[(((int64_t)b * h + sy) * w + sx) * cin + ci]) : 0.f;
-    }
-    float o[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int co = g * 8 + k;
-      float acc = bias ? bias[co] : 0.f;
-      const float* wr = s_w + co * kk;
-      for (int q = 0; q < kk; ++q) acc = fmaf(in[q], wr[q], acc);
-      o[k] = acc;
+      for (int ci = 0; ci < CIN; ++ci)
+        in[t * CIN + ci] = ok ? __bfloat162float(x[(((int64_t)b * h + sy) * w + sx) * CIN + ci]) : 0.f;
     }
-    store8(y + pix * cout + g * 8, o);
+#pragma unroll 1
+    for (int k0 = 0; k0 < 32; k0 += 8) {
+      float o[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int co = g * 32 + k0 + k;
+        const float* wr = s_w + co * KK;
+        float acc = s_w[cout * KK + co];
+#pragma unroll
+        for (int q = 0; q < KK; ++q) acc = fmaf(in[q], wr[q], acc);
+        o[k] = acc;
+      }
+      store8(y + pix * cout + g * 32 + k0, o);
+    }
   }
 }
 
-// conv_out style: cout small (<= 8), cin multiple of 8. One warp per output pixel.
-__global__ void conv_small_out_kernel(const bf16* __restrict__ x, int n, int h, int w, int cin,
-                                      const float* __restrict__ wgt, const float* __restrict__ bias, int cout,
-                                      void* __restrict__ y, int y_f32) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+// conv_out: cout = COUT (<= 8), cin multiple of 8. Thread = output pixel;
+// weights [cout][9][cin] in shared memory (broadcast reads).
+template <int COUT>
+__global__ void __launch_bounds__(256)
+conv_small_out_kernel(const bf16* __restrict__ x, int n, int h, int w, int cin, const float* __restrict__ wgt,
+                      const float* __restrict__ bias, void* __restrict__ y, int y_f32) {
+  extern __shared__ float s_w[];
+  const int KK = 9 * cin;
+  for (int i = threadIdx.x; i < COUT * KK; i += blockDim.x) s_w[i] = wgt[i];
+  __syncthreads();
   const int64_t pixels = (int64_t)n * h * w;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int V = cin / 8;
-  for (int64_t pix = warp; pix < pixels; pix += nwarps) {
+  for (int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pix < pixels;
+       pix += (int64_t)gridDim.x * blockDim.x) {
     const int xx = (int)(pix % w);
     const int yy = (int)((pix / w) % h);
     const int b = (int)(pix / ((int64_t)w * h));
-    float acc[8] = {0};
-    for (int q = lane; q < 9 * V; q += 32) {
-      const int t = q / V, j = q - t * V;
+    float acc[COUT];
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) acc[co] = bias ? bias[co] : 0.f;
+    for (int t = 0; t < 9; ++t) {
       const int sy = yy + t / 3 - 1, sx = xx + t % 3 - 1;
       if (sy < 0 || sy >= h || sx < 0 || sx >= w) continue;
-      float v[8];
-      load8(x + (((int64_t)b * h + sy) * w + sx) * cin + j * 8, v);
-      for (int co = 0; co < cout; ++co) {
-        const float* wr = wgt + ((int64_t)co * 9 + t) * cin + j * 8;
-        float a = acc[co];
+      const bf16* src = x + (((int64_t)b * h + sy) * w + sx) * cin;
+#pragma unroll 2
+      for (int j = 0; j < V; ++j) {
+        float v[8];
+        load8(src + j * 8, v);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) a = fmaf(v[i], wr[i], a);
-        acc[co] = a;
+        for (int co = 0; co < COUT; ++co) {
+          const float4* w4 = reinterpret_cast<const float4*>(s_w + co * KK + t * cin + j * 8);
+          const float4 wa = w4[0], wb = w4[1];
+          float a = acc[co];
+          a = fmaf(v[0], wa.x, a); a = fmaf(v[1], wa.y, a); a = fmaf(v[2], wa.z, a); a = fmaf(v[3], wa.w, a);
+          a = fmaf(v[4], wb.x, a); a = fmaf(v[5], wb.y, a); a = fmaf(v[6], wb.z, a); a = fmaf(v[7], wb.w, a);
+          acc[co] = a;
+        }
       }
     }
-    for (int co = 0; co < cout; ++co) acc[co] = hp_warp_sum_f(acc[co]);
-    if (lane < cout) {
-      float r = 0.f;
-      for (int co = 0; co < cout; ++co) if (co == lane) r = acc[co];
-      r += bias ? bias[lane] : 0.f;
-      if (y_f32) static_cast<float*>(y)[pix * cout + lane] = r;
-      else static_cast<bf16*>(y)[pix * cout + lane] = __float2bfloat16_rn(r);
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) {
+      if (y_f32) static_cast<float*>(y)[pix * COUT + co] = acc[co];
+      else static_cast<bf16*>(y)[pix * COUT + co] = __float2bfloat16_rn(acc[co]);
     }
   }
 }
@@ -489,20 +510,30 @@ int hp_conv3x3_small(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin
                      const float* bias, int32_t cout, void* y, int32_t y_is_f32, void* stream) {
   if (!x || !wgt || !y) return HP_ERR_PARAMETER;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cin <= 16 && cout % 8 == 0 && !y_is_f32) {
-    const size_t smem = (size_t)cout * 9 * cin * sizeof(float);
+  if (cin == 4 && cout % 32 == 0 && !y_is_f32) {
+    const size_t smem = (size_t)cout * (9 * cin + 1) * sizeof(float);
     if (smem > 200 * 1024) return HP_ERR_UNSUPPORTED;
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(conv_small_in_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int64_t total = (int64_t)n * h * w * (cout / 8);
-    conv_small_in_kernel<<<nblocks(total, 256, 148 * 4), 256, smem, st>>>(static_cast<const bf16*>(x), n, h, w, cin,
-                                                                           wgt, bias, cout, static_cast<bf16*>(y));
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(conv_small_in_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    const int64_t total = ((int64_t)n * h * w + 31) / 32 * 32 * (cout / 32);
+    conv_small_in_kernel<4><<<nblocks(total, 256, 148 * 8), 256, smem, st>>>(static_cast<const bf16*>(x), n, h, w,
+                                                                              wgt, bias, cout, static_cast<bf16*>(y));
     return ok();
   }
-  if (cout <= 8 && cin % 8 == 0) {
+  if (cout == 4 && cin % 8 == 0) {
+    const size_t smem = (size_t)cout * 9 * cin * sizeof(float);
+    if (smem > 200 * 1024) return HP_ERR_UNSUPPORTED;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(conv_small_out_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
     const int64_t pixels = (int64_t)n * h * w;
-    conv_small_out_kernel<<<nblocks(pixels * 32, 256, 148 * 16), 256, 0, st>>>(static_cast<const bf16*>(x), n, h, w,
-                                                                                cin, wgt, bias, cout, y, y_is_f32);
+    conv_small_out_kernel<4><<<nblocks(pixels, 128, 148 * 8), 128, smem, st>>>(static_cast<const bf16*>(x), n, h, w,
+                                                                                cin, wgt, bias, y, y_is_f32);
     return ok();
   }
   return HP_ERR_UNSUPPORTED;
