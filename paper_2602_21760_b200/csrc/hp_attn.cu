@@ -1,16 +1,20 @@
 // hp_attn.cu — K5: fused multi-head attention (head_dim 64) on tcgen05.
 //
-// One CTA per (128-query tile, head, batch). Warp roles:
-//   warp 0      TMA: Q once, then K/V tiles of 128 keys through a 3-stage ring
-//   warp 1      MMA: S(j) = Q K(j)^T into a double-buffered TMEM S (2 x 128 cols),
-//               O~(j) = P(j) V(j) into a double-buffered TMEM O~ (2 x 64 cols);
-//               V is consumed MN-major straight from its [keys][64] tile
-//   warp 2      TMEM allocation
-//   warps 4..7  softmax: thread i owns query row i; tcgen05.ld of S, online
-//               max/exp2/sum in fp32 registers, P as bf16 written to a
-//               double-buffered SW128 smem tile (the A operand of the PV MMA),
-//               O accumulated in registers with the running rescale.
-// S(j+1) is computed on the tensor core while the softmax warps work on S(j).
+// One CTA = two 128-query tiles of one (head, batch); 320 threads:
+//   warps 0-3   softmax for query tile 0 (thread i owns query row i)
+//   warps 4-7   softmax for query tile 1
+//   warp 8      TMA: Q0, Q1 once, then K/V tiles of 128 keys (3-stage ring)
+//   warp 9      TMEM allocation + MMA issue:
+//                 S_q(j) = Q_q K(j)^T           -> TMEM S_q   (128 cols fp32)
+//                 O_q   += P_q(j) V(j)          -> TMEM O_q   (64 cols fp32, accumulated)
+//               issued S0(j), PV0(j-1), S1(j), PV1(j-1), so the tensor core
+//               works on one tile while the other tile's softmax runs.
+// Softmax (per row, fp32, log2 domain): one TMEM pass over S, block max, lazy
+// rescale of O in TMEM only when the running max grows by more than 2^8
+// (otherwise the stale max is kept: p <= 2^8, exact after the final 1/l), and
+// exp2 split between MUFU.EX2 and a degree-4 polynomial on the FMA pipe (P is
+// rounded to bf16 anyway). P goes to shared memory as the SW128 K-major A
+// operand of the PV MMA; V is consumed MN-major straight from its TMA tile.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -26,13 +30,13 @@ namespace {
 
 constexpr int kBQ = 128, kBK = 128, kD = 64;
 constexpr int kStages = 3;
-constexpr int kThreads = 256;
+constexpr int kThreads = 320;
 constexpr uint32_t kTileBytes = kBQ * kD * 2;        // 16 KB (Q, K or V tile)
 constexpr uint32_t kPBytes = kBQ * kBK * 2;          // 32 KB (two 64-key SW128 atoms)
 constexpr uint32_t kIdescS = idesc_bf16_f32(kBQ, kBK, 0);
 constexpr uint32_t kIdescO = idesc_bf16_f32(kBQ, kD, 1);  // B (= V) MN-major
-constexpr uint32_t kTmemCols = 512;                  // S0 S1 (256) + O0 O1 (128)
-constexpr uint32_t kColS = 0, kColO = 256;
+constexpr uint32_t kTmemCols = 512;
+constexpr float kRescaleThreshold = 8.0f;            // log2 units
 
 struct AttnParams {
   int sq, skv, heads;
@@ -42,46 +46,85 @@ struct AttnParams {
   int n_kv;
 };
 
+__device__ __forceinline__ float exp2_poly(float x) {
+  // 2^x for x <= 0 on the FMA pipe: x = i + f, f in [-0.5, 0.5], 2^f by a degree-4 polynomial
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;                   // 1.5 * 2^23: round to integer in the mantissa
+  const float fi = t - 12582912.0f;
+  const int i = __float_as_int(t) - 0x4B400000;
+  const float f = x - fi;
+  float p = fmaf(0.0096181291f, f, 0.0555041087f);
+  p = fmaf(p, f, 0.2402265070f);
+  p = fmaf(p, f, 0.6931471806f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (i << 23));
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+         "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+         "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+         "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+#define HP_R8(b) "=r"(r[(b) + 0]), "=r"(r[(b) + 1]), "=r"(r[(b) + 2]), "=r"(r[(b) + 3]), \
+                 "=r"(r[(b) + 4]), "=r"(r[(b) + 5]), "=r"(r[(b) + 6]), "=r"(r[(b) + 7])
+// 32 columns of TMEM into r[base .. base+31] (base a compile-time constant after inlining)
+__device__ __forceinline__ void tmem_ld_x32_at(uint32_t taddr, uint32_t* r, const int base) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : HP_R8(base), HP_R8(base + 8), HP_R8(base + 16), HP_R8(base + 24)
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __global__ void __launch_bounds__(kThreads, 1)
 attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + kTileBytes;
+  uint8_t* sQ = smem;                                  // 2 tiles
+  uint8_t* sK = sQ + 2 * kTileBytes;
   uint8_t* sV = sK + kStages * kTileBytes;
-  uint8_t* sP = sV + kStages * kTileBytes;  // 2 buffers
+  uint8_t* sP = sV + kStages * kTileBytes;            // 2 tiles (one P buffer per query tile)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
   uint64_t* q_full = bars;
   uint64_t* kv_full = q_full + 1;
   uint64_t* kv_empty = kv_full + kStages;
-  uint64_t* s_full = kv_empty + kStages;   // [2]
+  uint64_t* s_full = kv_empty + kStages;   // [2] per query tile
   uint64_t* p_full = s_full + 2;           // [2]
-  uint64_t* o_full = p_full + 2;           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* o_done = p_full + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-  const int q0 = qt * kBQ;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int q0 = blockIdx.x * 2 * kBQ;
   const int J = p.n_kv;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
     mbar_init(q_full, 1);
     for (int s = 0; s < kStages; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_full[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1); }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 9) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 8) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, kTileBytes);
+      mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
       tma_load_3d(sQ, &tmQ, q_full, p.q_col0 + h * kD, q0, b);
+      tma_load_3d(sQ + kTileBytes, &tmQ, q_full, p.q_col0 + h * kD, q0 + kBQ, b);
       for (int j = 0; j < J; ++j) {
         const int s = j % kStages;
         mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
@@ -90,150 +133,160 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         tma_load_3d(sV + s * kTileBytes, &tmV, &kv_full[s], p.v_col0 + h * kD, j * kBK, b);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 9) {
     if (lane == 0) {
       mbar_wait(q_full, 0);
-      const uint64_t dq = sdesc_sw128_kmajor(sQ);
-      auto issue_pv = [&](int j) {
-        const int s = j % kStages, pb = j & 1;
-        mbar_wait(&p_full[pb], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t d_o = tmem + kColO + pb * kD;
-#pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          // A = P: K-major, two 64-key atoms of 16 KB; B = V: MN-major, +16 keys = +2048 B
-          const uint64_t da = sdesc_sw128_kmajor(sP + pb * kPBytes + (k >> 2) * (kBQ * 128)) + 2 * (k & 3);
-          const uint64_t dv = sdesc_sw128_mnmajor(sV + s * kTileBytes + k * 2048, 8192);
-          umma_bf16(d_o, da, dv, kIdescO, k > 0 ? 1u : 0u);
-        }
-        umma_commit(&o_full[pb]);
-        umma_commit(&kv_empty[s]);
-      };
-      for (int j = 0; j < J; ++j) {
-        const int s = j % kStages, sb = j & 1;
-        mbar_wait(&kv_full[s], (j / kStages) & 1);
-        tc_fence_after();
+      auto issue_s = [&](int q, int j) {
+        const int s = j % kStages;
+        const uint64_t dq = sdesc_sw128_kmajor(sQ + q * kTileBytes);
         const uint64_t dk = sdesc_sw128_kmajor(sK + s * kTileBytes);
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem + kColS + sb * kBK, dq + 2 * k, dk + 2 * k, kIdescS, k > 0 ? 1u : 0u);
-        umma_commit(&s_full[sb]);
-        if (j >= 1) issue_pv(j - 1);
-      }
-      issue_pv(J - 1);
-    }
-  } else if (warp >= 4) {
-    // ------------------------------ softmax / correction ------------------------------
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;          // query row inside the tile
-    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    float o_acc[kD];
+        for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem + q * kBK, dq + 2 * k, dk + 2 * k, kIdescS, k > 0 ? 1u : 0u);
+        umma_commit(&s_full[q]);
+      };
+      auto issue_pv = [&](int q, int j, bool wait) {
+        const int s = j % kStages;
+        if (wait) {
+          mbar_wait(&p_full[q], j & 1);
+          tc_fence_after();
+        }
+        const uint32_t d_o = tmem + 256 + q * kD;
 #pragma unroll
-    for (int i = 0; i < kD; ++i) o_acc[i] = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;
-    float m_prev_pv = -INFINITY;    // max the pending O~(j-1) is relative to
-    float m_acc = -INFINITY;        // max o_acc is relative to
-    for (int j = 0; j < J; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      const int valid = min(kBK, p.skv - j * kBK);
-      // pass 1: row max over this block
-      uint32_t r[32];
-      float blk_max = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < kBK / 32; ++c) {
-        tmem_ld_32x32b_x32(tmem + lane_base + kColS + sb * kBK + c * 32, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float v = (c * 32 + i < valid) ? __uint_as_float(r[i]) : -INFINITY;
-          blk_max = fmaxf(blk_max, v);
+        for (int k = 0; k < kBK / 16; ++k) {
+          const uint64_t da = sdesc_sw128_kmajor(sP + q * kPBytes + (k >> 2) * (kBQ * 128)) + 2 * (k & 3);
+          const uint64_t dv = sdesc_sw128_mnmajor(sV + s * kTileBytes + k * 2048, 8192);
+          umma_bf16(d_o, da, dv, kIdescO, (j > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&o_done[q]);
+      };
+      for (int j = 0; j < J; ++j) {
+        mbar_wait(&kv_full[j % kStages], (j / kStages) & 1);
+        tc_fence_after();
+        for (int q = 0; q < 2; ++q) {
+          if (j > 0) {
+            // S_q(j) overwrites S_q(j-1): the softmax has consumed it once P_q(j-1) is out
+            mbar_wait(&p_full[q], (j - 1) & 1);
+            tc_fence_after();
+          }
+          issue_s(q, j);
+          if (j > 0) {
+            issue_pv(q, j - 1, false);      // P_q(j-1) was waited for above
+            if (q == 1) umma_commit(&kv_empty[(j - 1) % kStages]);
+          }
         }
       }
-      const float m_new = fmaxf(m_run, blk_max * p.scale_log2);
-      const float corr = exp2f(m_run - m_new);   // 0 on the first block
+      issue_pv(0, J - 1, true);
+      issue_pv(1, J - 1, true);
+      umma_commit(&kv_empty[(J - 1) % kStages]);
+    }
+  } else {
+    // ------------------------------ softmax ------------------------------
+    const int q = warp >> 2;                  // query tile of this warpgroup
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t t_s = tmem + lane_base + q * kBK;
+    const uint32_t t_o = tmem + lane_base + 256 + q * kD;
+    uint8_t* pbase = sP + q * kPBytes;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < J; ++j) {
+      mbar_wait(&s_full[q], j & 1);
+      tc_fence_after();
+      uint32_t r[kBK];
+      tmem_ld_x32_at(t_s + 0, r, 0);
+      tmem_ld_x32_at(t_s + 32, r, 32);
+      tmem_ld_x32_at(t_s + 64, r, 64);
+      tmem_ld_x32_at(t_s + 96, r, 96);
+      tmem_ld_wait();
+      const int valid = min(kBK, p.skv - j * kBK);
+      float mx = -INFINITY;
+      if (valid == kBK) {
+#pragma unroll
+        for (int i = 0; i < kBK; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < kBK; ++i) {
+          if (i >= valid) r[i] = __float_as_uint(-INFINITY);
+          mx = fmaxf(mx, __uint_as_float(r[i]));
+        }
+      }
+      const float m_blk = mx * p.scale_log2;
+      // lazy rescale: move the reference max only when it grows by > 2^8
+      const bool grow = (j == 0) || (m_blk > m_run + kRescaleThreshold);
+      if (j > 0) {
+        // PV(j-1) must be complete before O is rescaled or P is overwritten
+        mbar_wait(&o_done[q], (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, grow)) {
+          const float alpha = grow ? exp2f(m_run - fmaxf(m_run, m_blk)) : 1.0f;
+          uint32_t o[32];
+#pragma unroll
+          for (int c = 0; c < kD / 32; ++c) {
+            tmem_ld_32x32b_x32(t_o + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st_32x32b_x32(t_o + c * 32, o);
+          }
+          tmem_st_wait();
+          if (grow) l_run *= alpha;
+        }
+      }
+      if (grow) m_run = fmaxf(m_run, m_blk);
       float sum = 0.f;
-      // pass 2: P = exp2(s*scale - m_new), written bf16 into the SW128 A tile
-      uint8_t* pbase = sP + sb * kPBytes;
-#pragma unroll 1
+#pragma unroll
       for (int c = 0; c < kBK / 32; ++c) {
-        tmem_ld_32x32b_x32(tmem + lane_base + kColS + sb * kBK + c * 32, r);
-        tmem_ld_wait();
         uint32_t packed[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const int key = c * 32 + i;
-          const float p0 = key < valid ? exp2f(fmaf(__uint_as_float(r[i]), p.scale_log2, -m_new)) : 0.f;
-          const float p1 = key + 1 < valid ? exp2f(fmaf(__uint_as_float(r[i + 1]), p.scale_log2, -m_new)) : 0.f;
-          sum += p0 + p1;
-          packed[i / 2] = pack_bf16(p0, p1);
+          const float x0 = fmaf(__uint_as_float(r[c * 32 + i]), p.scale_log2, -m_run);
+          const float x1 = fmaf(__uint_as_float(r[c * 32 + i + 1]), p.scale_log2, -m_run);
+          // 3 of every 8 exponentials on the FMA pipe, the rest on MUFU
+          const float e0 = ((i & 7) == 6) ? exp2_poly(x0) : exp2f(x0);
+          const float e1 = ((i & 7) == 2 || (i & 7) == 6) ? exp2_poly(x1) : exp2f(x1);
+          sum += e0 + e1;
+          packed[i / 2] = pack_bf16(e0, e1);
         }
-        // keys c*32 .. c*32+31 live in atom (c>>1), 16-byte chunks 4*(c&1) .. +3
         uint8_t* atom = pbase + (c >> 1) * (kBQ * 128) + row * 128;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = ((c & 1) * 4 + q) ^ (row & 7);
+        for (int qq = 0; qq < 4; ++qq) {
+          const int chunk = ((c & 1) * 4 + qq) ^ (row & 7);
           *reinterpret_cast<uint4*>(atom + chunk * 16) =
-              make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+              make_uint4(packed[4 * qq], packed[4 * qq + 1], packed[4 * qq + 2], packed[4 * qq + 3]);
         }
       }
-      l_run = l_run * corr + sum;
-      m_run = m_new;
-      fence_proxy_async_smem();     // generic-proxy smem writes -> visible to the tensor core
+      l_run += sum;
+      fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[sb]);
-      // fold the previous block's O~ (relative to m_prev_pv) into o_acc
-      if (j >= 1) {
-        const int ob = (j - 1) & 1;
-        mbar_wait(&o_full[ob], ((j - 1) >> 1) & 1);
-        tc_fence_after();
-        const float a_old = exp2f(m_acc - m_prev_pv);
-        uint32_t ro[32];
+      if (lane == 0) mbar_arrive(&p_full[q]);
+    }
+    mbar_wait(&o_done[q], (J - 1) & 1);
+    tc_fence_after();
+    const int qrow = q0 + q * kBQ + row;
+    const float inv = 1.0f / l_run;
+    uint32_t o[32];
 #pragma unroll
-        for (int c = 0; c < kD / 32; ++c) {
-          tmem_ld_32x32b_x32(tmem + lane_base + kColO + ob * kD + c * 32, ro);
-          tmem_ld_wait();
+    for (int c = 0; c < kD / 32; ++c) {
+      tmem_ld_32x32b_x32(t_o + c * 32, o);
+      tmem_ld_wait();
+      if (qrow < p.sq) {
+        __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + c * 32;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = fmaf(o_acc[c * 32 + i], a_old, __uint_as_float(ro[i]));
+        for (int qq = 0; qq < 4; ++qq) {
+          uint4 u = make_uint4(pack_bf16(__uint_as_float(o[8 * qq]) * inv, __uint_as_float(o[8 * qq + 1]) * inv),
+                               pack_bf16(__uint_as_float(o[8 * qq + 2]) * inv, __uint_as_float(o[8 * qq + 3]) * inv),
+                               pack_bf16(__uint_as_float(o[8 * qq + 4]) * inv, __uint_as_float(o[8 * qq + 5]) * inv),
+                               pack_bf16(__uint_as_float(o[8 * qq + 6]) * inv, __uint_as_float(o[8 * qq + 7]) * inv));
+          reinterpret_cast<uint4*>(dst)[qq] = u;
         }
-        m_acc = m_prev_pv;
-      }
-      m_prev_pv = m_new;
-    }
-    // last block
-    {
-      const int ob = (J - 1) & 1;
-      mbar_wait(&o_full[ob], ((J - 1) >> 1) & 1);
-      tc_fence_after();
-      const float a_old = exp2f(m_acc - m_prev_pv);
-      uint32_t ro[32];
-#pragma unroll
-      for (int c = 0; c < kD / 32; ++c) {
-        tmem_ld_32x32b_x32(tmem + lane_base + kColO + ob * kD + c * 32, ro);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = fmaf(o_acc[c * 32 + i], a_old, __uint_as_float(ro[i]));
-      }
-    }
-    const int qrow = q0 + row;
-    if (qrow < p.sq) {
-      const float inv = 1.0f / l_run;
-      __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD;
-#pragma unroll
-      for (int q = 0; q < kD / 8; ++q) {
-        uint4 u = make_uint4(pack_bf16(o_acc[8 * q] * inv, o_acc[8 * q + 1] * inv),
-                             pack_bf16(o_acc[8 * q + 2] * inv, o_acc[8 * q + 3] * inv),
-                             pack_bf16(o_acc[8 * q + 4] * inv, o_acc[8 * q + 5] * inv),
-                             pack_bf16(o_acc[8 * q + 6] * inv, o_acc[8 * q + 7] * inv));
-        reinterpret_cast<uint4*>(dst)[q] = u;
       }
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<kTmemCols>(tmem);
+  if (warp == 9) tmem_dealloc<kTmemCols>(tmem);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -284,14 +337,14 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   p.o = static_cast<__nv_bfloat16*>(d->o); p.ldo = d->ldo;
   p.scale_log2 = d->scale * 1.4426950408889634f;
   p.n_kv = (d->skv + kBK - 1) / kBK;
-  constexpr size_t smem = 1024 + kTileBytes * (1 + 2 * kStages) + 2 * kPBytes + 256;
+  constexpr size_t smem = 1024 + kTileBytes * (2 + 2 * kStages) + 2 * kPBytes + 256;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return HP_ERR_CUDA;
     attr = true;
   }
-  dim3 grid((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
+  dim3 grid((d->sq + 2 * kBQ - 1) / (2 * kBQ), d->heads, d->batch);
   attn_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, p);
   return cudaGetLastError() == cudaSuccess ? HP_OK : HP_ERR_CUDA;
 }

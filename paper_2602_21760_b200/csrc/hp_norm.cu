@@ -104,7 +104,9 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
                 int groups, int splits, const float* __restrict__ part, float eps,
                 const float* __restrict__ gamma, const float* __restrict__ beta, int do_silu,
                 bf16* __restrict__ y) {
+  // per-channel affine folded once per block: y = x * sa[c] + sb[c]
   __shared__ float s_mean[64], s_rstd[64];
+  __shared__ __align__(16) float sa[kMaxC], sb[kMaxC];
   const int C = c1 + c2;
   const int V = C / 8;
   const int n = blockIdx.y;
@@ -124,23 +126,33 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
     s_rstd[threadIdx.x] = (float)(1.0 / sqrt(var + (double)eps));
   }
   __syncthreads();
-  const int64_t total = hw * V;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = i / V;
-    const int j = (int)(i - p * V);
-    const int ch = j * 8;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const int g = c / cg;
+    const float a = s_rstd[g] * gamma[c];
+    sa[c] = a;
+    sb[c] = beta[c] - s_mean[g] * a;
+  }
+  __syncthreads();
+  const int total = (int)(hw * V);                       // < 2^31 per image
+  const bf16* xa = x1 + (int64_t)n * hw * c1;
+  const bf16* xb = x2 ? x2 + (int64_t)n * hw * c2 : nullptr;
+  bf16* yo = y + (int64_t)n * hw * C;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int p = i / V;
+    const int ch = (i - p * V) * 8;
     float v[8];
-    if (ch < c1) load8(x1 + ((int64_t)n * hw + p) * c1 + ch, v);
-    else load8(x2 + ((int64_t)n * hw + p) * c2 + (ch - c1), v);
+    if (ch < c1) load8(xa + (int64_t)p * c1 + ch, v);
+    else load8(xb + (int64_t)p * c2 + (ch - c1), v);
+    const float4 a0 = *reinterpret_cast<const float4*>(sa + ch), a1 = *reinterpret_cast<const float4*>(sa + ch + 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(sb + ch), b1 = *reinterpret_cast<const float4*>(sb + ch + 4);
+    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int c = ch + k;
-      const int g = c / cg;
-      float o = (v[k] - s_mean[g]) * s_rstd[g];
-      o = o * gamma[c] + beta[c];
+      const float o = fmaf(v[k], av[k], bv[k]);
       v[k] = do_silu ? silu(o) : o;
     }
-    store8(y + ((int64_t)n * hw + p) * C + ch, v);
+    store8(yo + (int64_t)p * C + ch, v);
   }
 }
 
@@ -185,15 +197,24 @@ ln_kernel(const bf16* __restrict__ x, int64_t rows, int c, float eps, const floa
   for (int k = 0; k < kLnVec; ++k) {
     const int j = lane + 32 * k;
     if (j >= V) continue;
-    float o[8], sh[8], sc[8];
+    float o[8], sh[8], sc[8], ga[8], be[8];
     if (shift) load8(shift + b * ldm + j * 8, sh);
     if (scale) load8(scale + b * ldm + j * 8, sc);
+    if (gamma) {
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + j * 8));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + j * 8 + 4));
+      ga[0] = g0.x; ga[1] = g0.y; ga[2] = g0.z; ga[3] = g0.w; ga[4] = g1.x; ga[5] = g1.y; ga[6] = g1.z; ga[7] = g1.w;
+    }
+    if (beta) {
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + j * 8));
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + j * 8 + 4));
+      be[0] = b0.x; be[1] = b0.y; be[2] = b0.z; be[3] = b0.w; be[4] = b1.x; be[5] = b1.y; be[6] = b1.z; be[7] = b1.w;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int ch = j * 8 + i;
       float t = (v[k][i] - mean) * rstd;
-      if (gamma) t = t * gamma[ch];
-      if (beta) t = t + beta[ch];
+      if (gamma) t = t * ga[i];
+      if (beta) t = t + be[i];
       if (scale) t = t * (1.0f + sc[i]);
       if (shift) t = t + sh[i];
       o[i] = t;
