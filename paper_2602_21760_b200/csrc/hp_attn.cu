@@ -60,6 +60,44 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (i << 23));
 }
 
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+  return ((uint64_t)__float_as_uint(b) << 32) | (uint64_t)__float_as_uint(a);
+}
+__device__ __forceinline__ uint64_t pack2u(uint32_t a, uint32_t b) { return ((uint64_t)b << 32) | (uint64_t)a; }
+__device__ __forceinline__ float lo2(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi2(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair (x <= 0) on the FMA pipe: x = i + f, |f| <= 1/2, 2^f by a degree-4
+// polynomial, then i added into the exponent field (t = x + 1.5*2^23 holds i in its mantissa)
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  const float a = fmaxf(lo2(x2), -126.0f), b = fmaxf(hi2(x2), -126.0f);
+  const uint64_t x = pack2(a, b);
+  const uint64_t magic = pack2(12582912.0f, 12582912.0f);
+  const uint64_t t = fadd2(x, magic);
+  const uint64_t fi = fadd2(t, pack2(-12582912.0f, -12582912.0f));
+  const uint64_t f = ffma2(fi, pack2(-1.0f, -1.0f), x);
+  uint64_t pz = ffma2(pack2(0.0096181291f, 0.0096181291f), f, pack2(0.0555041087f, 0.0555041087f));
+  pz = ffma2(pz, f, pack2(0.2402265070f, 0.2402265070f));
+  pz = ffma2(pz, f, pack2(0.6931471806f, 0.6931471806f));
+  pz = ffma2(pz, f, pack2(1.0f, 1.0f));
+  const uint32_t lo = (uint32_t)pz + ((uint32_t)t << 23);
+  const uint32_t hi = (uint32_t)(pz >> 32) + ((uint32_t)(t >> 32) << 23);
+  return ((uint64_t)hi << 32) | lo;
+}
 __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -189,26 +227,25 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     const uint32_t t_o = tmem + lane_base + 256 + q * kD;
     uint8_t* pbase = sP + q * kPBytes;
     float m_run = -INFINITY, l_run = 0.f;
+    const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
     for (int j = 0; j < J; ++j) {
       mbar_wait(&s_full[q], j & 1);
       tc_fence_after();
-      uint32_t r[kBK];
-      tmem_ld_x32_at(t_s + 0, r, 0);
-      tmem_ld_x32_at(t_s + 32, r, 32);
-      tmem_ld_x32_at(t_s + 64, r, 64);
-      tmem_ld_x32_at(t_s + 96, r, 96);
-      tmem_ld_wait();
       const int valid = min(kBK, p.skv - j * kBK);
+      // pass 1: block row max straight from TMEM (32 columns at a time)
       float mx = -INFINITY;
-      if (valid == kBK) {
 #pragma unroll
-        for (int i = 0; i < kBK; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
-      } else {
+      for (int c = 0; c < kBK / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_s + c * 32, r);
+        tmem_ld_wait();
+        if (valid < kBK) {
 #pragma unroll
-        for (int i = 0; i < kBK; ++i) {
-          if (i >= valid) r[i] = __float_as_uint(-INFINITY);
-          mx = fmaxf(mx, __uint_as_float(r[i]));
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
         }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
       }
       const float m_blk = mx * p.scale_log2;
       // lazy rescale: move the reference max only when it grows by > 2^8
@@ -218,7 +255,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         mbar_wait(&o_done[q], (j - 1) & 1);
         tc_fence_after();
         if (__any_sync(0xffffffffu, grow)) {
-          const float alpha = grow ? exp2f(m_run - fmaxf(m_run, m_blk)) : 1.0f;
+          const float alpha = grow ? ex2f(m_run - fmaxf(m_run, m_blk)) : 1.0f;
           uint32_t o[32];
 #pragma unroll
           for (int c = 0; c < kD / 32; ++c) {
@@ -233,19 +270,32 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         }
       }
       if (grow) m_run = fmaxf(m_run, m_blk);
-      float sum = 0.f;
+      const uint64_t negm2 = pack2(-m_run, -m_run);
+      uint64_t sum2 = 0ull;
+      // pass 2: P = 2^(s*scale - m) in packed fp32 pairs; 3 of 8 pairs on the FMA-pipe polynomial
 #pragma unroll
       for (int c = 0; c < kBK / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_s + c * 32, r);
+        tmem_ld_wait();
+        if (valid < kBK) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
+        }
         uint32_t packed[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const float x0 = fmaf(__uint_as_float(r[c * 32 + i]), p.scale_log2, -m_run);
-          const float x1 = fmaf(__uint_as_float(r[c * 32 + i + 1]), p.scale_log2, -m_run);
-          // 3 of every 8 exponentials on the FMA pipe, the rest on MUFU
-          const float e0 = ((i & 7) == 6) ? exp2_poly(x0) : exp2f(x0);
-          const float e1 = ((i & 7) == 2 || (i & 7) == 6) ? exp2_poly(x1) : exp2f(x1);
-          sum += e0 + e1;
-          packed[i / 2] = pack_bf16(e0, e1);
+          const uint64_t x2 = ffma2(pack2u(r[i], r[i + 1]), scale2, negm2);
+          uint64_t e2;
+          const int pr = (i >> 1) & 7;
+          if (pr == 2 || pr == 5 || pr == 7) {
+            e2 = exp2_poly2(x2);
+          } else {
+            e2 = pack2(ex2f(lo2(x2)), ex2f(hi2(x2)));
+          }
+          sum2 = fadd2(sum2, e2);
+          packed[i / 2] = pack_bf16(lo2(e2), hi2(e2));
         }
         uint8_t* atom = pbase + (c >> 1) * (kBQ * 128) + row * 128;
 #pragma unroll
@@ -255,7 +305,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
               make_uint4(packed[4 * qq], packed[4 * qq + 1], packed[4 * qq + 2], packed[4 * qq + 3]);
         }
       }
-      l_run += sum;
+      l_run += lo2(sum2) + hi2(sum2);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
