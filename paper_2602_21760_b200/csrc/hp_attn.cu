@@ -22,6 +22,7 @@
 #include <math.h>
 #include <mutex>
 #include "hybridpar_b200_denoiser.h"
+#include "hp_common.cuh"
 #include "hp_tc.cuh"
 
 using namespace hptc;
@@ -157,6 +158,8 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 8) {
     if (lane == 0) {
@@ -395,6 +398,8 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
     attr = true;
   }
   dim3 grid((d->sq + 2 * kBQ - 1) / (2 * kBQ), d->heads, d->batch);
-  attn_kernel<<<grid, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, p);
-  return cudaGetLastError() == cudaSuccess ? HP_OK : HP_ERR_CUDA;
+  if (hp_launch_pdl(attn_kernel, grid, dim3(kThreads), smem, static_cast<cudaStream_t>(stream), tq, tk, tv, p) !=
+      cudaSuccess)
+    return HP_ERR_CUDA;
+  return HP_OK;
 }

@@ -24,6 +24,7 @@
 #include <string.h>
 #include <mutex>
 #include "hybridpar_b200_denoiser.h"
+#include "hp_common.cuh"
 #include "hp_tc.cuh"
 
 using namespace hptc;
@@ -176,6 +177,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();        // previous kernel's outputs (our A / residual) are complete from here on
+  pdl_trigger();     // let the next kernel's CTAs start their prologue on idle SMs
 
   if (warp == 0) {
     if (lane == 0) {
@@ -320,8 +323,9 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& 
   }
   const int tiles = p.num_m_tiles * p.num_n_tiles;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_kernel<BN, STAGES><<<grid, kThreads, smem, st>>>(ta, tb, p);
-  return cudaGetLastError() == cudaSuccess ? HP_OK : HP_ERR_CUDA;
+  if (hp_launch_pdl(gemm_kernel<BN, STAGES>, dim3(grid), dim3(kThreads), smem, st, ta, tb, p) != cudaSuccess)
+    return HP_ERR_CUDA;
+  return HP_OK;
 }
 
 int pick_bn(int64_t M, int64_t N, int act) {

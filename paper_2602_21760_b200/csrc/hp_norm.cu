@@ -53,6 +53,8 @@ constexpr int kMaxC = 2560;
 __global__ void __launch_bounds__(kGnThreads)
 gn_stats_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
                 int groups, int splits, float* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
   // fixed-order reduction (no float atomics): deterministic, batch-invariant
   __shared__ float s_sum[kMaxC], s_sq[kMaxC];
   __shared__ float p_sum[kGnThreads * 8], p_sq[kGnThreads * 8];
@@ -104,6 +106,8 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
                 int groups, int splits, const float* __restrict__ part, float eps,
                 const float* __restrict__ gamma, const float* __restrict__ beta, int do_silu,
                 bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   // per-channel affine folded once per block: y = x * sa[c] + sb[c]
   __shared__ float s_mean[64], s_rstd[64];
   __shared__ __align__(16) float sa[kMaxC], sb[kMaxC];
@@ -163,6 +167,8 @@ __global__ void __launch_bounds__(256)
 ln_kernel(const bf16* __restrict__ x, int64_t rows, int c, float eps, const float* __restrict__ gamma,
           const float* __restrict__ beta, const bf16* __restrict__ shift, const bf16* __restrict__ scale,
           int64_t ldm, int64_t rows_per_batch, bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * 8 + warp;
   if (row >= rows) return;
@@ -225,6 +231,8 @@ ln_kernel(const bf16* __restrict__ x, int64_t rows, int c, float eps, const floa
 
 // ---------------------------------------------------------------------------
 __global__ void silu_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, int64_t n8) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     float v[8];
     load8(x + i * 8, v);
@@ -235,6 +243,8 @@ __global__ void silu_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, in
 }
 
 __global__ void upsample2x_kernel(const bf16* __restrict__ x, int n, int h, int w, int c, bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int V = c / 8;
   const int64_t total = (int64_t)n * 2 * h * 2 * w * V;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -251,6 +261,8 @@ __global__ void upsample2x_kernel(const bf16* __restrict__ x, int n, int h, int 
 
 __global__ void concat_kernel(const bf16* __restrict__ a, int c1, const bf16* __restrict__ b, int c2,
                               int64_t pixels, bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int V1 = c1 / 8, V = (c1 + c2) / 8;
   const int64_t total = pixels * V;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -269,6 +281,8 @@ template <int CIN>
 __global__ void __launch_bounds__(256)
 conv_small_in_kernel(const bf16* __restrict__ x, int n, int h, int w, const float* __restrict__ wgt,
                      const float* __restrict__ bias, int cout, bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float s_w[];  // [cout][9*CIN] then bias[cout]
   constexpr int KK = 9 * CIN;
   for (int i = threadIdx.x; i < cout * KK; i += blockDim.x) s_w[i] = wgt[i];
@@ -316,6 +330,8 @@ template <int COUT>
 __global__ void __launch_bounds__(256)
 conv_small_out_kernel(const bf16* __restrict__ x, int n, int h, int w, int cin, const float* __restrict__ wgt,
                       const float* __restrict__ bias, void* __restrict__ y, int y_f32) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float s_w[];
   const int KK = 9 * cin;
   for (int i = threadIdx.x; i < COUT * KK; i += blockDim.x) s_w[i] = wgt[i];
@@ -374,6 +390,8 @@ constexpr int kSmallMaxM = 8;
 __global__ void linear_small_kernel(const float* __restrict__ x, int M, int K, const bf16* __restrict__ w,
                                     const float* __restrict__ bias, int N, int act_in, int act_out,
                                     float* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int n = warp; n < N; n += nwarps) {
@@ -407,6 +425,8 @@ __global__ void linear_small_kernel(const float* __restrict__ x, int M, int K, c
 
 __global__ void patchify_kernel(const bf16* __restrict__ x, int n, int h, int w, int c, int p, int inverse,
                                 bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   // token t = (ty, tx); feature f = (py * p + px) * c + ch
   const int64_t total = (int64_t)n * h * w * c;
   const int tw = w / p;
@@ -426,6 +446,8 @@ __global__ void patchify_kernel(const bf16* __restrict__ x, int n, int h, int w,
 
 __global__ void add_rows_kernel(const bf16* __restrict__ x, const bf16* __restrict__ add, int64_t rows,
                                 int64_t add_rows, int c, bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int V = c / 8;
   const int64_t total = rows * V;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -443,6 +465,8 @@ __global__ void add_rows_kernel(const bf16* __restrict__ x, const bf16* __restri
 __global__ void gated_residual_kernel(bf16* __restrict__ x, const bf16* __restrict__ yv,
                                       const bf16* __restrict__ gate, int64_t ldg, int64_t rows, int c,
                                       int64_t rows_per_batch) {
+  pdl_wait();
+  pdl_trigger();
   const int V = c / 8;
   const int64_t total = rows * V;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -481,15 +505,17 @@ int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_
   int splits = (296 + n - 1) / n;
   if (splits > hw) splits = (int)hw;
   if (splits > 64) splits = 64;
-  gn_stats_kernel<<<dim3(splits, n), kGnThreads, 0, st>>>(static_cast<const bf16*>(x1), c1,
+  hp_launch_pdl(gn_stats_kernel, dim3(splits, n), dim3(kGnThreads), 0, st, static_cast<const bf16*>(x1), c1,
                                                           static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups,
                                                           splits, stats);
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   const int64_t per_img = hw * (C / 8);
   int chunks = nblocks(per_img, kGnThreads * 4, 4096);
-  gn_apply_kernel<<<dim3(chunks, n), kGnThreads, 0, st>>>(static_cast<const bf16*>(x1), c1,
+  hp_launch_pdl(gn_apply_kernel, dim3(chunks, n), dim3(kGnThreads), 0, st, static_cast<const bf16*>(x1), c1,
                                                           static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups,
                                                           splits, stats, eps, gamma, beta, do_silu,
                                                           static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }
 
@@ -499,31 +525,35 @@ int hp_layer_norm(const void* x, int64_t rows, int32_t c, float eps, const float
   if (c % 8 || c > 32 * 8 * kLnVec || rows < 1) return HP_ERR_SHAPE;
   if ((shift || scale) && (rows_per_batch < 1 || ldm % 8)) return HP_ERR_PARAMETER;
   const int blocks = (int)((rows + 7) / 8);
-  ln_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  hp_launch_pdl(ln_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(x), rows, c, eps, gamma, beta, static_cast<const bf16*>(shift),
       static_cast<const bf16*>(scale), ldm, rows_per_batch, static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }
 
 int hp_silu(const void* x, void* y, int64_t n, void* stream) {
   if (!x || !y || n % 8) return HP_ERR_PARAMETER;
-  silu_kernel<<<nblocks(n / 8, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const bf16*>(x),
+  hp_launch_pdl(silu_kernel, dim3(nblocks(n / 8, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), static_cast<const bf16*>(x),
                                                                                    static_cast<bf16*>(y), n / 8);
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }
 
 int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, void* y, void* stream) {
   if (!x || !y || c % 8) return HP_ERR_PARAMETER;
   const int64_t total = (int64_t)n * 4 * h * w * (c / 8);
-  upsample2x_kernel<<<nblocks(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  hp_launch_pdl(upsample2x_kernel, dim3(nblocks(total, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(x), n, h, w, c, static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }
 
 int hp_concat_channels(const void* a, int32_t c1, const void* b, int32_t c2, int64_t pixels, void* y, void* stream) {
   if (!a || !b || !y || c1 % 8 || c2 % 8) return HP_ERR_PARAMETER;
-  concat_kernel<<<nblocks(pixels * ((c1 + c2) / 8), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  hp_launch_pdl(concat_kernel, dim3(nblocks(pixels * ((c1 + c2) / 8), 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(a), c1, static_cast<const bf16*>(b), c2, pixels, static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }
 
@@ -540,8 +570,9 @@ int hp_conv3x3_small(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin
       attr = true;
     }
     const int64_t total = ((int64_t)n * h * w + 31) / 32 * 32 * (cout / 32);
-    conv_small_in_kernel<4><<<nblocks(total, 256, 148 * 8), 256, smem, st>>>(static_cast<const bf16*>(x), n, h, w,
+    hp_launch_pdl(conv_small_in_kernel<4>, dim3(nblocks(total, 256, 148 * 8)), dim3(256), smem, st, static_cast<const bf16*>(x), n, h, w,
                                                                               wgt, bias, cout, static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
     return ok();
   }
   if (cout == 4 && cin % 8 == 0) {
@@ -553,8 +584,9 @@ int hp_conv3x3_small(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin
       attr = true;
     }
     const int64_t pixels = (int64_t)n * h * w;
-    conv_small_out_kernel<4><<<nblocks(pixels, 128, 148 * 8), 128, smem, st>>>(static_cast<const bf16*>(x), n, h, w,
+    hp_launch_pdl(conv_small_out_kernel<4>, dim3(nblocks(pixels, 128, 148 * 8)), dim3(128), smem, st, static_cast<const bf16*>(x), n, h, w,
                                                                                 cin, wgt, bias, y, y_is_f32);
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
     return ok();
   }
   return HP_ERR_UNSUPPORTED;
@@ -571,32 +603,36 @@ int hp_linear_small(const float* x, int32_t M, int32_t K, const void* w, const f
                     int32_t act_in, int32_t act_out, float* y, void* stream) {
   if (!x || !w || !y) return HP_ERR_PARAMETER;
   if (M < 1 || M > kSmallMaxM || K % 8) return HP_ERR_SHAPE;
-  linear_small_kernel<<<nblocks((int64_t)N * 32, 256, 148 * 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  hp_launch_pdl(linear_small_kernel, dim3(nblocks((int64_t)N * 32, 256, 148 * 8)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       x, M, K, static_cast<const bf16*>(w), bias, N, act_in, act_out, y);
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }
 
 int hp_patchify(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, int32_t p, int32_t inverse, void* y,
                 void* stream) {
   if (!x || !y || p < 1 || h % p || w % p) return HP_ERR_PARAMETER;
-  patchify_kernel<<<nblocks((int64_t)n * h * w * c, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  hp_launch_pdl(patchify_kernel, dim3(nblocks((int64_t)n * h * w * c, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(x), n, h, w, c, p, inverse, static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }
 
 int hp_add_rows(const void* x, const void* add, int64_t rows, int64_t add_rows, int32_t c, void* y, void* stream) {
   if (!x || !add || !y || c % 8 || add_rows < 1) return HP_ERR_PARAMETER;
-  add_rows_kernel<<<nblocks(rows * (c / 8), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  hp_launch_pdl(add_rows_kernel, dim3(nblocks(rows * (c / 8), 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(x), static_cast<const bf16*>(add), rows, add_rows, c, static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }
 
 int hp_gated_residual(void* x, const void* y, const void* gate, int64_t ldg, int64_t rows, int32_t c,
                       int64_t rows_per_batch, void* stream) {
   if (!x || !y || !gate || c % 8 || rows_per_batch < 1 || ldg % 8) return HP_ERR_PARAMETER;
-  gated_residual_kernel<<<nblocks(rows * (c / 8), 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  hp_launch_pdl(gated_residual_kernel, dim3(nblocks(rows * (c / 8), 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<bf16*>(x), static_cast<const bf16*>(y), static_cast<const bf16*>(gate), ldg, rows, c,
       rows_per_batch);
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }
 

@@ -1,0 +1,37 @@
+"""Time one GEMM shape through hp_gemm (for ncu captures / quick sweeps).
+
+    python tools/prof_gemm.py M N K [block_n] [act] [reps]
+"""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2602_21760_b200.denoiser import kernels as K  # noqa: E402
+
+
+def main():
+    M, N, Kd = (int(v) for v in sys.argv[1:4])
+    bn = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    act = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+    reps = int(sys.argv[6]) if len(sys.argv) > 6 else 20
+    a = torch.randn(M, Kd, device="cuda").bfloat16()
+    w = (torch.randn(N, Kd, device="cuda") * Kd ** -0.5).bfloat16()
+    bias = torch.randn(N, device="cuda")
+    out = torch.empty(M, N // 2 if act == 3 else N, device="cuda", dtype=torch.bfloat16)
+    run = lambda: K.gemm(a, w, bias=bias, out=out, act=act, block_n=bn)  # noqa: E731
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        run()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    print(f"gemm M={M} N={N} K={Kd} bn={bn} act={act}: {ms * 1e3:.1f} us {2.0 * M * N * Kd / ms / 1e9:.1f} TFLOP/s")
+
+
+if __name__ == "__main__":
+    main()
