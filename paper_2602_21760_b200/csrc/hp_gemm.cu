@@ -55,9 +55,11 @@ struct GemmParams {
 __device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
 
+// Epilogue for one 128 x BN tile; thread = one output row. `sb` is the tile's
+// column bias (bias + per-image bias2 folded) staged in shared memory, or null.
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
-                                              int lane) {
+                                              int lane, const float* sb) {
   const int row = m0 + quarter * 32 + lane;
   const bool row_ok = row < p.M;
   const uint32_t lane_addr = tmem_acc + ((uint32_t)(quarter * 32) << 16);
@@ -78,11 +80,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
       for (int j = 0; j < 32; j += 2) {
         float a0 = __uint_as_float(ra[j]) * p.alpha, a1 = __uint_as_float(ra[j + 1]) * p.alpha;
         float g0 = __uint_as_float(rg[j]) * p.alpha, g1 = __uint_as_float(rg[j + 1]) * p.alpha;
-        if (p.bias) {
-          a0 += p.bias[n0 + c * 32 + j];
-          a1 += p.bias[n0 + c * 32 + j + 1];
-          g0 += p.bias[n0 + BN / 2 + c * 32 + j];
-          g1 += p.bias[n0 + BN / 2 + c * 32 + j + 1];
+        if (sb) {
+          a0 += sb[c * 32 + j];
+          a1 += sb[c * 32 + j + 1];
+          g0 += sb[BN / 2 + c * 32 + j];
+          g1 += sb[BN / 2 + c * 32 + j + 1];
         }
         packed[j / 2] = pack_bf16(a0 * gelu_erf(g0), a1 * gelu_erf(g1));
       }
@@ -93,29 +95,35 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     }
     return;
   }
+  const bool has_res = p.res != nullptr && row_ok;
+  const uint4* res_row = has_res ? reinterpret_cast<const uint4*>(p.res + (long long)row * p.ldr + n0) : nullptr;
+  uint4 rn[4];
+  if (has_res) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rn[q] = res_row[q];
+  }
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     uint32_t r[32];
     tmem_ld_32x32b_x32(lane_addr + c * 32, r);
+    uint4 rc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rc[q] = rn[q];
+    if (has_res && c + 1 < BN / 32) {          // residual of the next chunk in flight meanwhile
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rn[q] = res_row[(c + 1) * 4 + q];
+    }
     tmem_ld_wait();
     if (!row_ok) continue;
     const int col = n0 + c * 32;
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
-    if (p.bias) {
-      const float4* b4 = reinterpret_cast<const float4*>(p.bias + col);
+    if (sb) {
+      const float4* b4 = reinterpret_cast<const float4*>(sb + c * 32);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        float4 b = __ldg(b4 + q);
-        v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
-      }
-    }
-    if (p.bias2) {
-      const float4* b4 = reinterpret_cast<const float4*>(p.bias2 + (long long)(row / p.bias2_div) * p.N + col);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 b = __ldg(b4 + q);
+        const float4 b = b4[q];
         v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
       }
     }
@@ -126,11 +134,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
     }
-    if (p.res) {
-      const uint4* src = reinterpret_cast<const uint4*>(p.res + (long long)row * p.ldr + col);
+    if (has_res) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        uint4 u = src[q];
+        const uint4 u = rc[q];
         float2 f0 = unpack_bf16(u.x), f1 = unpack_bf16(u.y), f2 = unpack_bf16(u.z), f3 = unpack_bf16(u.w);
         v[8 * q + 0] += f0.x; v[8 * q + 1] += f0.y; v[8 * q + 2] += f1.x; v[8 * q + 3] += f1.y;
         v[8 * q + 4] += f2.x; v[8 * q + 5] += f2.y; v[8 * q + 6] += f3.x; v[8 * q + 7] += f3.y;
@@ -161,6 +168,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);   // [2][BN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_tiles = p.num_m_tiles * p.num_n_tiles;
@@ -247,15 +255,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   } else if (warp >= 4) {
     // ------------------------------ epilogue ------------------------------
     const int quarter = warp & 3;
+    const int et = threadIdx.x - 128;                 // 0..127 across the 4 epilogue warps
+    const bool any_bias = p.bias != nullptr || p.bias2 != nullptr;
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const uint32_t acc = local & 1;
       const uint32_t use = local >> 1;
       const int m0 = (tile % p.num_m_tiles) * BM;
       const int n0 = (tile / p.num_m_tiles) * BN;
+      float* sb = any_bias ? sbias + acc * BN : nullptr;
+      if (any_bias) {
+        // stage this tile's column bias while the tensor core is still busy; every row
+        // of a tile belongs to one image (bias2_div is a multiple of 128)
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const long long img = (long long)(m0 / p.bias2_div);
+        for (int i = et; i < BN; i += 128) {
+          float b = p.bias ? __ldg(p.bias + n0 + i) : 0.0f;
+          if (p.bias2) b += __ldg(p.bias2 + img * p.N + n0 + i);
+          sb[i] = b;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-      epilogue_tile<BN>(p, tmem_base + acc * BN, m0, n0, quarter, lane);
+      epilogue_tile<BN>(p, tmem_base + acc * BN, m0, n0, quarter, lane, sb);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -313,7 +336,7 @@ int num_sms() {
 
 template <int BN, int STAGES>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
-  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + BN * BK * 2) + 256;
+  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + BN * BK * 2) + 256 + 2 * BN * sizeof(float);
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -370,6 +393,7 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   p.mode = d->a_mode;
   p.d = static_cast<__nv_bfloat16*>(d->d); p.ldd = d->ldd;
   p.bias = d->bias; p.bias2 = d->bias2; p.bias2_div = d->bias2_div > 0 ? d->bias2_div : 1;
+  if (d->bias2 && (p.bias2_div % BM)) return HP_ERR_UNSUPPORTED;   // one image per 128-row tile
   p.res = static_cast<const __nv_bfloat16*>(d->residual); p.ldr = d->ldr;
   p.act = d->act;
   p.alpha = d->alpha == 0.0f ? 1.0f : d->alpha;
