@@ -44,6 +44,13 @@ typedef struct hp_gemm_desc {
     int32_t act;                               /* HP_ACT_*                       */
     int32_t block_n;                           /* 0 = auto                       */
     float alpha;                               /* acc scale before bias          */
+    const float* colscale;                     /* [N] or NULL: d = residual + colscale[col] *
+                                                  act(alpha*acc + bias)  (adaLN-Zero gate) */
+    /* batched plain GEMM (a_mode HP_A_PLAIN only): `batch` independent row
+     * blocks of M rows each; element strides between consecutive blocks of A,
+     * D, residual and colscale (0 = shared). batch <= 1 = ordinary GEMM.    */
+    int32_t batch;
+    int64_t a_bstride, d_bstride, r_bstride, cs_bstride;
 } hp_gemm_desc;
 
 int hp_gemm(const hp_gemm_desc* d, void* stream);
@@ -72,10 +79,16 @@ int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_
                   void* y, float* stats, void* stream);
 /* LayerNorm over rows of bf16 [rows, c]; optional gamma/beta (fp32);
  * optional adaLN modulation y = norm*(1+scale[b]) + shift[b] with
- * b = row / rows_per_batch, scale/shift bf16 rows of length c (stride ldm). */
+ * b = row / rows_per_batch, scale/shift fp32 rows of length c (stride ldm). */
 int hp_layer_norm(const void* x, int64_t rows, int32_t c, float eps, const float* gamma,
                   const float* beta, const void* shift, const void* scale, int64_t ldm,
                   int64_t rows_per_batch, void* y, void* stream);
+/* Joint (two-stream) modulated LayerNorm for MMDiT token buffers laid out
+ * [batch][rows_per_batch][c]: row i of a batch uses (shift, scale) when
+ * i < split and (shift2, scale2) otherwise (each fp32, batch stride ldm). */
+int hp_layer_norm_joint(const void* x, int64_t rows, int32_t c, float eps, const float* shift,
+                        const float* scale, const float* shift2, const float* scale2, int64_t ldm,
+                        int64_t rows_per_batch, int64_t split, void* y, void* stream);
 /* y = silu(x) elementwise, bf16 */
 int hp_silu(const void* x, void* y, int64_t n, void* stream);
 /* nearest 2x upsample NHWC bf16: [n, h, w, c] -> [n, 2h, 2w, c] */

@@ -50,7 +50,19 @@ struct GemmParams {
   const __nv_bfloat16* res; long long ldr;
   int act;
   float alpha;
+  const float* colscale;
+  int batch;                       // >= 1; plain mode only
+  long long a_bs, d_bs, r_bs, cs_bs;  // element strides between batches
 };
+
+template <int BN>
+__device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& b, int& m0, int& n0) {
+  const int mt_all = p.num_m_tiles * p.batch;
+  const int mt = tile % mt_all;
+  b = mt / p.num_m_tiles;
+  m0 = (mt - b * p.num_m_tiles) * BM;
+  n0 = (tile / mt_all) * BN;
+}
 
 __device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
@@ -134,6 +146,14 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
     }
+    if (p.colscale) {
+      const float4* g4 = reinterpret_cast<const float4*>(p.colscale + col);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 g = __ldg(g4 + q);
+        v[4 * q] *= g.x; v[4 * q + 1] *= g.y; v[4 * q + 2] *= g.z; v[4 * q + 3] *= g.w;
+      }
+    }
     if (has_res) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -171,7 +191,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   float* sbias = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);   // [2][BN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+  const int num_tiles = p.num_m_tiles * p.batch * p.num_n_tiles;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -193,8 +213,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       // ------------------------------ TMA producer ------------------------------
       uint32_t it = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % p.num_m_tiles) * BM;
-        const int n0 = (tile / p.num_m_tiles) * BN;
+        int bt, m0, n0;
+        decode_tile<BN>(p, tile, bt, m0, n0);
         int img = 0, y0 = 0, x0 = 0;
         if (p.mode != HP_A_PLAIN) {
           const int hw = p.out_h * p.out_w;
@@ -210,7 +230,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           mbar_arrive_expect_tx(&full[s], kStageBytes);
           uint8_t* a_dst = smA + s * kABytes;
           if (p.mode == HP_A_PLAIN) {
-            tma_load_2d(a_dst, &tmA, &full[s], kb * BK, m0);
+            if (p.batch > 1) tma_load_3d(a_dst, &tmA, &full[s], kb * BK, m0, bt);
+            else tma_load_2d(a_dst, &tmA, &full[s], kb * BK, m0);
           } else {
             const int tap = kb / p.cin_blocks;
             const int cb = kb - tap * p.cin_blocks;
@@ -261,14 +282,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const uint32_t acc = local & 1;
       const uint32_t use = local >> 1;
-      const int m0 = (tile % p.num_m_tiles) * BM;
-      const int n0 = (tile / p.num_m_tiles) * BN;
+      int bt, m0, n0;
+      decode_tile<BN>(p, tile, bt, m0, n0);
       float* sb = any_bias ? sbias + acc * BN : nullptr;
       if (any_bias) {
         // stage this tile's column bias while the tensor core is still busy; every row
         // of a tile belongs to one image (bias2_div is a multiple of 128)
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        const long long img = (long long)(m0 / p.bias2_div);
+        const long long img = p.batch > 1 ? (long long)bt : (long long)(m0 / p.bias2_div);
         for (int i = et; i < BN; i += 128) {
           float b = p.bias ? __ldg(p.bias + n0 + i) : 0.0f;
           if (p.bias2) b += __ldg(p.bias2 + img * p.N + n0 + i);
@@ -278,7 +299,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-      epilogue_tile<BN>(p, tmem_base + acc * BN, m0, n0, quarter, lane, sb);
+      if (p.batch > 1) {
+        GemmParams q = p;
+        q.d += (long long)bt * p.d_bs;
+        if (q.res) q.res += (long long)bt * p.r_bs;
+        if (q.colscale) q.colscale += (long long)bt * p.cs_bs;
+        epilogue_tile<BN>(q, tmem_base + acc * BN, m0, n0, quarter, lane, sb);
+      } else {
+        epilogue_tile<BN>(p, tmem_base + acc * BN, m0, n0, quarter, lane, sb);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -344,7 +373,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& 
       return HP_ERR_CUDA;
     attr_set = true;
   }
-  const int tiles = p.num_m_tiles * p.num_n_tiles;
+  const int tiles = p.num_m_tiles * p.batch * p.num_n_tiles;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   if (hp_launch_pdl(gemm_kernel<BN, STAGES>, dim3(grid), dim3(kThreads), smem, st, ta, tb, p) != cudaSuccess)
     return HP_ERR_CUDA;
@@ -380,7 +409,7 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if ((d->K % 8) || (d->ldb % 8)) return HP_ERR_UNSUPPORTED;   // 16-byte TMA strides
   if ((reinterpret_cast<uintptr_t>(d->a) | reinterpret_cast<uintptr_t>(d->b)) & 15) return HP_ERR_UNSUPPORTED;
   num_sms();
-  const int bn = d->block_n ? d->block_n : pick_bn(d->M, d->N, d->act);
+  const int bn = d->block_n ? d->block_n : pick_bn(d->M * (d->batch > 1 ? d->batch : 1), d->N, d->act);
   if (bn == 0 || d->N % bn) return HP_ERR_UNSUPPORTED;
   if (d->act == HP_ACT_GEGLU && (bn % 64)) return HP_ERR_UNSUPPORTED;
   const int64_t n_out = d->act == HP_ACT_GEGLU ? d->N / 2 : d->N;
@@ -396,7 +425,13 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if (d->bias2 && (p.bias2_div % BM)) return HP_ERR_UNSUPPORTED;   // one image per 128-row tile
   p.res = static_cast<const __nv_bfloat16*>(d->residual); p.ldr = d->ldr;
   p.act = d->act;
+  p.colscale = d->colscale;
+  if (d->colscale && (reinterpret_cast<uintptr_t>(d->colscale) & 15)) return HP_ERR_UNSUPPORTED;
   p.alpha = d->alpha == 0.0f ? 1.0f : d->alpha;
+  p.batch = d->batch > 1 ? d->batch : 1;
+  p.a_bs = d->a_bstride; p.d_bs = d->d_bstride; p.r_bs = d->r_bstride; p.cs_bs = d->cs_bstride;
+  if (p.batch > 1 && d->a_mode != HP_A_PLAIN) return HP_ERR_UNSUPPORTED;
+  if (p.batch > 1 && ((p.a_bs | p.d_bs | p.r_bs) % 8 || p.cs_bs % 4)) return HP_ERR_UNSUPPORTED;
   p.num_m_tiles = (int)((d->M + BM - 1) / BM);
   p.num_n_tiles = (int)(d->N / bn);
 
@@ -404,10 +439,17 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if (d->a_mode == HP_A_PLAIN) {
     if (d->lda % 8) return HP_ERR_UNSUPPORTED;
     p.num_kb = (int)((d->K + BK - 1) / BK);
-    const uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)d->M};
-    const uint64_t str[1] = {(uint64_t)d->lda * 2};
-    const uint32_t box[2] = {BK, BM};
-    if (!make_map(&ta, d->a, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;
+    if (p.batch > 1) {
+      const uint64_t dims[3] = {(uint64_t)d->K, (uint64_t)d->M, (uint64_t)p.batch};
+      const uint64_t str[2] = {(uint64_t)d->lda * 2, (uint64_t)p.a_bs * 2};
+      const uint32_t box[3] = {BK, BM, 1};
+      if (!make_map(&ta, d->a, 3, dims, str, box, nullptr)) return HP_ERR_CUDA;
+    } else {
+      const uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)d->M};
+      const uint64_t str[1] = {(uint64_t)d->lda * 2};
+      const uint32_t box[2] = {BK, BM};
+      if (!make_map(&ta, d->a, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;
+    }
   } else if (d->a_mode == HP_A_CONV3X3 || d->a_mode == HP_A_CONV3X3_S2) {
     const int s = d->a_mode == HP_A_CONV3X3_S2 ? 2 : 1;
     const int c = d->img_c;

@@ -34,6 +34,10 @@ __device__ __forceinline__ void store8(bf16* p, const float* v) {
   for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
   *reinterpret_cast<uint4*>(p) = u;
 }
+__device__ __forceinline__ void load8f(const float* p, float* v) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
 inline int nblocks(int64_t work, int per_block, int cap = 148 * 16) {
@@ -165,8 +169,9 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
 constexpr int kLnVec = 8;
 __global__ void __launch_bounds__(256)
 ln_kernel(const bf16* __restrict__ x, int64_t rows, int c, float eps, const float* __restrict__ gamma,
-          const float* __restrict__ beta, const bf16* __restrict__ shift, const bf16* __restrict__ scale,
-          int64_t ldm, int64_t rows_per_batch, bf16* __restrict__ y) {
+          const float* __restrict__ beta, const float* __restrict__ shift, const float* __restrict__ scale,
+          int64_t ldm, int64_t rows_per_batch, bf16* __restrict__ y, const float* __restrict__ shift2,
+          const float* __restrict__ scale2, int64_t split) {
   pdl_wait();
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -199,13 +204,17 @@ ln_kernel(const bf16* __restrict__ x, int64_t rows, int c, float eps, const floa
   sq = hp_warp_sum_f(sq);
   const float rstd = rsqrtf(sq / c + eps);
   const int64_t b = rows_per_batch > 0 ? row / rows_per_batch : 0;
+  if (split >= 0 && row - b * rows_per_batch >= split) {   // second stream of a joint buffer
+    shift = shift2;
+    scale = scale2;
+  }
 #pragma unroll
   for (int k = 0; k < kLnVec; ++k) {
     const int j = lane + 32 * k;
     if (j >= V) continue;
     float o[8], sh[8], sc[8], ga[8], be[8];
-    if (shift) load8(shift + b * ldm + j * 8, sh);
-    if (scale) load8(scale + b * ldm + j * 8, sc);
+    if (shift) load8f(shift + b * ldm + j * 8, sh);
+    if (scale) load8f(scale + b * ldm + j * 8, sc);
     if (gamma) {
       const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + j * 8));
       const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + j * 8 + 4));
@@ -526,8 +535,22 @@ int hp_layer_norm(const void* x, int64_t rows, int32_t c, float eps, const float
   if ((shift || scale) && (rows_per_batch < 1 || ldm % 8)) return HP_ERR_PARAMETER;
   const int blocks = (int)((rows + 7) / 8);
   hp_launch_pdl(ln_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), 
-      static_cast<const bf16*>(x), rows, c, eps, gamma, beta, static_cast<const bf16*>(shift),
-      static_cast<const bf16*>(scale), ldm, rows_per_batch, static_cast<bf16*>(y));
+      static_cast<const bf16*>(x), rows, c, eps, gamma, beta, static_cast<const float*>(shift),
+      static_cast<const float*>(scale), ldm, rows_per_batch, static_cast<bf16*>(y), (const float*)nullptr,
+      (const float*)nullptr, (int64_t)-1);
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
+  return ok();
+}
+
+int hp_layer_norm_joint(const void* x, int64_t rows, int32_t c, float eps, const float* shift, const float* scale,
+                        const float* shift2, const float* scale2, int64_t ldm, int64_t rows_per_batch, int64_t split,
+                        void* y, void* stream) {
+  if (!x || !y || !shift || !scale || !shift2 || !scale2) return HP_ERR_PARAMETER;
+  if (c % 8 || c > 32 * 8 * kLnVec || rows < 1 || rows_per_batch < 1 || split < 0 || ldm % 8) return HP_ERR_SHAPE;
+  const int blocks = (int)((rows + 7) / 8);
+  hp_launch_pdl(ln_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream),
+      static_cast<const bf16*>(x), rows, c, eps, (const float*)nullptr, (const float*)nullptr, shift, scale, ldm,
+      rows_per_batch, static_cast<bf16*>(y), shift2, scale2, split);
   if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }

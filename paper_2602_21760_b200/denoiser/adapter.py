@@ -106,7 +106,8 @@ class NetDenoiser:
         self._slot.copy_(x.to(torch.bfloat16).view(self.B, self.numel))
 
     def _set_t(self, buf, t):
-        buf.fill_(net_timestep(t, self.sched.T))
+        tf = getattr(self.net, "timestep_for", None)
+        buf.fill_(tf(t, self.sched.T) if tf is not None else net_timestep(t, self.sched.T))
 
     def branches(self, x, t, x_bf16=None):
         if x_bf16 is None or x_bf16.data_ptr() != self._slot.data_ptr():

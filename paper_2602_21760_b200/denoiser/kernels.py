@@ -43,6 +43,9 @@ class HpGemmDesc(C.Structure):
         ("bias2", _VP), ("bias2_div", _I64),
         ("residual", _VP), ("ldr", _I64),
         ("act", _I32), ("block_n", _I32), ("alpha", _F32),
+        ("colscale", _VP),
+        ("batch", _I32),
+        ("a_bstride", _I64), ("d_bstride", _I64), ("r_bstride", _I64), ("cs_bstride", _I64),
     ]
 
 
@@ -63,6 +66,7 @@ SIGNATURES = {
     "hp_attention": (C.c_int, [C.POINTER(HpAttnDesc), _VP]),
     "hp_group_norm": (C.c_int, [_VP, _I32, _VP, _I32, _I32, _I64, _I32, _F32, _VP, _VP, _I32, _VP, _VP, _VP]),
     "hp_layer_norm": (C.c_int, [_VP, _I64, _I32, _F32, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
+    "hp_layer_norm_joint": (C.c_int, [_VP, _I64, _I32, _F32, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP, _VP]),
     "hp_silu": (C.c_int, [_VP, _VP, _I64, _VP]),
     "hp_upsample2x": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP]),
     "hp_concat_channels": (C.c_int, [_VP, _I32, _VP, _I32, _I64, _VP, _VP]),
@@ -91,14 +95,40 @@ def _bf16(t, name):
 
 
 def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, act=ACT_NONE,
-         alpha=1.0, block_n=0, conv=None):
-    """out[M, N'] = epi(alpha * A @ W^T). ``conv=(n, h, w, c, stride)`` reads A as NHWC."""
+         alpha=1.0, block_n=0, conv=None, colscale=None):
+    """out[M, N'] = residual + colscale * act(alpha * A @ W^T + bias).
+    ``conv=(n, h, w, c, stride)`` reads A as NHWC."""
     lib = N.load()
     _bf16(a, "A")
     _bf16(w, "W")
     Nn, K = w.shape
     d = HpGemmDesc()
     d.a = _p(a)
+    if conv is None and a.dim() == 3:
+        # batched: a [batch, M, K] (any batch stride), out [batch, M, N'], residual
+        # [batch, M, N'] or [M, N'] (shared), colscale [batch, N] or [N] (shared)
+        nb, M, _ = a.shape
+        if a.shape[2] != K:
+            raise ShapeError(f"gemm K mismatch: A {tuple(a.shape)} vs W {tuple(w.shape)}")
+        n_out = Nn // 2 if act == ACT_GEGLU else Nn
+        if out is None:
+            out = torch.empty((nb, M, n_out), dtype=torch.bfloat16, device=a.device)
+        d.lda, d.a_mode, d.batch, d.a_bstride = a.stride(1), HP_A_PLAIN, nb, a.stride(0)
+        d.b, d.ldb = _p(w), w.stride(0)
+        d.d, d.ldd, d.d_bstride = _p(out), out.stride(1), out.stride(0)
+        d.M, d.N, d.K = M, Nn, K
+        d.bias = _p(bias)
+        d.bias2, d.bias2_div = _p(bias2), 1
+        d.residual = _p(residual)
+        if residual is not None:
+            d.ldr = residual.stride(-2)
+            d.r_bstride = residual.stride(0) if residual.dim() == 3 else 0
+        d.act, d.block_n, d.alpha = int(act), int(block_n), float(alpha)
+        d.colscale = _p(colscale)
+        if colscale is not None:
+            d.cs_bstride = colscale.stride(0) if colscale.dim() == 2 else 0
+        check(lib.hp_gemm(C.byref(d), _s()), f"hp_gemm batched {nb}x M={M} N={Nn} K={K}")
+        return out
     if conv is None:
         M = a.numel() // a.shape[-1]
         if a.shape[-1] != K:
@@ -124,6 +154,7 @@ def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, a
     d.residual = _p(residual)
     d.ldr = residual.stride(-2) if residual is not None else 0
     d.act, d.block_n, d.alpha = int(act), int(block_n), float(alpha)
+    d.colscale = _p(colscale)
     check(lib.hp_gemm(C.byref(d), _s()), f"hp_gemm M={M} N={Nn} K={K}")
     return out
 
@@ -162,6 +193,17 @@ def layer_norm(x, c, *, eps=1e-6, gamma=None, beta=None, shift=None, scale=None,
         out = torch.empty((rows, c), dtype=torch.bfloat16, device=x.device)
     check(lib.hp_layer_norm(_p(x), rows, c, eps, _p(gamma), _p(beta), _p(shift), _p(scale), int(ldm),
                             int(rows_per_batch), _p(out), _s()), "hp_layer_norm")
+    return out
+
+
+def layer_norm_joint(x, c, rows_per_batch, split, shift, scale, shift2, scale2, ldm, *, eps=1e-6, out=None):
+    """Two-stream modulated LayerNorm over a [batch, rows_per_batch, c] token buffer."""
+    lib = N.load()
+    rows = x.numel() // c
+    if out is None:
+        out = torch.empty_like(x)
+    check(lib.hp_layer_norm_joint(_p(x), rows, c, eps, _p(shift), _p(scale), _p(shift2), _p(scale2), int(ldm),
+                                  int(rows_per_batch), int(split), _p(out), _s()), "hp_layer_norm_joint")
     return out
 
 

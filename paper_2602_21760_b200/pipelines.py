@@ -83,6 +83,32 @@ def build_sdxl_denoiser(spec, n_prompts=1, steps=50, seed=0, use_graph=True, wei
     return den
 
 
+def build_sd3_denoiser(spec, n_prompts=1, steps=28, seed=0, use_graph=True, weights=None, conditioning=None):
+    import torch
+    from .denoiser.adapter import NetDenoiser
+    from .denoiser.mmdit import build_mmdit
+    from .denoiser.weights import synthetic_conditioning
+    net = build_mmdit(spec, seed=seed, device="cuda", weights=weights)
+    cond = conditioning or synthetic_conditioning(n_prompts, spec.ctx_len, spec.ctx_dim, spec.pooled_dim)
+    conditions = tuple(Condition((i,)) for i in range(n_prompts))
+    den = NetDenoiser(net, cond, conditions, sd3_schedule(steps),
+                      (spec.latent_hw, spec.latent_hw, spec.in_channels), use_graph=use_graph)
+    torch.cuda.synchronize()
+    return den
+
+
+def sd3_plan(spec, *, variant="serial", steps=28, n_prompts=1, seed=0, guidance=5.0, denoiser=None,
+             switch_key="sd3", **kw) -> ExecutionPlan:
+    """SD3-shaped MMDiT, flow-matching Euler (x_1 = x0 + e straight path, engine
+    ``sampler="euler"``), CFG; BASELINE configs 3 and 5."""
+    if denoiser is None:
+        denoiser = build_sd3_denoiser(spec, n_prompts=n_prompts, steps=steps)
+    numel = spec.latent_hw * spec.latent_hw * spec.in_channels
+    return make_plan(variant=variant, denoiser=denoiser, schedule=sd3_schedule(steps), numel=numel,
+                     n_prompts=n_prompts, seed=seed, guidance=guidance, switch=SWITCH[switch_key],
+                     sampler="euler", **kw)
+
+
 def sdxl_plan(spec, *, variant="serial", steps=50, n_prompts=1, seed=0, guidance=5.0,
               denoiser=None, switch_key=None, **kw) -> ExecutionPlan:
     if denoiser is None:

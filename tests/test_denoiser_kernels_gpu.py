@@ -141,11 +141,21 @@ def test_layer_norm(c):
     x = rnd(700, c) + 1.0
     g, b = torch.randn(c, device="cuda"), torch.randn(c, device="cuda")
     close(K.layer_norm(x, c, gamma=g, beta=b, eps=1e-5), F.layer_norm(x.float(), (c,), g, b, eps=1e-5))
-    sh, sc = rnd(2, c), rnd(2, c)
+    sh, sc = torch.randn(2, c, device="cuda"), torch.randn(2, c, device="cuda") * 0.3
     out = K.layer_norm(x[:600], c, shift=sh, scale=sc, ldm=c, rows_per_batch=300)
     ref = F.layer_norm(x[:600].float(), (c,), eps=1e-6)
-    ref = ref * (1 + sc.float().repeat_interleave(300, 0)) + sh.float().repeat_interleave(300, 0)
+    ref = ref * (1 + sc.repeat_interleave(300, 0)) + sh.repeat_interleave(300, 0)
     close(out, ref)
+
+
+def test_gemm_colscale_gate():
+    """adaLN-Zero gated residual fused in the epilogue: d = res + gate[col] * (A W^T + b)."""
+    M, N, Kd = 384, 256, 192
+    a, w = rnd(M, Kd), rnd(N, Kd, s=Kd ** -0.5)
+    b, g = torch.randn(N, device="cuda"), torch.randn(N, device="cuda")
+    res = rnd(M, N)
+    close(K.gemm(a, w, bias=b, colscale=g, residual=res),
+          res.float() + g * (a.float() @ w.float().t() + b))
 
 
 def test_small_ops():
