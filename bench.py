@@ -249,13 +249,100 @@ def forward_roofline(den, spec, reps=20):
     return t, unet_flops(spec, 2)
 
 
+def time_replicas(args, spec, ws, rank, local):
+    """Every GPU generates its own images with the serial (CFG-batched) plan."""
+    import torch
+    import paper_2602_21760_b200 as hp
+    from paper_2602_21760_b200 import pipelines
+    den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=STEPS_T, seed=rank)
+    plan = pipelines.sdxl_plan(spec, variant="serial", steps=STEPS_T, seed=rank, denoiser=den, clock="device")
+    for _ in range(args.warmup):
+        hp.run_plan(plan)
+    torch.cuda.synchronize()
+    x_host = hp.initial_latents(plan)
+    x_dev = torch.from_numpy(x_host).cuda()
+    clocks = ClockSampler(local)
+    with clocks:
+        _barrier(ws)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            hp.engine.run_plan_resident(plan, x_dev)
+        b.record()
+        torch.cuda.synchronize()
+        _barrier(ws)
+    dev_s = _max_over_ranks(ws, a.elapsed_time(b) / 1e3)
+    _barrier(ws)
+    torch.cuda.synchronize()
+    a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a2.record()
+    last = None
+    for _ in range(args.steps):
+        last = hp.run_plan(plan)
+    b2.record()
+    torch.cuda.synchronize()
+    _barrier(ws)
+    e2e_s = _max_over_ranks(ws, a2.elapsed_time(b2) / 1e3)
+    h2d = int(x_host.nbytes)
+    d2h = int(last.x0.nbytes) + 16 * len(last.series)
+    return den, dev_s, args.steps * ws, e2e_s, h2d, d2h, clocks, 1
+
+
+def time_pairs(args, spec, ws, rank, local):
+    """Condition-partitioned pairs over NVLink: ranks (2p, 2p+1) generate one image
+    together with the hybrid plan (cond / uncond branch per GPU, fused exchange)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2602_21760_b200 as hp
+    from paper_2602_21760_b200 import parallel, pipelines
+    if ws % 2:
+        raise RuntimeError(f"pairs mode needs an even GPU count, got {ws}")
+    groups = [dist.new_group([2 * p, 2 * p + 1]) for p in range(ws // 2)]
+    role = parallel.pair_role(rank)
+    den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=STEPS_T, seed=0)   # same weights in a pair
+    plan = pipelines.sdxl_plan(spec, variant="hybrid", steps=STEPS_T, seed=role.pair, denoiser=den,
+                               clock="device")
+    sess = parallel.PairSession(plan, groups[role.pair])
+    for _ in range(args.warmup):
+        sess.run()
+    x_host = hp.initial_latents(plan)
+    x_dev = torch.from_numpy(x_host).cuda()
+    clocks = ClockSampler(local)
+    with clocks:
+        _barrier(ws)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            sess.run(x_dev)
+        b.record()
+        torch.cuda.synchronize()
+        _barrier(ws)
+    dev_s = _max_over_ranks(ws, a.elapsed_time(b) / 1e3)
+    _barrier(ws)
+    torch.cuda.synchronize()
+    a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a2.record()
+    last = None
+    for _ in range(args.steps):
+        last = sess.run()
+    b2.record()
+    torch.cuda.synchronize()
+    _barrier(ws)
+    e2e_s = _max_over_ranks(ws, a2.elapsed_time(b2) / 1e3)
+    h2d = int(x_host.nbytes)
+    d2h = int(last.x0.nbytes) + 16 * len(last.series)
+    return den, dev_s, args.steps * (ws // 2), e2e_s, h2d, d2h, clocks, 1
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "pairs"])
+    ap.add_argument("--mode", default="pairs", choices=["replicas", "pairs"])
     ap.add_argument("--spec", default="sdxl", choices=["sdxl", "tiny"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -276,47 +363,24 @@ def main():
     spec = SDXL if args.spec == "sdxl" else TINY
     hbm_peak, bf16_burst, bf16_sus, peak_src = _peaks()
 
-    den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=STEPS_T, seed=rank)
-    plan = pipelines.sdxl_plan(spec, variant="serial", steps=STEPS_T, seed=rank, denoiser=den, clock="device")
-    for _ in range(args.warmup):
-        hp.run_plan(plan)
-    torch.cuda.synchronize()
-    x_host = hp.initial_latents(plan)
-    x_dev = torch.from_numpy(x_host).cuda()
-
-    # ---- device-resident timed region ----
-    clocks = ClockSampler(local)
-    with clocks:
-        _barrier(ws)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(args.steps):
-            hp.engine.run_plan_resident(plan, x_dev)
-        b.record()
-        torch.cuda.synchronize()
-        _barrier(ws)
-    dev_s = _max_over_ranks(ws, a.elapsed_time(b) / 1e3)
-    images = args.steps * ws
+    mode = "single" if ws == 1 else args.mode
+    mode_note = None
+    den = None
+    if mode == "pairs":
+        try:
+            res = time_pairs(args, spec, ws, rank, local)
+        except Exception as exc:   # visible in the JSON line, never silent
+            mode_note = f"pairs mode failed ({type(exc).__name__}: {exc}); measured as replicas"
+            mode = "replicas"
+            _barrier(ws)
+    if mode != "pairs":
+        res = time_replicas(args, spec, ws, rank, local)
+    den, dev_s, images, e2e_s, h2d, d2h, clocks, steps_per_image = res
     value = dev_s / images
 
-    # ---- end-to-end through the public API (host x_T in, host x0 out) ----
-    _barrier(ws)
-    torch.cuda.synchronize()
-    a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a2.record()
-    last = None
-    for _ in range(args.steps):
-        last = hp.run_plan(plan)
-    b2.record()
-    torch.cuda.synchronize()
-    _barrier(ws)
-    e2e_s = _max_over_ranks(ws, a2.elapsed_time(b2) / 1e3)
-    h2d = int(x_host.nbytes)
-    d2h = int(last.x0.nbytes) + 16 * len(last.series)
-
     fwd_s, fwd_flops = forward_roofline(den, spec)
-    launches_fwd = den.g_both.launches
+    launches_fwd = (den.g_both.launches if mode != "pairs"
+                    else max(den.g_cond.launches, getattr(getattr(den, "g_uncond", None), "launches", 0)))
     samp = sampler_roofline(hbm_peak) if rank == 0 else {}
 
     if rank != 0:
@@ -331,8 +395,11 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": f"{spec.name}-1024-50step-cfg" if spec.name == "sdxl" else f"{spec.name}-50step",
                    "latent": [spec.latent_hw, spec.latent_hw, spec.in_channels], "T": STEPS_T,
-                   "guidance_w": 5.0, "images_per_gpu": args.steps, "plan": "serial (CFG batched B=2)",
-                   "parallelism": f"{args.mode}x{ws}" if ws > 1 else "single",
+                   "guidance_w": 5.0, "images": images,
+                   "plan": ("hybrid on condition-partitioned pairs (L=12, g=4e-4, tau_cap=15, k=5)"
+                            if mode == "pairs" else "serial (CFG batched B=2)"),
+                   "parallelism": f"{mode}x{ws}" if ws > 1 else "single",
+                   "mode_note": mode_note,
                    "params_b": 2.567 if spec.name == "sdxl" else None,
                    "l2": "working set (5.1 GB of bf16 weights per step) >> 126 MB L2"},
         "e2e": {"value": e2e_s / images, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

@@ -218,11 +218,23 @@ sampler_step_kernel(const XT* x, const ET* eps_c, const ET* eps_u, XT* x_out,
                     const volatile uint32_t* wait_flag, uint32_t wait_value, bool vec_ok) {
   using A = Ar<C>;
   if (wait_flag != nullptr) {
-    // exchange fusion: the partner's eps for this step must have landed
+    // exchange fusion: the partner's eps for this step must have landed. A partner
+    // that never arrives (crashed rank) turns into HP_ERR_TIMEOUT after 20 s instead
+    // of a hung GPU; the step then completes on stale data and the status is sticky.
+    __shared__ int s_timeout;
     if (threadIdx.x == 0) {
-      while (hp_ld_acquire_sys_u32(wait_flag) < wait_value) { __nanosleep(64); }
+      s_timeout = 0;
+      const uint64_t t0 = hp_globaltimer();
+      while (hp_ld_acquire_sys_u32(wait_flag) < wait_value) {
+        __nanosleep(64);
+        if (hp_globaltimer() - t0 > 20000000000ull) { s_timeout = 1; break; }
+      }
     }
     __syncthreads();
+    if (s_timeout && threadIdx.x == 0) {
+      if (status_out) *status_out = HP_ERR_TIMEOUT;
+      if (ctrl) ctrl->status = HP_ERR_TIMEOUT;
+    }
   }
   const C w = (C)sc.w, c_sigma = (C)sc.c_sigma, c_sab = (C)sc.c_sqrt_ab,
           c_sabp = (C)sc.c_sqrt_ab_prev, c_s1m = (C)sc.c_sqrt_1m_ab_prev, dt = (C)sc.dt;

@@ -239,6 +239,7 @@ class _StepRunner:
         else:
             K.ctrl_init(self.ctrl, 1, 1.0, plan.schedule.T, 0, plan.schedule.T)
         self.mirror = K.PinnedMirror()
+        self._sw = sw
         T = plan.schedule.T
         if plan.sampler == "euler":
             self.coef = {t: None for t in range(1, T + 1)}
@@ -247,6 +248,18 @@ class _StepRunner:
         else:
             self.coef = {t: StepCoefficients.ddim(plan.schedule, t) for t in range(1, T + 1)}
         self.update = N.HP_UPDATE_EULER if plan.sampler == "euler" else N.HP_UPDATE_DDIM
+
+    def reset(self):
+        """Fresh controller + mirror for another run on the same runner."""
+        torch.cuda.synchronize()
+        T = self.plan.schedule.T
+        sw = self._sw
+        if sw is not None:
+            K.ctrl_init(self.ctrl, sw.L, sw.g_slope, sw.tau_cap, sw.k, T)
+        else:
+            K.ctrl_init(self.ctrl, 1, 1.0, T, 0, T)
+        self.mirror.view.seq = -1
+        torch.cuda.synchronize()
 
     def upload(self, x_host):
         if isinstance(x_host, torch.Tensor):

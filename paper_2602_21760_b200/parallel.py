@@ -158,6 +158,12 @@ class CudaPairOps:
         self.buf = PeerBuffers(self.numel, esz, group, role.peer_rank) if exchange == "p2p" else None
         self.msgs = []        # (kind, nbytes, step)
         self.lib = N.load()
+        self.seq0 = 0         # flag value offset of the current run
+
+    def begin_run(self, seq0: int):
+        self.seq0 = seq0
+        self.msgs = []
+        self.st.reset()
 
     # ---- branch evaluation ----
     def upload(self, x_init):
@@ -178,12 +184,13 @@ class CudaPairOps:
         self.msgs.append((kind, nbytes, s))
         if self.kind == "p2p":
             flag_idx = self.role.role            # my slot in the partner's flag words
-            check(self.lib.hp_stage_send(C.c_void_p(self.buf.peer_slot(s)), C.c_void_p(e.data_ptr()), nbytes,
-                                         C.c_void_p(self.buf.peer_flags + 4 * flag_idx), s,
+            q = self.seq0 + s                     # global message sequence number
+            check(self.lib.hp_stage_send(C.c_void_p(self.buf.peer_slot(q)), C.c_void_p(e.data_ptr()), nbytes,
+                                         C.c_void_p(self.buf.peer_flags + 4 * flag_idx), q,
                                          C.c_void_p(N.stream_ptr())), "hp_stage_send")
-            peer = _Raw(self.buf.local_slot(s), e.numel(), e.dtype, e.device)
+            peer = _Raw(self.buf.local_slot(q), e.numel(), e.dtype, e.device)
             wait = self.buf.flags + 4 * (1 - self.role.role)
-            return (peer, wait, s)
+            return (peer, wait, q)
         import torch.distributed as dist
         other = torch.empty_like(e)
         ops = [dist.P2POp(dist.isend, e.contiguous(), self.role.peer_rank, self.group),
@@ -226,39 +233,57 @@ class CudaPairOps:
         return self.st.finish(x)
 
 
+class PairSession:
+    """Set up a pair once (IPC buffers, graphs, controller) and run it repeatedly.
+
+    Flag values are a monotonically increasing message sequence across runs
+    (run r, step s -> r*T + s), so a new run can never consume a flag left
+    over from the previous one."""
+
+    def __init__(self, plan: ExecutionPlan, group=None, exchange: str = "p2p"):
+        import torch.distributed as dist
+        if plan.variant not in (PlanVariant.FULL_CONDITION_PARTITION, PlanVariant.HYBRID):
+            raise PlanError(f"a pair runs condition-partitioned plans, got {plan.variant.value}")
+        self.plan, self.group = plan, group
+        self.role = pair_role(dist.get_rank())
+        self.ops = CudaPairOps(plan, self.role, group, exchange)
+        self.runs = 0
+
+    def run(self, x_init=None) -> RunResult:
+        import torch.distributed as dist
+        plan, ops, role = self.plan, self.ops, self.role
+        ops.begin_run(self.runs * plan.schedule.T)
+        self.runs += 1
+        loop = PairLoop(plan, role, ops)
+        dist.barrier(self.group)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        x0, series, tau1, tau2, stages = loop.run(initial_latents(plan) if x_init is None else x_init)
+        b.record()
+        torch.cuda.synchronize()
+        mine = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
+        dist.all_reduce(mine, op=dist.ReduceOp.MAX, group=self.group)
+        latency = float(mine.item())
+        trace = RunTrace()
+        me = plan.devices[role.role].name
+        trace.busy.append(BusyInterval(me, 0.0, latency, plan.schedule.T, "", "run"))
+        peer_name = plan.devices[1 - role.role].name
+        for kind, nb, s in ops.msgs:
+            trace.messages.append(MessageEvent(me, peer_name, kind, nb, 0.0, 0.0, s))
+        comm = 2 * sum(nb for _, nb, _ in ops.msgs)     # both directions of the pair
+        ref = serial_latency_ref(plan)
+        return RunResult(x0=x0, latency_s=latency, comm_bytes=comm, speedup=ref / latency,
+                         throughput_samples_per_s=1.0 / latency, tau1=tau1, tau2=tau2, trace=trace,
+                         series=series, stages=tuple(stages))
+
+
 def run_pair(plan: ExecutionPlan, group=None, exchange: str = "p2p") -> RunResult:
     """Execute a FULL_CONDITION_PARTITION or HYBRID plan on this rank's pair.
 
     Every rank of the pair calls this with the same plan; both return the same
     x0 and series. latency_s is the max over the pair of the device time."""
-    import torch.distributed as dist
-    if plan.variant not in (PlanVariant.FULL_CONDITION_PARTITION, PlanVariant.HYBRID):
-        raise PlanError(f"run_pair runs condition-partitioned plans, got {plan.variant.value}")
-    rank = dist.get_rank()
-    role = pair_role(rank)
-    ops = CudaPairOps(plan, role, group, exchange)
-    loop = PairLoop(plan, role, ops)
-    dist.barrier(group)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    x0, series, tau1, tau2, stages = loop.run(initial_latents(plan))
-    b.record()
-    torch.cuda.synchronize()
-    mine = torch.tensor([a.elapsed_time(b) / 1e3], dtype=torch.float64, device="cuda")
-    dist.all_reduce(mine, op=dist.ReduceOp.MAX, group=group)
-    latency = float(mine.item())
-    trace = RunTrace()
-    me = plan.devices[role.role].name
-    trace.busy.append(BusyInterval(me, 0.0, latency, plan.schedule.T, "", "run"))
-    peer_name = plan.devices[1 - role.role].name
-    for kind, nb, s in ops.msgs:
-        trace.messages.append(MessageEvent(me, peer_name, kind, nb, 0.0, 0.0, s))
-    comm = 2 * sum(nb for _, nb, _ in ops.msgs)     # both directions of the pair
-    ref = serial_latency_ref(plan)
-    return RunResult(x0=x0, latency_s=latency, comm_bytes=comm, speedup=ref / latency,
-                     throughput_samples_per_s=1.0 / latency, tau1=tau1, tau2=tau2, trace=trace,
-                     series=series, stages=tuple(stages))
+    return PairSession(plan, group, exchange).run()
 
 
 def run_batch_level_distributed(plan: ExecutionPlan, exchange: str = "p2p") -> RunResult:
