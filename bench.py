@@ -6,10 +6,11 @@ One bench "step" is one complete 50-step classifier-free-guided generation of
 one 1024^2 image (128x128x4 latent) with a random-init SDXL-shaped U-Net
 (2.57 B parameters) on this package's sm_100a kernels, driven through the
 drop-in ``run_plan`` API. At N=1 the plan is ``serial`` (both guidance
-branches on one GPU, batched); at N>1 each GPU pair runs one image
-(``--mode pairs``, condition partitioning over NVLink) or every GPU runs its
-own image (``--mode replicas``, the default until the pair path has been
-validated on multi-GPU hardware).
+branches on one GPU, batched); at N>1 each GPU pair runs one image with the
+hybrid plan (``--mode pairs``, the default: condition partitioning with the
+branch exchange fused into the sampler kernel over NVLink) or every GPU runs
+its own image (``--mode replicas``). If the pair path fails the line says so
+(``config.mode_note``) and reports replicas instead.
 
 Printed JSON (rank 0, one line): ``value`` = device-resident seconds per image
 for the whole job (inputs resident, no host copies); ``e2e`` = the same metric
