@@ -168,3 +168,40 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def gen_cli():
+    """Reference CLI outputs (cli.py:44-228) for the harness parity tests."""
+    import contextlib
+    import io
+    import shutil
+    hp = _ref()
+    from hybridpar import cli
+    d = OUT / "cli"
+    if d.exists():
+        shutil.rmtree(d)
+    d.mkdir(parents=True)
+    small = {"condition_batch": 4, "seeds": [0, 1], "schedule": {"T": 12}, "switch": {"L": 2, "tau_cap": 3, "k": 4}}
+    (d / "small.json").write_text(json.dumps(small))
+    runs = {
+        "simulate": ["simulate", "--out", str(d / "sim")],
+        "curve": ["curve", "--out", str(d / "curve.csv")],
+        "sweep": ["sweep", "--k", "0,5,10,40", "--out", str(d / "sweep.csv")],
+        "sweep_small": ["sweep", "--config", str(d / "small.json"), "--k", "0,2,4,9"],
+    }
+    outs = {}
+    for name, argv in runs.items():
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            assert cli.main(argv) == 0, name
+        outs[name] = buf.getvalue()
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        assert cli.main(["detect", "--series", str(d / "curve.csv")]) == 0
+    outs["detect"] = buf.getvalue()
+    (d / "stdout.json").write_text(json.dumps(outs, indent=1))
+    _ = hp
+
+
+if __name__ == "__main__" and "--cli" in sys.argv:
+    gen_cli()
