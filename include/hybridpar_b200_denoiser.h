@@ -51,6 +51,7 @@ typedef struct hp_gemm_desc {
      * D, residual and colscale (0 = shared). batch <= 1 = ordinary GEMM.    */
     int32_t batch;
     int64_t a_bstride, d_bstride, r_bstride, cs_bstride;
+    int64_t bias2_ld;                          /* row stride of bias2 (0 = N)    */
 } hp_gemm_desc;
 
 int hp_gemm(const hp_gemm_desc* d, void* stream);

@@ -46,7 +46,7 @@ struct GemmParams {
   int num_m_tiles, num_n_tiles;
   __nv_bfloat16* d; long long ldd;
   const float* bias;
-  const float* bias2; long long bias2_div;
+  const float* bias2; long long bias2_div; long long bias2_ld;
   const __nv_bfloat16* res; long long ldr;
   int act;
   float alpha;
@@ -292,7 +292,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const long long img = p.batch > 1 ? (long long)bt : (long long)(m0 / p.bias2_div);
         for (int i = et; i < BN; i += 128) {
           float b = p.bias ? __ldg(p.bias + n0 + i) : 0.0f;
-          if (p.bias2) b += __ldg(p.bias2 + img * p.N + n0 + i);
+          if (p.bias2) b += __ldg(p.bias2 + img * p.bias2_ld + n0 + i);
           sb[i] = b;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -422,6 +422,7 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   p.mode = d->a_mode;
   p.d = static_cast<__nv_bfloat16*>(d->d); p.ldd = d->ldd;
   p.bias = d->bias; p.bias2 = d->bias2; p.bias2_div = d->bias2_div > 0 ? d->bias2_div : 1;
+  p.bias2_ld = d->bias2_ld > 0 ? d->bias2_ld : d->N;
   if (d->bias2 && (p.bias2_div % BM)) return HP_ERR_UNSUPPORTED;   // one image per 128-row tile
   p.res = static_cast<const __nv_bfloat16*>(d->residual); p.ldr = d->ldr;
   p.act = d->act;

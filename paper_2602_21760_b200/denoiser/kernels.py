@@ -46,6 +46,7 @@ class HpGemmDesc(C.Structure):
         ("colscale", _VP),
         ("batch", _I32),
         ("a_bstride", _I64), ("d_bstride", _I64), ("r_bstride", _I64), ("cs_bstride", _I64),
+        ("bias2_ld", _I64),
     ]
 
 
@@ -151,6 +152,7 @@ def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, a
     d.M, d.N, d.K = M, Nn, K
     d.bias = _p(bias)
     d.bias2, d.bias2_div = _p(bias2), int(bias2_div)
+    d.bias2_ld = bias2.stride(0) if (bias2 is not None and bias2.dim() == 2) else 0
     d.residual = _p(residual)
     d.ldr = residual.stride(-2) if residual is not None else 0
     d.act, d.block_n, d.alpha = int(act), int(block_n), float(alpha)

@@ -75,10 +75,11 @@ class _ResBlock:
         self.tproj = _Lin(W, name + ".time_emb_proj", dev=dev)
         self.short = _Conv(W, name + ".conv_shortcut", dev) if (name + ".conv_shortcut.weight") in W else None
 
-    def __call__(self, x, n, h, w, temb, groups, stats):
+    def __call__(self, x, n, h, w, tb, groups, stats):
+        """tb: this block's time-embedding bias [n, co] (a column slice of the
+        UNet's single batched projection of SiLU(temb))."""
         ci, co = self.c1.ci, self.c1.co
         hw = h * w
-        tb = K.linear_small(temb, self.tproj.w, self.tproj.b, act_in=K.ACT_SILU)   # [n, co]
         y = K.group_norm(x, n, hw, ci, self.n1.g, self.n1.b, groups=groups, silu=True, stats=stats)
         y = self.c1(y, n, h, w, bias2=tb, bias2_div=hw)
         y = K.group_norm(y, n, hw, co, self.n2.g, self.n2.b, groups=groups, silu=True, stats=stats)
@@ -186,6 +187,18 @@ class UNet:
         self.stats = torch.empty(2 * 64 * 64 * 32, dtype=torch.float32, device=dev)
         self.aug = {}
         self.ctx_len = s.context_len
+        # every ResBlock's time_emb_proj(SiLU(temb)) as ONE small GEMV per forward
+        blocks = [r for res, _, _ in self.down for r in res] + [self.mid[0], self.mid[2]] + \
+                 [r for res, _, _ in self.up for r in res]
+        offs, o = [], 0
+        for r in blocks:
+            offs.append(o)
+            o += r.c1.co
+        self.tproj_w = torch.cat([r.tproj.w for r in blocks]).contiguous()
+        self.tproj_b = torch.cat([r.tproj.b for r in blocks]).contiguous()
+        self.tproj_slot = {id(r): (off, r.c1.co) for r, off in zip(blocks, offs)}
+        for r in blocks:
+            r.tproj = None
 
     def _transformers(self):
         for res, att, _ in self.down + self.up:
@@ -221,12 +234,17 @@ class UNet:
         te = K.linear_small(te, self.t1.w, self.t1.b, act_out=K.ACT_SILU)
         temb = K.linear_small(te, self.t2.w, self.t2.b)
         temb = temb + self.aug[key]                    # tiny [n, 1280] add
+        tb_all = K.linear_small(temb, self.tproj_w, self.tproj_b, act_in=K.ACT_SILU)   # [n, sum(co)]
+
+        def tb(r):
+            off, co = self.tproj_slot[id(r)]
+            return tb_all[:, off:off + co]             # row stride sum(co): GEMM bias2_ld
         h = K.conv3x3_small(x, n, H, Wd, s.in_channels, self.conv_in_w, self.conv_in_b, s.block_out[0])
         skips = [h]
         hh, ww = H, Wd
         for res, att, ds in self.down:
             for r, a in zip(res, att):
-                h = r(h, n, hh, ww, temb, g, st)
+                h = r(h, n, hh, ww, tb(r), g, st)
                 if a is not None:
                     h = a(h, n, hh * ww, g, st, self.ctx_len, key)
                 skips.append(h)
@@ -235,14 +253,14 @@ class UNet:
                 hh, ww = hh // 2, ww // 2
                 skips.append(h)
         r0, tr, r1 = self.mid
-        h = r0(h, n, hh, ww, temb, g, st)
+        h = r0(h, n, hh, ww, tb(r0), g, st)
         h = tr(h, n, hh * ww, g, st, self.ctx_len, key)
-        h = r1(h, n, hh, ww, temb, g, st)
+        h = r1(h, n, hh, ww, tb(r1), g, st)
         for res, att, us in self.up:
             for r, a in zip(res, att):
                 sk = skips.pop()
                 cat = K.concat_channels(h, h.shape[1], sk, sk.shape[1], n * hh * ww)
-                h = r(cat, n, hh, ww, temb, g, st)
+                h = r(cat, n, hh, ww, tb(r), g, st)
                 if a is not None:
                     h = a(h, n, hh * ww, g, st, self.ctx_len, key)
             if us is not None:

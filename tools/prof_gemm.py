@@ -1,6 +1,7 @@
-"""Time one GEMM shape through hp_gemm (for ncu captures / quick sweeps).
+"""Time one GEMM shape through hp_gemm, back-to-back inside a CUDA graph (no host
+overhead, PDL between launches), for quick sweeps and ncu targets.
 
-    python tools/prof_gemm.py M N K [block_n] [act] [reps]
+    python tools/prof_gemm.py M N K [block_n] [act] [reps] [eager]
 """
 import sys
 
@@ -15,6 +16,7 @@ def main():
     bn = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     act = int(sys.argv[5]) if len(sys.argv) > 5 else 0
     reps = int(sys.argv[6]) if len(sys.argv) > 6 else 20
+    eager = len(sys.argv) > 7 and sys.argv[7] == "eager"
     a = torch.randn(M, Kd, device="cuda").bfloat16()
     w = (torch.randn(N, Kd, device="cuda") * Kd ** -0.5).bfloat16()
     bias = torch.randn(N, device="cuda")
@@ -23,14 +25,24 @@ def main():
     for _ in range(3):
         run()
     torch.cuda.synchronize()
+    if eager:
+        body = lambda: [run() for _ in range(reps)]  # noqa: E731
+    else:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                run()
+        body = g.replay
+    body()
+    torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for _ in range(reps):
-        run()
+    body()
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
-    print(f"gemm M={M} N={N} K={Kd} bn={bn} act={act}: {ms * 1e3:.1f} us {2.0 * M * N * Kd / ms / 1e9:.1f} TFLOP/s")
+    print(f"gemm M={M} N={N} K={Kd} bn={bn} act={act} {'eager' if eager else 'graph'}: "
+          f"{ms * 1e3:.1f} us {2.0 * M * N * Kd / ms / 1e9:.1f} TFLOP/s")
 
 
 if __name__ == "__main__":
