@@ -52,6 +52,12 @@ typedef struct hp_gemm_desc {
     int32_t batch;
     int64_t a_bstride, d_bstride, r_bstride, cs_bstride;
     int64_t bias2_ld;                          /* row stride of bias2 (0 = N)    */
+    /* fused LayerNorm of the output rows (ln_y != NULL): also writes
+     * ln_y = LayerNorm(d) with gamma/beta [N] fp32; the N tiles of each
+     * 128-row block run as one thread-block cluster and combine their
+     * row partial sums through distributed shared memory (N/block_n <= 8). */
+    const float* ln_gamma; const float* ln_beta; float ln_eps;
+    void* ln_y; int64_t ldy;
 } hp_gemm_desc;
 
 int hp_gemm(const hp_gemm_desc* d, void* stream);

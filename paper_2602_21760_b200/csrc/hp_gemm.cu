@@ -47,6 +47,10 @@ struct GemmParams {
   __nv_bfloat16* d; long long ldd;
   const float* bias;
   const float* bias2; long long bias2_div; long long bias2_ld;
+  // fused LayerNorm of the output rows (cluster of all N tiles of a 128-row block)
+  int ln_mode;
+  const float* ln_g; const float* ln_b; float ln_eps;
+  __nv_bfloat16* ln_y; long long ldy;
   const __nv_bfloat16* res; long long ldr;
   int act;
   float alpha;
@@ -57,6 +61,12 @@ struct GemmParams {
 
 template <int BN>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& b, int& m0, int& n0) {
+  if (p.ln_mode) {             // one cluster = every N tile of one 128-row block
+    b = 0;
+    m0 = (tile / p.num_n_tiles) * BM;
+    n0 = (tile % p.num_n_tiles) * BN;
+    return;
+  }
   const int mt_all = p.num_m_tiles * p.batch;
   const int mt = tile % mt_all;
   b = mt / p.num_m_tiles;
@@ -71,7 +81,7 @@ __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)
 // column bias (bias + per-image bias2 folded) staged in shared memory, or null.
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
-                                              int lane, const float* sb) {
+                                              int lane, const float* sb, float* row_stats) {
   const int row = m0 + quarter * 32 + lane;
   const bool row_ok = row < p.M;
   const uint32_t lane_addr = tmem_acc + ((uint32_t)(quarter * 32) << 16);
@@ -110,6 +120,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
   const bool has_res = p.res != nullptr && row_ok;
   const uint4* res_row = has_res ? reinterpret_cast<const uint4*>(p.res + (long long)row * p.ldr + n0) : nullptr;
   uint4 rn[4];
+  float st_sum = 0.f, st_sq = 0.f;            // LayerNorm partials of the stored (bf16) row
   if (has_res) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) rn[q] = res_row[q];
@@ -165,9 +176,85 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     }
     uint4* dst = reinterpret_cast<uint4*>(p.d + (long long)row * p.ldd + col);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      dst[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                          pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+    for (int q = 0; q < 4; ++q) {
+      const uint4 u = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                 pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+      dst[q] = u;
+      if (row_stats) {
+        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = unpack_bf16(w4[e]);
+          st_sum += f.x + f.y;
+          st_sq = fmaf(f.x, f.x, fmaf(f.y, f.y, st_sq));
+        }
+      }
+    }
+  }
+  if (row_stats) {
+    row_stats[0] = st_sum;
+    row_stats[1] = st_sq;
+  }
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+// Second pass of the fused LayerNorm: row statistics of the full N from every
+// CTA of the cluster (DSMEM), then y = (h - mean) * rstd * gamma + beta on this
+// CTA's N tile, re-reading the h values this very thread just stored.
+template <int BN>
+__device__ __forceinline__ void ln_pass2(const GemmParams& p, int m0, int n0, int quarter, int lane,
+                                         const float* s_stats) {
+  const int row = m0 + quarter * 32 + lane;
+  if (row >= p.M) return;
+  uint32_t ncta;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta));
+  const int r = quarter * 32 + lane;
+  float ps[8], pq[8];
+#pragma unroll
+  for (uint32_t c = 0; c < 8; ++c) {               // independent DSMEM loads, all in flight
+    ps[c] = c < ncta ? ld_dsmem_f32(s_stats + 2 * r, c) : 0.f;
+    pq[c] = c < ncta ? ld_dsmem_f32(s_stats + 2 * r + 1, c) : 0.f;
+  }
+  float sum = 0.f, sq = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) { sum += ps[c]; sq += pq[c]; }
+  const float mean = sum / (float)p.N;
+  const float var = fmaxf(sq / (float)p.N - mean * mean, 0.f);
+  const float rstd = rsqrtf(var + p.ln_eps);
+  const uint4* src = reinterpret_cast<const uint4*>(p.d + (long long)row * p.ldd + n0);
+  uint4* dst = reinterpret_cast<uint4*>(p.ln_y + (long long)row * p.ldy + n0);
+  constexpr int kG = 4;                              // 4 x 16 B of h in flight per round trip
+  static_assert((BN / 8) % kG == 0, "BN/8 must be a multiple of the load group");
+#pragma unroll 1
+  for (int q0 = 0; q0 < BN / 8; q0 += kG) {
+    uint4 u[kG];
+#pragma unroll
+    for (int i = 0; i < kG; ++i) u[i] = src[q0 + i];
+#pragma unroll
+    for (int i = 0; i < kG; ++i) {
+      const int q = q0 + i;
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(p.ln_g + n0 + q * 8));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(p.ln_g + n0 + q * 8 + 4));
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.ln_b + n0 + q * 8));
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.ln_b + n0 + q * 8 + 4));
+      const float2 x0 = unpack_bf16(u[i].x), x1 = unpack_bf16(u[i].y), x2 = unpack_bf16(u[i].z),
+                   x3 = unpack_bf16(u[i].w);
+      dst[q] = make_uint4(pack_bf16((x0.x - mean) * rstd * g0.x + b0.x, (x0.y - mean) * rstd * g0.y + b0.y),
+                          pack_bf16((x1.x - mean) * rstd * g0.z + b0.z, (x1.y - mean) * rstd * g0.w + b0.w),
+                          pack_bf16((x2.x - mean) * rstd * g1.x + b1.x, (x2.y - mean) * rstd * g1.y + b1.y),
+                          pack_bf16((x3.x - mean) * rstd * g1.z + b1.z, (x3.y - mean) * rstd * g1.w + b1.w));
+    }
   }
 }
 
@@ -189,6 +276,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* sbias = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);   // [2][BN]
+  float* s_stats = sbias + 2 * BN;                                               // [128][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_tiles = p.num_m_tiles * p.batch * p.num_n_tiles;
@@ -304,14 +392,25 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         q.d += (long long)bt * p.d_bs;
         if (q.res) q.res += (long long)bt * p.r_bs;
         if (q.colscale) q.colscale += (long long)bt * p.cs_bs;
-        epilogue_tile<BN>(q, tmem_base + acc * BN, m0, n0, quarter, lane, sb);
+        epilogue_tile<BN>(q, tmem_base + acc * BN, m0, n0, quarter, lane, sb, nullptr);
       } else {
-        epilogue_tile<BN>(p, tmem_base + acc * BN, m0, n0, quarter, lane, sb);
+        epilogue_tile<BN>(p, tmem_base + acc * BN, m0, n0, quarter, lane, sb,
+                          p.ln_mode ? s_stats + 2 * (quarter * 32 + lane) : nullptr);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+  }
+  if (p.ln_mode) {
+    // every CTA of the cluster has published its per-row partial sums
+    cluster_sync_all();
+    if (warp >= 4) {
+      int bt, m0, n0;
+      decode_tile<BN>(p, blockIdx.x, bt, m0, n0);
+      ln_pass2<BN>(p, m0, n0, warp & 3, lane, s_stats);
+    }
+    cluster_sync_all();   // nobody leaves while a peer may still read its partials
   }
   tc_fence_before();
   __syncthreads();
@@ -365,7 +464,8 @@ int num_sms() {
 
 template <int BN, int STAGES>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
-  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + BN * BK * 2) + 256 + 2 * BN * sizeof(float);
+  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + BN * BK * 2) + 256 + 2 * BN * sizeof(float) +
+                         2 * BM * sizeof(float);
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -374,6 +474,25 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& 
     attr_set = true;
   }
   const int tiles = p.num_m_tiles * p.batch * p.num_n_tiles;
+  if (p.ln_mode) {
+    // non-persistent: one CTA per tile, a cluster spans the N tiles of a row block
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tiles);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.num_n_tiles;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = hp_pdl_enabled() ? 2 : 1;
+    if (cudaLaunchKernelEx(&cfg, gemm_kernel<BN, STAGES>, ta, tb, p) != cudaSuccess) return HP_ERR_CUDA;
+    return HP_OK;
+  }
   const int grid = tiles < num_sms() ? tiles : num_sms();
   if (hp_launch_pdl(gemm_kernel<BN, STAGES>, dim3(grid), dim3(kThreads), smem, st, ta, tb, p) != cudaSuccess)
     return HP_ERR_CUDA;
@@ -430,11 +549,18 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if (d->colscale && (reinterpret_cast<uintptr_t>(d->colscale) & 15)) return HP_ERR_UNSUPPORTED;
   p.alpha = d->alpha == 0.0f ? 1.0f : d->alpha;
   p.batch = d->batch > 1 ? d->batch : 1;
+  p.ln_mode = d->ln_y != nullptr;
+  p.ln_g = d->ln_gamma; p.ln_b = d->ln_beta; p.ln_eps = d->ln_eps;
+  p.ln_y = static_cast<__nv_bfloat16*>(d->ln_y); p.ldy = d->ldy;
+  if (p.ln_mode && (p.batch > 1 || d->act == HP_ACT_GEGLU || !d->ln_gamma || !d->ln_beta || (d->ldy % 8) ||
+                    (reinterpret_cast<uintptr_t>(d->ln_y) & 15)))
+    return HP_ERR_UNSUPPORTED;
   p.a_bs = d->a_bstride; p.d_bs = d->d_bstride; p.r_bs = d->r_bstride; p.cs_bs = d->cs_bstride;
   if (p.batch > 1 && d->a_mode != HP_A_PLAIN) return HP_ERR_UNSUPPORTED;
   if (p.batch > 1 && ((p.a_bs | p.d_bs | p.r_bs) % 8 || p.cs_bs % 4)) return HP_ERR_UNSUPPORTED;
   p.num_m_tiles = (int)((d->M + BM - 1) / BM);
   p.num_n_tiles = (int)(d->N / bn);
+  if (p.ln_mode && p.num_n_tiles > 8) return HP_ERR_UNSUPPORTED;     // portable cluster size
 
   CUtensorMap ta, tb;
   if (d->a_mode == HP_A_PLAIN) {

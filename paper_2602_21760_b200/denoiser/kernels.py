@@ -47,6 +47,7 @@ class HpGemmDesc(C.Structure):
         ("batch", _I32),
         ("a_bstride", _I64), ("d_bstride", _I64), ("r_bstride", _I64), ("cs_bstride", _I64),
         ("bias2_ld", _I64),
+        ("ln_gamma", _VP), ("ln_beta", _VP), ("ln_eps", _F32), ("ln_y", _VP), ("ldy", _I64),
     ]
 
 
@@ -96,7 +97,7 @@ def _bf16(t, name):
 
 
 def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, act=ACT_NONE,
-         alpha=1.0, block_n=0, conv=None, colscale=None):
+         alpha=1.0, block_n=0, conv=None, colscale=None, ln=None):
     """out[M, N'] = residual + colscale * act(alpha * A @ W^T + bias).
     ``conv=(n, h, w, c, stride)`` reads A as NHWC."""
     lib = N.load()
@@ -157,6 +158,10 @@ def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, a
     d.ldr = residual.stride(-2) if residual is not None else 0
     d.act, d.block_n, d.alpha = int(act), int(block_n), float(alpha)
     d.colscale = _p(colscale)
+    if ln is not None:
+        # ln = (gamma, beta, eps, y_out): also write y_out = LayerNorm(out) (fused epilogue)
+        g, b_, eps, y = ln
+        d.ln_gamma, d.ln_beta, d.ln_eps, d.ln_y, d.ldy = _p(g), _p(b_), float(eps), _p(y), y.stride(-2)
     check(lib.hp_gemm(C.byref(d), _s()), f"hp_gemm M={M} N={Nn} K={K}")
     return out
 

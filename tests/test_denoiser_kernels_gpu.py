@@ -193,3 +193,20 @@ def test_small_ops():
     ref = lat.view(2, 4, 2, 4, 2, 16).permute(0, 1, 3, 2, 4, 5).reshape(-1)
     assert torch.equal(tok, ref)
     assert torch.equal(K.patchify(tok, 2, 8, 8, 16, 2, inverse=True), lat.reshape(-1))
+
+
+@pytest.mark.parametrize("M,N,Kd,bn", [(2048, 1280, 1280, 160), (2048, 1280, 1280, 256), (8192, 640, 640, 160),
+                                       (300, 640, 320, 128), (256, 1536, 256, 256)])
+def test_gemm_fused_layernorm_cluster(M, N, Kd, bn):
+    """Residual GEMM + LayerNorm of its output rows in one launch (cluster DSMEM row sums)."""
+    torch.manual_seed(M + N)
+    a, w = rnd(M, Kd), rnd(N, Kd, s=Kd ** -0.5)
+    b = torch.randn(N, device="cuda")
+    h = rnd(M, N, s=2.0) + 0.3
+    h_ref = h.float() + a.float() @ w.float().t() + b
+    g, be = torch.randn(N, device="cuda"), torch.randn(N, device="cuda")
+    y = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    out = K.gemm(a, w, bias=b, residual=h, out=h, block_n=bn, ln=(g, be, 1e-5, y))
+    close(out, h_ref)
+    ref_y = F.layer_norm(out.float(), (N,), g, be, eps=1e-5)      # LN of the stored bf16 rows
+    close(y, ref_y, tol=2e-2)

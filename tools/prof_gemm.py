@@ -16,12 +16,18 @@ def main():
     bn = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     act = int(sys.argv[5]) if len(sys.argv) > 5 else 0
     reps = int(sys.argv[6]) if len(sys.argv) > 6 else 20
-    eager = len(sys.argv) > 7 and sys.argv[7] == "eager"
+    eager = "eager" in sys.argv[7:]
+    use_ln = "ln" in sys.argv[7:]
     a = torch.randn(M, Kd, device="cuda").bfloat16()
     w = (torch.randn(N, Kd, device="cuda") * Kd ** -0.5).bfloat16()
     bias = torch.randn(N, device="cuda")
     out = torch.empty(M, N // 2 if act == 3 else N, device="cuda", dtype=torch.bfloat16)
-    run = lambda: K.gemm(a, w, bias=bias, out=out, act=act, block_n=bn)  # noqa: E731
+    ln = None
+    if use_ln:
+        ln = (torch.ones(N, device="cuda"), torch.zeros(N, device="cuda"), 1e-5,
+              torch.empty(M, N, device="cuda", dtype=torch.bfloat16))
+    res = torch.randn(M, N, device="cuda").bfloat16() if use_ln else None
+    run = lambda: K.gemm(a, w, bias=bias, out=out, act=act, block_n=bn, residual=res, ln=ln)  # noqa: E731
     for _ in range(3):
         run()
     torch.cuda.synchronize()
@@ -42,7 +48,7 @@ def main():
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
     print(f"gemm M={M} N={N} K={Kd} bn={bn} act={act} {'eager' if eager else 'graph'}: "
-          f"{ms * 1e3:.1f} us {2.0 * M * N * Kd / ms / 1e9:.1f} TFLOP/s")
+          f"{' +LN' if use_ln else ''} {ms * 1e3:.1f} us {2.0 * M * N * Kd / ms / 1e9:.1f} TFLOP/s")
 
 
 if __name__ == "__main__":
