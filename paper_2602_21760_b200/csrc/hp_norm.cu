@@ -39,6 +39,12 @@ __device__ __forceinline__ void load8f(const float* p, float* v) {
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+// x * sigmoid(x) = 0.5 x (1 + tanh(x / 2)): one MUFU.TANH instead of EX2 + RCP
+__device__ __forceinline__ float silu_fast(float x) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+  return 0.5f * x * (1.0f + t);
+}
 
 inline int nblocks(int64_t work, int per_block, int cap = 148 * 16) {
   int64_t b = (work + per_block - 1) / per_block;
@@ -114,24 +120,37 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
   pdl_trigger();
   // per-channel affine folded once per block: y = x * sa[c] + sb[c]
   __shared__ float s_mean[64], s_rstd[64];
+  __shared__ double s_pa[kGnThreads], s_pb[kGnThreads];
   __shared__ __align__(16) float sa[kMaxC], sb[kMaxC];
   const int C = c1 + c2;
   const int V = C / 8;
   const int n = blockIdx.y;
   const int cg = C / groups;
-  if (threadIdx.x < groups) {
+  {
+    // fold the per-split partials: kGnThreads/groups threads per group, fixed order
+    const int per = kGnThreads / groups;
+    const int g = threadIdx.x % groups, k = threadIdx.x / groups;
     double a = 0.0, b = 0.0;
-    for (int s = 0; s < splits; ++s) {
-      const float* o = part + (((int64_t)n * splits + s) * groups + threadIdx.x) * 2;
-      a += (double)o[0];
-      b += (double)o[1];
+    if (k < per) {
+      for (int s = k; s < splits; s += per) {
+        const float* o = part + (((int64_t)n * splits + s) * groups + g) * 2;
+        a += (double)o[0];
+        b += (double)o[1];
+      }
     }
-    const double cnt = (double)hw * cg;
-    const double mean = a / cnt;
-    double var = b / cnt - mean * mean;
-    if (var < 0) var = 0;
-    s_mean[threadIdx.x] = (float)mean;
-    s_rstd[threadIdx.x] = (float)(1.0 / sqrt(var + (double)eps));
+    s_pa[threadIdx.x] = a;
+    s_pb[threadIdx.x] = b;
+    __syncthreads();
+    if (threadIdx.x < groups) {
+      double ta = 0.0, tb = 0.0;
+      for (int kk = 0; kk < per; ++kk) { ta += s_pa[kk * groups + threadIdx.x]; tb += s_pb[kk * groups + threadIdx.x]; }
+      const double cnt = (double)hw * cg;
+      const double mean = ta / cnt;
+      double var = tb / cnt - mean * mean;
+      if (var < 0) var = 0;
+      s_mean[threadIdx.x] = (float)mean;
+      s_rstd[threadIdx.x] = (float)(1.0 / sqrt(var + (double)eps));
+    }
   }
   __syncthreads();
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
@@ -141,26 +160,32 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
     sb[c] = beta[c] - s_mean[g] * a;
   }
   __syncthreads();
-  const int total = (int)(hw * V);                       // < 2^31 per image
+  // thread -> fixed 8-channel vector j, strided over pixels: no per-element index math
+  const int vc = V < kGnThreads ? V : kGnThreads;
+  const int rows = kGnThreads / vc;
+  const int r = threadIdx.x / vc;
   const bf16* xa = x1 + (int64_t)n * hw * c1;
   const bf16* xb = x2 ? x2 + (int64_t)n * hw * c2 : nullptr;
   bf16* yo = y + (int64_t)n * hw * C;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int p = i / V;
-    const int ch = (i - p * V) * 8;
-    float v[8];
-    if (ch < c1) load8(xa + (int64_t)p * c1 + ch, v);
-    else load8(xb + (int64_t)p * c2 + (ch - c1), v);
-    const float4 a0 = *reinterpret_cast<const float4*>(sa + ch), a1 = *reinterpret_cast<const float4*>(sa + ch + 4);
-    const float4 b0 = *reinterpret_cast<const float4*>(sb + ch), b1 = *reinterpret_cast<const float4*>(sb + ch + 4);
-    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+  if (r >= rows) return;
+  for (int j = threadIdx.x % vc; j < V; j += vc) {
+    const int ch = j * 8;
+    float av[8], bv[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float o = fmaf(v[k], av[k], bv[k]);
-      v[k] = do_silu ? silu(o) : o;
+    for (int k = 0; k < 8; ++k) { av[k] = sa[ch + k]; bv[k] = sb[ch + k]; }
+    const bool first = ch < c1;
+    const bf16* src = first ? xa + ch : xb + (ch - c1);
+    const int64_t sstride = first ? c1 : c2;
+    for (int64_t p = (int64_t)blockIdx.x * rows + r; p < hw; p += (int64_t)gridDim.x * rows) {
+      float v[8];
+      load8(src + p * sstride, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float o = fmaf(v[k], av[k], bv[k]);
+        v[k] = do_silu ? silu_fast(o) : o;
+      }
+      store8(yo + p * C + ch, v);
     }
-    store8(yo + (int64_t)p * C + ch, v);
   }
 }
 
@@ -511,15 +536,15 @@ int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_
   if (C % 8 || c1 % 8 || C > kMaxC || groups < 1 || groups > 64 || C % groups || n < 1 || hw < 1) return HP_ERR_SHAPE;
   if (!a16(x1) || (x2 && !a16(x2)) || !a16(y)) return HP_ERR_UNSUPPORTED;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int splits = (296 + n - 1) / n;
-  if (splits > hw) splits = (int)hw;
-  if (splits > 64) splits = 64;
+  // the pixel partition depends on hw only (never on the batch size n), so one
+  // image's statistics are bit-identical whatever else is in the batch
+  int splits = hw < 128 ? (int)hw : 128;
   hp_launch_pdl(gn_stats_kernel, dim3(splits, n), dim3(kGnThreads), 0, st, static_cast<const bf16*>(x1), c1,
                                                           static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups,
                                                           splits, stats);
   if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   const int64_t per_img = hw * (C / 8);
-  int chunks = nblocks(per_img, kGnThreads * 4, 4096);
+  int chunks = nblocks(per_img, kGnThreads * 8, 4096);
   hp_launch_pdl(gn_apply_kernel, dim3(chunks, n), dim3(kGnThreads), 0, st, static_cast<const bf16*>(x1), c1,
                                                           static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups,
                                                           splits, stats, eps, gamma, beta, do_silu,

@@ -186,7 +186,7 @@ def group_norm(x, n, hw, c, gamma, beta, *, groups=32, eps=1e-5, silu=False, x2=
     if out is None:
         out = torch.empty((n * hw, C_), dtype=torch.bfloat16, device=x.device)
     if stats is None:
-        stats = torch.empty(2 * n * groups * 64, dtype=torch.float32, device=x.device)
+        stats = torch.empty(2 * n * groups * 256, dtype=torch.float32, device=x.device)
     check(lib.hp_group_norm(_p(x), c, _p(x2), c2, n, hw, groups, eps, _p(gamma), _p(beta), int(silu),
                             _p(out), _p(stats), _s()), "hp_group_norm")
     return out
