@@ -71,6 +71,7 @@ extern "C" {
 #define HP_STAGE_FULLY_CONNECTING  2
 
 #define HP_MAX_T 1024   /* largest schedule length the device series holds */
+#define HP_MAX_PEERS 8  /* destinations of one hp_stage_broadcast (one NVLink domain of 8 GPUs) */
 
 /* Device-resident controller state: StageState (monitor.py:135-143) plus the
  * DiscrepancySeries values (monitor.py:65-100) indexed by timestep t, plus the
@@ -184,6 +185,16 @@ int hp_flag_wait(const volatile uint32_t* flag, uint32_t value,
  * engine.py:322-337 activation hand-off. */
 int hp_stage_send(void* dst, const void* src, int64_t nbytes, uint32_t* flag,
                   uint32_t value, void* stream);
+
+/* K3 fan-out: copy nbytes from src (local) to each of n_dst <= HP_MAX_PEERS
+ * destinations (peer-mapped pointers; `dsts` and `flags` are HOST arrays read
+ * at call time), then release *flags[i] = value for every non-NULL flag
+ * (flags itself may be NULL; with nbytes == 0 only the flags are released and
+ * dsts/src may be NULL). One launch per step for the layer-wise window,
+ * where every segment rank hands its contribution to all ranks
+ * (engine.py:330-337; the reference sends N-1 activations to device 0). */
+int hp_stage_broadcast(void* const* dsts, uint32_t* const* flags, int32_t n_dst, const void* src,
+                       int64_t nbytes, uint32_t value, void* stream);
 
 /* Zero-filled device allocation with an exact base pointer (IPC-exportable
  * exchange buffers and flag words); hp_free releases it. Not for the hot loop. */

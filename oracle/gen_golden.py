@@ -117,6 +117,7 @@ def gen_loops(hp):
         ("hybrid", {"condition_batch": 4, "schedule": {"T": 10},
                     "switch": {"L": 2, "tau_cap": 3, "k": 4}}, [2]),
         ("full_condition_partition", {"link": {"base_latency_s": 0.00995}}, [0]),
+        ("layer_wise", {"devices": 3}, [7]),
     ]
     for variant, over, seeds in spec:
         for seed in seeds:

@@ -16,6 +16,8 @@ from pathlib import Path
 from .errors import NativeError, check
 
 _LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhybridpar_b200.so"
+if os.environ.get("HP_LIB_VARIANT"):          # A/B kernel experiments (tools/): lib/<variant>.so
+    _LIB_PATH = _LIB_PATH.parent / (os.environ["HP_LIB_VARIANT"] + ".so")
 _lock = threading.Lock()
 _lib = None
 
@@ -25,6 +27,7 @@ HP_UPDATE_DDIM, HP_UPDATE_EULER, HP_UPDATE_NONE = 0, 1, 2
 HP_CTRL_NONE, HP_CTRL_RECORD, HP_CTRL_RECORD_UPDATE = 0, 1, 2
 HP_STAGE_WARM_UP, HP_STAGE_PARALLELISM, HP_STAGE_FULLY_CONNECTING = 0, 1, 2
 HP_MAX_T = 1024
+HP_MAX_PEERS = 8
 HP_IPC_HANDLE_BYTES = 64
 
 
@@ -85,6 +88,7 @@ SIGNATURES = {
     "hp_signal": (C.c_int, [_VP, _U32, _VP]),
     "hp_flag_wait": (C.c_int, [_VP, _U32, _VP, C.c_uint64, _VP]),
     "hp_stage_send": (C.c_int, [_VP, _VP, _I64, _VP, _U32, _VP]),
+    "hp_stage_broadcast": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int32, _VP, _I64, _U32, _VP]),
     "hp_alloc": (C.c_int, [_I64, C.POINTER(C.c_void_p)]),
     "hp_free": (C.c_int, [_VP]),
     "hp_version": (C.c_char_p, []),

@@ -42,6 +42,31 @@ __global__ void stage_copy_kernel(int4* __restrict__ dst, const int4* __restrict
   if (blockIdx.x == 0 && threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
 }
 
+struct PeerPtrs {
+  int4* dst[HP_MAX_PEERS];
+  uint32_t* flag[HP_MAX_PEERS];
+};
+
+// one copy per destination (blockIdx.y); the source tile is read once per
+// destination but stays in L2, so HBM sees ~one read and the NVLink ports
+// carry the n_dst writes concurrently
+__global__ void broadcast_copy_kernel(PeerPtrs p, const int4* __restrict__ src, int64_t n16,
+                                      const uint8_t* src_tail, int tail) {
+  int4* dst = p.dst[blockIdx.y];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    dst[i] = src[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x < tail)
+    reinterpret_cast<uint8_t*>(dst + n16)[threadIdx.x] = src_tail[threadIdx.x];
+}
+
+__global__ void broadcast_signal_kernel(PeerPtrs p, int n, uint32_t value) {
+  __threadfence_system();
+  for (int i = 0; i < n; ++i)
+    if (p.flag[i]) hp_st_release_sys_u32(p.flag[i], value);
+}
+
 }  // namespace
 
 extern "C" {
@@ -109,6 +134,40 @@ int hp_stage_send(void* dst, const void* src, int64_t nbytes, uint32_t* flag, ui
     if (cudaGetLastError() != cudaSuccess) return HP_ERR_CUDA;
   }
   if (flag) return hp_signal(flag, value, stream);
+  return HP_OK;
+}
+
+int hp_stage_broadcast(void* const* dsts, uint32_t* const* flags, int32_t n_dst, const void* src,
+                       int64_t nbytes, uint32_t value, void* stream) {
+  if (n_dst < 0 || n_dst > HP_MAX_PEERS || nbytes < 0) return HP_ERR_PARAMETER;
+  if (n_dst == 0) return HP_OK;
+  if (nbytes > 0 && (!src || !dsts)) return HP_ERR_PARAMETER;
+  PeerPtrs p{};
+  uintptr_t align = reinterpret_cast<uintptr_t>(src);
+  for (int i = 0; i < n_dst; ++i) {
+    p.flag[i] = flags ? flags[i] : nullptr;
+    if (nbytes == 0) continue;                 // signal-only (acknowledgements)
+    if (!dsts[i]) return HP_ERR_PARAMETER;
+    p.dst[i] = static_cast<int4*>(dsts[i]);
+    align |= reinterpret_cast<uintptr_t>(dsts[i]);
+  }
+  if (align & 15) return HP_ERR_UNSUPPORTED;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (nbytes > 0) {
+    const int64_t n16 = nbytes / 16;
+    const int tail = (int)(nbytes - n16 * 16);
+    int bx = (int)((n16 + 255) / 256);
+    if (bx < 1) bx = 1;
+    const int cap = (148 * 4 + n_dst - 1) / n_dst;
+    if (bx > cap) bx = cap;
+    broadcast_copy_kernel<<<dim3(bx, n_dst), 256, 0, st>>>(p, static_cast<const int4*>(src), n16,
+                                                           static_cast<const uint8_t*>(src) + n16 * 16, tail);
+    if (cudaGetLastError() != cudaSuccess) return HP_ERR_CUDA;
+  }
+  if (flags) {
+    broadcast_signal_kernel<<<1, 1, 0, st>>>(p, n_dst, value);
+    if (cudaGetLastError() != cudaSuccess) return HP_ERR_CUDA;
+  }
   return HP_OK;
 }
 

@@ -1,13 +1,15 @@
-"""GPU (one device, two processes): the pair exchange mechanics for real.
+"""GPU (one device, three processes): the group exchange mechanics for real.
 
-Each rank exports its receive buffer and flag words by CUDA IPC
-(`hp_alloc` + `hp_ipc_get_handle`), opens the partner's (`hp_ipc_open`), and
-pushes a known branch output into the partner's buffer with `hp_stage_send`
-(vector stores through the mapped pointer + system-scope release of the step
-number). After a host barrier each rank checks the payload and the flag, then
-runs the fused sampler kernel with the in-kernel flag wait on an ALREADY
-released flag (so no kernel ever waits on another process's kernel — the
-rule for sharing one GPU) and the partner's data as eps_u, against torch.
+Each rank exports its receive buffers and flag words by CUDA IPC
+(`hp_alloc` + `hp_ipc_get_handle`), opens the others' (`hp_ipc_open`), and
+pushes a known branch output into every other rank's slot with ONE
+`hp_stage_broadcast` (vector stores through the mapped pointers + system-scope
+release of the message number into each destination's flag). Rank 2 (a passive
+layer-wise rank) also acknowledges to ranks 0 and 1. After a host barrier each
+rank checks payloads, flags and acks, then runs the fused sampler kernel with
+the in-kernel flag wait on ALREADY released flags (so no kernel ever waits on
+another process's kernel — the rule for sharing one GPU) and remote operands
+read from its receive buffer, against torch.
 """
 import os
 import socket
@@ -19,6 +21,12 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WORLD = 3
+
+
+def _payload(src, n):
+    g = torch.Generator(device="cuda").manual_seed(100 + src)
+    return torch.randn(n, device="cuda", generator=g).bfloat16()
 
 
 def _worker(rank, port, q):
@@ -26,49 +34,53 @@ def _worker(rank, port, q):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=2)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     torch.cuda.set_device(0)
     try:
         from paper_2602_21760_b200 import _kernels as K, _native as N
-        from paper_2602_21760_b200.parallel import PeerBuffers, _Raw
+        from paper_2602_21760_b200.parallel import GroupBuffers, _Raw
         lib = N.load()
         n = 65536 + 40
-        buf = PeerBuffers(n, 2, None, 1 - rank)
-        gen = torch.Generator(device="cuda").manual_seed(100 + rank)
-        mine = torch.randn(n, device="cuda", generator=gen).bfloat16()
+        buf = GroupBuffers(n, 2, None, rank, WORLD)
+        mine = _payload(rank, n)
         s = 7
-        # push my branch output into the partner's slot for step s and release the flag
-        rc = lib.hp_stage_send(C.c_void_p(buf.peer_slot(s)), C.c_void_p(mine.data_ptr()), n * 2,
-                               C.c_void_p(buf.peer_flags + 4 * rank), s, C.c_void_p(N.stream_ptr()))
+        others = [r for r in range(WORLD) if r != rank]
+        dsts = (C.c_void_p * len(others))(*[buf.peer_slot(r, s) for r in others])
+        flags = (C.c_void_p * len(others))(*[buf.peer_data_flag(r) for r in others])
+        rc = lib.hp_stage_broadcast(dsts, flags, len(others), C.c_void_p(mine.data_ptr()), n * 2, s,
+                                    C.c_void_p(N.stream_ptr()))
         assert rc == 0, rc
+        if rank == 2:       # passive rank: acknowledge message s to the branch ranks
+            acks = (C.c_void_p * 2)(buf.peer_ack_flag(0), buf.peer_ack_flag(1))
+            rc = lib.hp_stage_broadcast((C.c_void_p * 2)(0, 0), acks, 2, None, 0, s, C.c_void_p(N.stream_ptr()))
+            assert rc == 0, rc
         torch.cuda.synchronize()
         dist.barrier()
-        # what the partner pushed into MY slot
-        other = torch.randn(n, device="cuda", generator=torch.Generator(device="cuda").manual_seed(100 + 1 - rank)).bfloat16()
-        got = torch.empty(n, dtype=torch.bfloat16, device="cuda")
-        cp = torch.cuda.current_stream()
-        rc = lib.hp_stage_send(C.c_void_p(got.data_ptr()), C.c_void_p(buf.local_slot(s)), n * 2, None, 0,
-                               C.c_void_p(cp.cuda_stream))
-        assert rc == 0
-        flags = torch.zeros(4, dtype=torch.int32, device="cuda")
-        rc = lib.hp_stage_send(C.c_void_p(flags.data_ptr()), C.c_void_p(buf.flags), 16, None, 0,
-                               C.c_void_p(cp.cuda_stream))
-        assert rc == 0
-        ok_payload = bool(torch.equal(got, other))
-        ok_flag = int(flags[1 - rank].item()) == s
-        # fused sampler with the in-kernel flag acquire (flag already released) and the
-        # partner's data read straight from this rank's receive buffer
+        st = C.c_void_p(N.stream_ptr())
+        ok_payload = True
+        for src in others:
+            got = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+            assert lib.hp_stage_send(C.c_void_p(got.data_ptr()), C.c_void_p(buf.local_slot(src, s)), n * 2,
+                                     None, 0, st) == 0
+            ok_payload &= bool(torch.equal(got, _payload(src, n)))
+        fl = torch.zeros(16, dtype=torch.int32, device="cuda")
+        assert lib.hp_stage_send(C.c_void_p(fl.data_ptr()), C.c_void_p(buf.flags), 64, None, 0, st) == 0
+        fl = fl.tolist()
+        ok_flag = all(fl[src] == s for src in others) and fl[rank] == 0
+        ok_ack = fl[WORLD + 2] == s if rank < 2 else True
+        # fused sampler: remote operands straight from this rank's receive buffer
         x = torch.randn(n, device="cuda")
         out = torch.empty_like(x)
-        eps_c, eps_u = (mine, _Raw(buf.local_slot(s), n, torch.bfloat16, x.device)) if rank == 0 else \
-            (_Raw(buf.local_slot(s), n, torch.bfloat16, x.device), mine)
-        K.sampler_step(x=x, eps_c=eps_c, eps_u=eps_u, x_out=out, update=N.HP_UPDATE_EULER, dt=0.05, w=2.0,
-                       wait_flag=buf.flags + 4 * (1 - rank), wait_value=s)
-        ec = (mine if rank == 0 else other).float()
-        eu = (other if rank == 0 else mine).float()
+        remote = {src: _Raw(buf.local_slot(src, s), n, torch.bfloat16, x.device) for src in others}
+        ops = {rank: mine, **remote}
+        if rank == 2:
+            assert lib.hp_flag_wait(C.c_void_p(buf.data_flag(0)), s, None, 1_000_000_000, st) == 0
+        K.sampler_step(x=x, eps_c=ops[0], eps_u=ops[1], x_out=out, update=N.HP_UPDATE_EULER, dt=0.05, w=2.0,
+                       wait_flag=buf.data_flag(1 if rank != 1 else 0), wait_value=s)
+        ec, eu = _payload(0, n).float(), _payload(1, n).float()
         ref = x - (ec + 2.0 * (ec - eu)) * 0.05
         ok_step = float((out - ref).abs().max()) < 1e-5
-        q.put((rank, ok_payload, ok_flag, ok_step))
+        q.put((rank, ok_payload, ok_flag, ok_ack, ok_step))
     finally:
         dist.destroy_process_group()
 
@@ -79,12 +91,13 @@ def _port():
         return s.getsockname()[1]
 
 
-def test_ipc_push_flag_and_fused_wait_on_one_gpu():
+def test_ipc_broadcast_flags_acks_and_fused_wait_on_one_gpu():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    mp.start_processes(_worker, args=(_port(), q), nprocs=2, join=True, start_method="spawn")
-    res = sorted(q.get(timeout=10) for _ in range(2))
-    for rank, ok_payload, ok_flag, ok_step in res:
+    mp.start_processes(_worker, args=(_port(), q), nprocs=WORLD, join=True, start_method="spawn")
+    res = sorted(q.get(timeout=10) for _ in range(WORLD))
+    for rank, ok_payload, ok_flag, ok_ack, ok_step in res:
         assert ok_payload, f"rank {rank}: payload over IPC differs"
         assert ok_flag, f"rank {rank}: flag not released"
+        assert ok_ack, f"rank {rank}: passive rank's acknowledgement missing"
         assert ok_step, f"rank {rank}: fused step with peer operand differs"
