@@ -58,6 +58,21 @@ typedef struct hp_gemm_desc {
      * row partial sums through distributed shared memory (N/block_n <= 8). */
     const float* ln_gamma; const float* ln_beta; float ln_eps;
     void* ln_y; int64_t ldy;
+    /* LayerNorm folded into the next GEMM (no normalised tensor is written).
+     * Producer side, stats_out != NULL: the epilogue also writes, for every
+     * output row and N tile, (mean, M2) of the STORED bf16 row segment as two
+     * floats at stats_out[2 * (row * (N / block_n) + tile)] (plain, batch 1,
+     * not GEGLU, N % block_n == 0).
+     * Consumer side, ln_stats != NULL: A holds the raw rows, B = W * gamma
+     * (columns scaled), ln_colsum[n] = sum_k B[n, k] (fp32 of the bf16 B),
+     * bias = b + W beta. The epilogue combines the ln_parts partials of
+     * ln_part_n columns each (Chan's formula, fixed order; ln_parts *
+     * ln_part_n == K) into mean / rstd per row and forms
+     *   LN(A) W^T + b = rstd * (acc - mean * ln_colsum[n]) + bias[n]
+     * before the activation. */
+    float* stats_out;
+    const float* ln_stats; int32_t ln_parts; int32_t ln_part_n;
+    const float* ln_colsum; float ln_fold_eps;
 } hp_gemm_desc;
 
 int hp_gemm(const hp_gemm_desc* d, void* stream);

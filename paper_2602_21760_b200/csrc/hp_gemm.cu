@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <string.h>
+#include <stdlib.h>
 #include <mutex>
 #include "hybridpar_b200_denoiser.h"
 #include "hp_common.cuh"
@@ -57,7 +58,39 @@ struct GemmParams {
   const float* colscale;
   int batch;                       // >= 1; plain mode only
   long long a_bs, d_bs, r_bs, cs_bs;  // element strides between batches
+  // LayerNorm folding: producer writes per-(row, N tile) (mean, M2); consumer folds
+  bool vec256;                     // output (and residual) rows 32-byte aligned: 256-bit accesses
+  float2* stats_out;
+  const float2* ln_stats; int ln_parts; float ln_part_n; const float* ln_colsum; float ln_fold_eps;
 };
+
+// mean / rstd of one row from its (mean, M2) partials, Chan's pairwise update in
+// a fixed order (deterministic, no E[x^2] - E[x]^2 cancellation)
+constexpr int kMaxFoldParts = 16;
+__device__ __forceinline__ void fold_row_stats(const GemmParams& p, int row, float& mean, float& rstd) {
+  const float2* s = p.ln_stats + (long long)row * p.ln_parts;
+  float2 v[kMaxFoldParts];
+#pragma unroll
+  for (int t = 0; t < kMaxFoldParts; ++t)          // all partial loads in flight at once
+    if (t < p.ln_parts) v[t] = __ldg(s + t);
+  float n = 0.f, mu = 0.f, m2 = 0.f;
+#pragma unroll
+  for (int t = 0; t < kMaxFoldParts; ++t) {
+    if (t < p.ln_parts) {
+      const float nn = n + p.ln_part_n;
+      const float w = __fdividef(p.ln_part_n, nn);
+      const float delta = v[t].x - mu;
+      mu = fmaf(delta, w, mu);
+      m2 += v[t].y + delta * delta * (n * w);
+      n = nn;
+    }
+  }
+  mean = mu;
+  rstd = rsqrtf(fmaxf(m2, 0.f) / n + p.ln_fold_eps);
+}
+
+// epilogue flavours (one template instance each, chosen per launch)
+constexpr int kEpiPlain = 0, kEpiStats = 1, kEpiFold = 2;
 
 template <int BN>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& b, int& m0, int& n0) {
@@ -74,14 +107,63 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& 
   n0 = (tile / mt_all) * BN;
 }
 
-__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+// exact-erf GELU x * Phi(x) with erf from Abramowitz-Stegun 7.1.26 (|erf error| <= 1.5e-7,
+// GELU error <= 2.2e-7 abs): one MUFU.RCP + one MUFU.EX2 + 8 FMA-pipe ops instead of erff
+__device__ __forceinline__ float gelu_erf(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  float t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
+  float poly = fmaf(t, 1.061405429f, -1.453152027f);
+  poly = fmaf(poly, t, 1.421413741f);
+  poly = fmaf(poly, t, -0.284496736f);
+  poly = fmaf(poly, t, 0.254829592f);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.44269504088896341f * z * z));
+  const float h = 0.5f * x * (poly * t * e);    // 0.5 x (1 - erf(z))
+  return x >= 0.f ? x - h : h;
+}
+
+// 64 contiguous bytes of one output row: two 256-bit stores when 32-byte aligned
+__device__ __forceinline__ void st_row64(__nv_bfloat16* dst, const uint32_t (&w)[16], bool v8) {
+  if (v8) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
+                    "r"(w[7]) : "memory");
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(dst + 16), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]),
+                    "r"(w[14]), "r"(w[15]) : "memory");
+  } else {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d4[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  }
+}
+__device__ __forceinline__ void ld_row64(const __nv_bfloat16* src, uint32_t (&w)[16], bool v8) {
+  if (v8) {
+    asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "l"(src));
+    asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]),
+                   "=r"(w[15])
+                 : "l"(src + 16));
+  } else {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 u = s4[q];
+      w[4 * q] = u.x; w[4 * q + 1] = u.y; w[4 * q + 2] = u.z; w[4 * q + 3] = u.w;
+    }
+  }
+}
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
 
 // Epilogue for one 128 x BN tile; thread = one output row. `sb` is the tile's
 // column bias (bias + per-image bias2 folded) staged in shared memory, or null.
-template <int BN>
+template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
-                                              int lane, const float* sb, float* row_stats) {
+                                              int lane, const float* sb, float* row_stats, const float* scs,
+                                              float f_mean, float f_rstd) {
   const int row = m0 + quarter * 32 + lane;
   const bool row_ok = row < p.M;
   const uint32_t lane_addr = tmem_acc + ((uint32_t)(quarter * 32) << 16);
@@ -102,6 +184,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
       for (int j = 0; j < 32; j += 2) {
         float a0 = __uint_as_float(ra[j]) * p.alpha, a1 = __uint_as_float(ra[j + 1]) * p.alpha;
         float g0 = __uint_as_float(rg[j]) * p.alpha, g1 = __uint_as_float(rg[j + 1]) * p.alpha;
+        if constexpr (EPI == kEpiFold) {
+          const float* cs = scs + c * 32 + j;
+          a0 = f_rstd * fmaf(-f_mean, cs[0], a0);
+          a1 = f_rstd * fmaf(-f_mean, cs[1], a1);
+          g0 = f_rstd * fmaf(-f_mean, cs[BN / 2], g0);
+          g1 = f_rstd * fmaf(-f_mean, cs[BN / 2 + 1], g1);
+        }
         if (sb) {
           a0 += sb[c * 32 + j];
           a1 += sb[c * 32 + j + 1];
@@ -110,38 +199,41 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         }
         packed[j / 2] = pack_bf16(a0 * gelu_erf(g0), a1 * gelu_erf(g1));
       }
-      uint4* dst = reinterpret_cast<uint4*>(p.d + (long long)row * p.ldd + ocol);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+      st_row64(p.d + (long long)row * p.ldd + ocol, packed, p.vec256);
     }
     return;
   }
   const bool has_res = p.res != nullptr && row_ok;
-  const uint4* res_row = has_res ? reinterpret_cast<const uint4*>(p.res + (long long)row * p.ldr + n0) : nullptr;
-  uint4 rn[4];
+  const __nv_bfloat16* res_row = has_res ? p.res + (long long)row * p.ldr + n0 : nullptr;
+  uint32_t rn[16];
   float st_sum = 0.f, st_sq = 0.f;            // LayerNorm partials of the stored (bf16) row
-  if (has_res) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) rn[q] = res_row[q];
-  }
+  float sh_k = 0.f, sh_s1 = 0.f, sh_s2 = 0.f;   // stats_out: sums shifted by the row's first value
+  if (has_res) ld_row64(res_row, rn, p.vec256);
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     uint32_t r[32];
     tmem_ld_32x32b_x32(lane_addr + c * 32, r);
-    uint4 rc[4];
+    uint32_t rc[16];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) rc[q] = rn[q];
-    if (has_res && c + 1 < BN / 32) {          // residual of the next chunk in flight meanwhile
-#pragma unroll
-      for (int q = 0; q < 4; ++q) rn[q] = res_row[(c + 1) * 4 + q];
-    }
+    for (int q = 0; q < 16; ++q) rc[q] = rn[q];
+    if (has_res && c + 1 < BN / 32) ld_row64(res_row + (c + 1) * 32, rn, p.vec256);   // next chunk in flight
     tmem_ld_wait();
     if (!row_ok) continue;
     const int col = n0 + c * 32;
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+    if constexpr (EPI == kEpiFold) {
+      const float4* c4 = reinterpret_cast<const float4*>(scs + c * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 cs = c4[q];
+        v[4 * q] = f_rstd * fmaf(-f_mean, cs.x, v[4 * q]);
+        v[4 * q + 1] = f_rstd * fmaf(-f_mean, cs.y, v[4 * q + 1]);
+        v[4 * q + 2] = f_rstd * fmaf(-f_mean, cs.z, v[4 * q + 2]);
+        v[4 * q + 3] = f_rstd * fmaf(-f_mean, cs.w, v[4 * q + 3]);
+      }
+    }
     if (sb) {
       const float4* b4 = reinterpret_cast<const float4*>(sb + c * 32);
 #pragma unroll
@@ -167,33 +259,43 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     }
     if (has_res) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 u = rc[q];
-        float2 f0 = unpack_bf16(u.x), f1 = unpack_bf16(u.y), f2 = unpack_bf16(u.z), f3 = unpack_bf16(u.w);
-        v[8 * q + 0] += f0.x; v[8 * q + 1] += f0.y; v[8 * q + 2] += f1.x; v[8 * q + 3] += f1.y;
-        v[8 * q + 4] += f2.x; v[8 * q + 5] += f2.y; v[8 * q + 6] += f3.x; v[8 * q + 7] += f3.y;
+      for (int q = 0; q < 16; ++q) {
+        const float2 f = unpack_bf16(rc[q]);
+        v[2 * q] += f.x;
+        v[2 * q + 1] += f.y;
       }
     }
-    uint4* dst = reinterpret_cast<uint4*>(p.d + (long long)row * p.ldd + col);
+    uint32_t w[16];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 u = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                                 pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
-      dst[q] = u;
-      if (row_stats) {
-        const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+    for (int q = 0; q < 16; ++q) w[q] = pack_bf16(v[2 * q], v[2 * q + 1]);
+    st_row64(p.d + (long long)row * p.ldd + col, w, p.vec256);
+    if constexpr (EPI == kEpiStats) {
+      if (c == 0) sh_k = unpack_bf16(w[0]).x;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = unpack_bf16(w4[e]);
-          st_sum += f.x + f.y;
-          st_sq = fmaf(f.x, f.x, fmaf(f.y, f.y, st_sq));
-        }
+      for (int e = 0; e < 16; ++e) {
+        const float2 f = unpack_bf16(w[e]);
+        const float d0 = f.x - sh_k, d1 = f.y - sh_k;
+        sh_s1 += d0 + d1;
+        sh_s2 = fmaf(d0, d0, fmaf(d1, d1, sh_s2));
+      }
+    }
+    if (row_stats) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float2 f = unpack_bf16(w[e]);
+        st_sum += f.x + f.y;
+        st_sq = fmaf(f.x, f.x, fmaf(f.y, f.y, st_sq));
       }
     }
   }
   if (row_stats) {
     row_stats[0] = st_sum;
     row_stats[1] = st_sq;
+  }
+  if (EPI == kEpiStats && row_ok) {
+    const float inv_n = 1.0f / (float)BN;
+    p.stats_out[(long long)row * p.num_n_tiles + n0 / BN] =
+        make_float2(fmaf(sh_s1, inv_n, sh_k), fmaxf(sh_s2 - sh_s1 * sh_s1 * inv_n, 0.f));
   }
 }
 
@@ -277,6 +379,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* sbias = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);   // [2][BN]
   float* s_stats = sbias + 2 * BN;                                               // [128][2]
+  float* scolsum = s_stats + 2 * BM;                                             // [2][BN] folded-LN column sums
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_tiles = p.num_m_tiles * p.batch * p.num_n_tiles;
@@ -373,29 +476,44 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       int bt, m0, n0;
       decode_tile<BN>(p, tile, bt, m0, n0);
       float* sb = any_bias ? sbias + acc * BN : nullptr;
-      if (any_bias) {
-        // stage this tile's column bias while the tensor core is still busy; every row
-        // of a tile belongs to one image (bias2_div is a multiple of 128)
+      float* scs = scolsum + acc * BN;
+      const bool fold = p.ln_stats != nullptr;
+      if (any_bias || fold) {
+        // stage this tile's column bias (and folded-LN column sums) while the tensor
+        // core is still busy; every row of a tile belongs to one image (bias2_div is a
+        // multiple of 128)
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const long long img = p.batch > 1 ? (long long)bt : (long long)(m0 / p.bias2_div);
         for (int i = et; i < BN; i += 128) {
-          float b = p.bias ? __ldg(p.bias + n0 + i) : 0.0f;
-          if (p.bias2) b += __ldg(p.bias2 + img * p.bias2_ld + n0 + i);
-          sb[i] = b;
+          if (any_bias) {
+            float b = p.bias ? __ldg(p.bias + n0 + i) : 0.0f;
+            if (p.bias2) b += __ldg(p.bias2 + img * p.bias2_ld + n0 + i);
+            sb[i] = b;
+          }
+          if (fold) scs[i] = __ldg(p.ln_colsum + n0 + i);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
+      // folded LayerNorm: this row's mean / rstd, also before the accumulator is ready
+      float f_mean = 0.f, f_rstd = 1.f;
+      const int my_row = m0 + quarter * 32 + lane;
+      if (fold && my_row < p.M) fold_row_stats(p, my_row, f_mean, f_rstd);
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
+      const uint32_t t_acc = tmem_base + acc * BN;
       if (p.batch > 1) {
         GemmParams q = p;
         q.d += (long long)bt * p.d_bs;
         if (q.res) q.res += (long long)bt * p.r_bs;
         if (q.colscale) q.colscale += (long long)bt * p.cs_bs;
-        epilogue_tile<BN>(q, tmem_base + acc * BN, m0, n0, quarter, lane, sb, nullptr);
+        epilogue_tile<BN, kEpiPlain>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+      } else if (fold) {
+        epilogue_tile<BN, kEpiFold>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
+      } else if (p.stats_out) {
+        epilogue_tile<BN, kEpiStats>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       } else {
-        epilogue_tile<BN>(p, tmem_base + acc * BN, m0, n0, quarter, lane, sb,
-                          p.ln_mode ? s_stats + 2 * (quarter * 32 + lane) : nullptr);
+        epilogue_tile<BN, kEpiPlain>(p, t_acc, m0, n0, quarter, lane, sb,
+                                     p.ln_mode ? s_stats + 2 * (quarter * 32 + lane) : nullptr, nullptr, 0.f, 1.f);
       }
       tc_fence_before();
       __syncwarp();
@@ -416,6 +534,187 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x BN tile. Each CTA TMA-loads its own 128 rows of A and HALF of the BN
+// B rows (both complete on the leader's barrier); the leader's single thread
+// issues M=256 MMAs that read A and B from both CTAs' shared memory and write
+// each CTA's 128 x BN accumulator into its own TMEM. Per CTA and k-block the
+// L2 traffic drops from (16 + BN/8) KB to (16 + BN/16) KB for the same MMA
+// work: the 1-CTA kernel is L2-bandwidth-bound on B200 (LTS cap), this is not.
+//   warp 0  TMA producer (both CTAs)   warp 1  MMA issuer (leader CTA)
+//   warp 2  TMEM allocator (both)      warps 4..7  epilogue (both, own rows)
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  constexpr uint32_t kBHalfBytes = (BN / 2) * BK * 2;
+  constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
+  constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  constexpr uint32_t kIdesc = idesc_bf16_f32(2 * BM, BN);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* sbias = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);   // [2][BN]
+  float* scolsum = sbias + 2 * BN;                                               // [2][BN]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
+  const int mp_all = p.num_m_tiles * p.batch;               // 256-row tiles (all batches)
+  const int num_tiles = mp_all * p.num_n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_barrier();                 // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  auto decode = [&](int tile, int& bt, int& m0, int& n0) {
+    const int mt = tile % mp_all;
+    bt = mt / p.num_m_tiles;
+    m0 = (mt - bt * p.num_m_tiles) * (2 * BM) + (int)rank * BM;   // this CTA's 128 rows
+    n0 = (tile / mp_all) * BN;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------ TMA producer (both CTAs) ------------------------------
+      uint32_t it = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
+        int bt, m0, n0;
+        decode(tile, bt, m0, n0);
+        int img = 0, y0 = 0, x0 = 0;
+        if (p.mode != HP_A_PLAIN) {
+          const int hw = p.out_h * p.out_w;
+          img = m0 / hw;
+          const int rem = m0 - img * hw;
+          y0 = rem / p.out_w;
+          x0 = rem - y0 * p.out_w;
+        }
+        const int nb = n0 + (int)rank * (BN / 2);
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+          const uint32_t fb = mapa_shared(&full[s], 0);
+          uint8_t* a_dst = smA + s * kABytes;
+          if (p.mode == HP_A_PLAIN) {
+            if (p.batch > 1) tma_load_3d_pair(a_dst, &tmA, fb, kb * BK, m0, bt);
+            else tma_load_2d_pair(a_dst, &tmA, fb, kb * BK, m0);
+          } else {
+            const int tap = kb / p.cin_blocks;
+            const int cb = kb - tap * p.cin_blocks;
+            const int dy = tap / 3, dx = tap - dy * 3;
+            if (p.mode == HP_A_CONV3X3) {
+              tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, x0 + dx - 1, y0 + dy - 1, img);
+            } else {
+              tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, 2 * x0 + dx - 1, 2 * y0 + dy - 1, img);
+            }
+          }
+          tma_load_2d_pair(smB + s * kBHalfBytes, &tmB, fb, kb * BK, nb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ------------------------------ MMA issuer (leader) ------------------------------
+      uint32_t it = 0, local = 0;
+      for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++local) {
+        const uint32_t acc = local & 1;
+        const uint32_t use = local >> 1;
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t da = sdesc_sw128_kmajor(smA + s * kABytes);
+          const uint64_t db = sdesc_sw128_kmajor(smB + s * kBHalfBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_pair(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb | k) ? 1u : 0u);
+          umma_commit_pair(&empty[s], 0x3);
+        }
+        umma_commit_pair(&tfull[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------ epilogue (both CTAs, own 128 rows) ------------------------------
+    const int quarter = warp & 3;
+    const int et = threadIdx.x - 128;
+    const bool any_bias = p.bias != nullptr || p.bias2 != nullptr;
+    const bool fold = p.ln_stats != nullptr;
+    uint32_t local = 0;
+    for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++local) {
+      const uint32_t acc = local & 1;
+      const uint32_t use = local >> 1;
+      int bt, m0, n0;
+      decode(tile, bt, m0, n0);
+      float* sb = any_bias ? sbias + acc * BN : nullptr;
+      float* scs = scolsum + acc * BN;
+      if (any_bias || fold) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const long long img = p.batch > 1 ? (long long)bt : (long long)(m0 / p.bias2_div);
+        for (int i = et; i < BN; i += 128) {
+          if (any_bias) {
+            float b = p.bias ? __ldg(p.bias + n0 + i) : 0.0f;
+            if (p.bias2) b += __ldg(p.bias2 + img * p.bias2_ld + n0 + i);
+            sb[i] = b;
+          }
+          if (fold) scs[i] = __ldg(p.ln_colsum + n0 + i);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      float f_mean = 0.f, f_rstd = 1.f;
+      const int my_row = m0 + quarter * 32 + lane;
+      if (fold && my_row < p.M) fold_row_stats(p, my_row, f_mean, f_rstd);
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const uint32_t t_acc = tmem_base + acc * BN;
+      if (p.batch > 1) {
+        GemmParams q = p;
+        q.d += (long long)bt * p.d_bs;
+        if (q.res) q.res += (long long)bt * p.r_bs;
+        if (q.colscale) q.colscale += (long long)bt * p.cs_bs;
+        epilogue_tile<BN, kEpiPlain>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+      } else if (fold) {
+        epilogue_tile<BN, kEpiFold>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
+      } else if (p.stats_out) {
+        epilogue_tile<BN, kEpiStats>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+      } else {
+        epilogue_tile<BN, kEpiPlain>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_relaxed(mapa_shared(&tempty[acc], 0));   // the leader's TMEM-free barrier
+    }
+  }
+  tc_fence_before();
+  cluster_barrier();                 // all MMAs consumed, both epilogues done
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
 }
 
 // ---------------------------------------------------------------------------
@@ -464,7 +763,7 @@ int num_sms() {
 
 template <int BN, int STAGES>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
-  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + BN * BK * 2) + 256 + 2 * BN * sizeof(float) +
+  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + BN * BK * 2) + 256 + 4 * BN * sizeof(float) +
                          2 * BM * sizeof(float);
   static bool attr_set = false;
   if (!attr_set) {
@@ -499,12 +798,54 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& 
   return HP_OK;
 }
 
+template <int BN, int STAGES>
+int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
+  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + (BN / 2) * BK * 2) + 256 + 4 * BN * sizeof(float);
+  static_assert(smem <= 227 * 1024, "pair GEMM smem");
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_pair_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return HP_ERR_CUDA;
+    attr_set = true;
+  }
+  const int tiles = p.num_m_tiles * p.batch * p.num_n_tiles;
+  const int pairs = num_sms() / 2;
+  const int clusters = tiles < pairs ? tiles : pairs;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = hp_pdl_enabled() ? 2 : 1;
+  if (cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BN, STAGES>, ta, tb, p) != cudaSuccess) return HP_ERR_CUDA;
+  return HP_OK;
+}
+
+bool pair_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HP_GEMM_PAIR");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 int pick_bn(int64_t M, int64_t N, int act) {
   const int cands[4] = {256, 160, 128, 64};
   int best = 0;
   double best_cost = 1e30;
-  const int64_t mt = (M + BM - 1) / BM;
-  const int sms = g_num_sms ? g_num_sms : 148;
+  const bool pair = pair_enabled() && M > BM;
+  const int64_t mt = pair ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM;
+  const int sms = (g_num_sms ? g_num_sms : 148) / (pair ? 2 : 1);
   for (int bn : cands) {
     if (N % bn) continue;
     if (act == HP_ACT_GEGLU && bn != 256 && bn != 128) continue;
@@ -555,6 +896,22 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if (p.ln_mode && (p.batch > 1 || d->act == HP_ACT_GEGLU || !d->ln_gamma || !d->ln_beta || (d->ldy % 8) ||
                     (reinterpret_cast<uintptr_t>(d->ln_y) & 15)))
     return HP_ERR_UNSUPPORTED;
+  p.vec256 = ((d->ldd % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->d) & 31) == 0) &&
+             (!d->residual || (((d->ldr % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->residual) & 31) == 0))) &&
+             (p.batch <= 1 || (((d->d_bstride | d->r_bstride) % 16) == 0));
+  p.stats_out = reinterpret_cast<float2*>(d->stats_out);
+  if (p.stats_out && (p.batch > 1 || d->act == HP_ACT_GEGLU || p.ln_mode || d->a_mode != HP_A_PLAIN ||
+                      (reinterpret_cast<uintptr_t>(d->stats_out) & 7)))
+    return HP_ERR_UNSUPPORTED;
+  p.ln_stats = reinterpret_cast<const float2*>(d->ln_stats);
+  p.ln_parts = d->ln_parts; p.ln_part_n = (float)d->ln_part_n;
+  p.ln_colsum = d->ln_colsum; p.ln_fold_eps = d->ln_fold_eps;
+  if (p.ln_stats) {
+    if (p.batch > 1 || p.ln_mode || d->a_mode != HP_A_PLAIN || !d->ln_colsum || d->ln_parts <= 0 ||
+        d->ln_part_n <= 0 || d->ln_parts > kMaxFoldParts || (int64_t)d->ln_parts * d->ln_part_n != d->K ||
+        (reinterpret_cast<uintptr_t>(d->ln_stats) & 7) || (reinterpret_cast<uintptr_t>(d->ln_colsum) & 15))
+      return HP_ERR_UNSUPPORTED;
+  }
   p.a_bs = d->a_bstride; p.d_bs = d->d_bstride; p.r_bs = d->r_bstride; p.cs_bs = d->cs_bstride;
   if (p.batch > 1 && d->a_mode != HP_A_PLAIN) return HP_ERR_UNSUPPORTED;
   if (p.batch > 1 && ((p.a_bs | p.d_bs | p.r_bs) % 8 || p.cs_bs % 4)) return HP_ERR_UNSUPPORTED;
@@ -597,13 +954,25 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   } else {
     return HP_ERR_PARAMETER;
   }
+  // CTA pairs for every GEMM with more than one 128-row block (not the cluster-LN mode)
+  const bool pair = pair_enabled() && !p.ln_mode && d->M > BM;
   {
     const uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)d->N};
     const uint64_t str[1] = {(uint64_t)d->ldb * 2};
-    const uint32_t box[2] = {BK, (uint32_t)bn};
+    const uint32_t box[2] = {BK, (uint32_t)(pair ? bn / 2 : bn)};
     if (!make_map(&tb, d->b, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (pair) {
+    p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
+    switch (bn) {
+      case 256: return launch_gemm_pair<256, 6>(ta, tb, p, st);
+      case 160: return launch_gemm_pair<160, 7>(ta, tb, p, st);
+      case 128: return launch_gemm_pair<128, 8>(ta, tb, p, st);
+      case 64: return launch_gemm_pair<64, 8>(ta, tb, p, st);
+      default: return HP_ERR_UNSUPPORTED;
+    }
+  }
   switch (bn) {
     case 256: return launch_gemm<256, 4>(ta, tb, p, st);
     case 160: return launch_gemm<160, 5>(ta, tb, p, st);

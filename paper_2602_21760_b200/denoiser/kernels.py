@@ -48,6 +48,8 @@ class HpGemmDesc(C.Structure):
         ("a_bstride", _I64), ("d_bstride", _I64), ("r_bstride", _I64), ("cs_bstride", _I64),
         ("bias2_ld", _I64),
         ("ln_gamma", _VP), ("ln_beta", _VP), ("ln_eps", _F32), ("ln_y", _VP), ("ldy", _I64),
+        ("stats_out", _VP),
+        ("ln_stats", _VP), ("ln_parts", _I32), ("ln_part_n", _I32), ("ln_colsum", _VP), ("ln_fold_eps", _F32),
     ]
 
 
@@ -96,10 +98,38 @@ def _bf16(t, name):
         raise ShapeError(f"{name} must be a bf16 CUDA tensor, got {t.dtype} on {t.device}")
 
 
+class RowStats:
+    """Per-(row, N tile) (mean, M2) of a GEMM's stored output (``gemm(stats_out=)``),
+    consumed by the next GEMM's folded LayerNorm (``gemm(ln_fold=)``)."""
+
+    def __init__(self, capacity_floats: int, device):
+        self.buf = torch.empty(capacity_floats, dtype=torch.float32, device=device)
+        self.parts = 0
+        self.part_n = 0
+
+
+class FoldedLN:
+    """LayerNorm(gamma, beta) folded into the weights of the GEMM it feeds:
+    W' = bf16(W * gamma), colsum = sum_k W', bias' = bias + W beta (all on the
+    host once). ``gemm(x, fold.w, bias=fold.bias, ln_fold=(stats, fold))``
+    equals ``gemm(layer_norm(x), W, bias=bias)`` up to bf16 rounding."""
+
+    def __init__(self, w, gamma, beta, bias=None, eps=1e-5):
+        wf = w.float()
+        self.w = (wf * gamma.float()[None, :]).to(torch.bfloat16).contiguous()
+        self.colsum = self.w.float().sum(1).contiguous()
+        b = wf @ beta.float()
+        self.bias = (b if bias is None else b + bias.float()).contiguous()
+        self.eps = float(eps)
+
+
 def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, act=ACT_NONE,
-         alpha=1.0, block_n=0, conv=None, colscale=None, ln=None):
+         alpha=1.0, block_n=0, conv=None, colscale=None, ln=None, stats_out=None, ln_fold=None):
     """out[M, N'] = residual + colscale * act(alpha * A @ W^T + bias).
-    ``conv=(n, h, w, c, stride)`` reads A as NHWC."""
+    ``conv=(n, h, w, c, stride)`` reads A as NHWC. ``stats_out`` (RowStats):
+    also record the output rows' LayerNorm partials; ``ln_fold=(RowStats,
+    FoldedLN)``: A is un-normalised, LN applied in the epilogue (w, bias must
+    be the FoldedLN's)."""
     lib = N.load()
     _bf16(a, "A")
     _bf16(w, "W")
@@ -162,6 +192,17 @@ def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, a
         # ln = (gamma, beta, eps, y_out): also write y_out = LayerNorm(out) (fused epilogue)
         g, b_, eps, y = ln
         d.ln_gamma, d.ln_beta, d.ln_eps, d.ln_y, d.ldy = _p(g), _p(b_), float(eps), _p(y), y.stride(-2)
+    if stats_out is not None:
+        bn = int(block_n) or int(lib.hp_gemm_pick_block_n(M, Nn, int(act)))
+        if bn == 0 or Nn % bn or stats_out.buf.numel() < 2 * M * (Nn // bn):
+            raise ShapeError(f"row stats: N={Nn} block_n={bn} capacity {stats_out.buf.numel()}")
+        d.block_n = bn
+        d.stats_out = _p(stats_out.buf)
+        stats_out.parts, stats_out.part_n = Nn // bn, bn
+    if ln_fold is not None:
+        st, fold = ln_fold
+        d.ln_stats, d.ln_parts, d.ln_part_n = _p(st.buf), st.parts, st.part_n
+        d.ln_colsum, d.ln_fold_eps = _p(fold.colsum), fold.eps
     check(lib.hp_gemm(C.byref(d), _s()), f"hp_gemm M={M} N={Nn} K={K}")
     return out
 

@@ -91,11 +91,14 @@ class _Block:
     def __init__(self, W, name, c, heads, dev):
         self.c, self.heads = c, heads
         self.n1, self.n2, self.n3 = (_Norm(W, f"{name}.norm{i}", dev) for i in (1, 2, 3))
+        # each LayerNorm feeds exactly one GEMM: fold gamma/beta into that GEMM's
+        # weights/bias; the producing GEMM's epilogue records the row statistics
         a1 = f"{name}.attn1"
-        self.qkv = _bf(torch.cat([W[f"{a1}.to_q.weight"], W[f"{a1}.to_k.weight"], W[f"{a1}.to_v.weight"]]).to(dev))
+        qkv = torch.cat([W[f"{a1}.to_q.weight"], W[f"{a1}.to_k.weight"], W[f"{a1}.to_v.weight"]]).to(dev)
+        self.f1 = K.FoldedLN(qkv, self.n1.g, self.n1.b, eps=1e-5)
         self.o1 = _Lin(W, f"{a1}.to_out.0", dev=dev)
         a2 = f"{name}.attn2"
-        self.q2 = _bf(W[f"{a2}.to_q.weight"].to(dev))
+        self.f2 = K.FoldedLN(W[f"{a2}.to_q.weight"].to(dev), self.n2.g, self.n2.b, eps=1e-5)
         self.kv2 = _bf(torch.cat([W[f"{a2}.to_k.weight"], W[f"{a2}.to_v.weight"]]).to(dev))
         self.o2 = _Lin(W, f"{a2}.to_out.0", dev=dev)
         # GEGLU: interleave hidden/gate rows per 256-wide output tile (128 + 128)
@@ -104,31 +107,30 @@ class _Block:
         half = 128
         idx = torch.cat([torch.cat([torch.arange(i, i + half), torch.arange(F_ + i, F_ + i + half)])
                          for i in range(0, F_, half)]).to(dev)
-        self.ff1_w, self.ff1_b = _bf(pw[idx]), _f32(pb[idx])
+        self.f3 = K.FoldedLN(pw[idx], self.n3.g, self.n3.b, bias=pb[idx], eps=1e-5)
         self.ff2 = _Lin(W, f"{name}.ff.net.2", dev=dev)
         self.kv_cache = {}
 
     def prepare(self, ctx2d, key):
         self.kv_cache[key] = K.gemm(ctx2d, self.kv2)        # [rows*L, 2C]
 
-    def __call__(self, h, n, S, ctx_len, key):
+    def __call__(self, h, n, S, ctx_len, key, rs):
+        """h: residual stream whose row statistics the producing GEMM left in rs."""
         c = self.c
         scale = 1.0 / math.sqrt(64)
-        y = K.layer_norm(h, c, gamma=self.n1.g, beta=self.n1.b, eps=1e-5)
-        qkv = K.gemm(y, self.qkv)
-        att = torch.empty_like(y)
+        f1, f2, f3 = self.f1, self.f2, self.f3
+        qkv = K.gemm(h, f1.w, bias=f1.bias, ln_fold=(rs, f1))                 # norm1 folded
+        att = torch.empty_like(h)
         K.attention(qkv, qkv, qkv, att, batch=n, heads=self.heads, sq=S, skv=S, scale=scale,
                     q_col0=0, k_col0=c, v_col0=2 * c)
-        h = self.o1(att, residual=h, out=h)
-        y = K.layer_norm(h, c, gamma=self.n2.g, beta=self.n2.b, eps=1e-5)
-        q = K.gemm(y, self.q2)
+        h = self.o1(att, residual=h, out=h, stats_out=rs)
+        q = K.gemm(h, f2.w, bias=f2.bias, ln_fold=(rs, f2))                   # norm2 folded
         kv = self.kv_cache[key]
         K.attention(q, kv, kv, att, batch=n, heads=self.heads, sq=S, skv=ctx_len, scale=scale,
                     q_col0=0, k_col0=0, v_col0=c)
-        h = self.o2(att, residual=h, out=h)
-        y = K.layer_norm(h, c, gamma=self.n3.g, beta=self.n3.b, eps=1e-5)
-        f = K.gemm(y, self.ff1_w, bias=self.ff1_b, act=K.ACT_GEGLU, block_n=256)
-        return self.ff2(f, residual=h, out=h)
+        h = self.o2(att, residual=h, out=h, stats_out=rs)
+        f = K.gemm(h, f3.w, bias=f3.bias, act=K.ACT_GEGLU, block_n=256, ln_fold=(rs, f3))   # norm3 folded
+        return self.ff2(f, residual=h, out=h, stats_out=rs)
 
 
 class _Transformer:
@@ -142,11 +144,11 @@ class _Transformer:
         for b in self.blocks:
             b.prepare(ctx2d, key)
 
-    def __call__(self, x, n, hw, groups, stats, ctx_len, key):
+    def __call__(self, x, n, hw, groups, stats, ctx_len, key, rs):
         y = K.group_norm(x, n, hw, self.c, self.norm.g, self.norm.b, groups=groups, eps=1e-6, stats=stats)
-        h = self.pin(y)
+        h = self.pin(y, stats_out=rs)
         for b in self.blocks:
-            h = b(h, n, hw, ctx_len, key)
+            h = b(h, n, hw, ctx_len, key, rs)
         return self.pout(h, residual=x)
 
 
@@ -200,6 +202,12 @@ class UNet:
         for r in blocks:
             r.tproj = None
 
+    def _row_stats(self, floats: int) -> "K.RowStats":
+        rs = getattr(self, "_rs", None)
+        if rs is None or rs.buf.numel() < floats:
+            rs = self._rs = K.RowStats(floats, self.dev)
+        return rs
+
     def _transformers(self):
         for res, att, _ in self.down + self.up:
             for a in att:
@@ -230,6 +238,7 @@ class UNet:
         s = self.spec
         n, H, Wd = x.shape[0], x.shape[1], x.shape[2]
         st, g = self.stats, s.groups
+        rs = self._row_stats(2 * n * H * Wd * max(c // 4 ** l for l, c in enumerate(s.block_out)) // 64)
         te = K.timestep_embedding(t, s.block_out[0])
         te = K.linear_small(te, self.t1.w, self.t1.b, act_out=K.ACT_SILU)
         temb = K.linear_small(te, self.t2.w, self.t2.b)
@@ -246,7 +255,7 @@ class UNet:
             for r, a in zip(res, att):
                 h = r(h, n, hh, ww, tb(r), g, st)
                 if a is not None:
-                    h = a(h, n, hh * ww, g, st, self.ctx_len, key)
+                    h = a(h, n, hh * ww, g, st, self.ctx_len, key, rs)
                 skips.append(h)
             if ds is not None:
                 h = ds(h, n, hh, ww, stride=2)
@@ -254,7 +263,7 @@ class UNet:
                 skips.append(h)
         r0, tr, r1 = self.mid
         h = r0(h, n, hh, ww, tb(r0), g, st)
-        h = tr(h, n, hh * ww, g, st, self.ctx_len, key)
+        h = tr(h, n, hh * ww, g, st, self.ctx_len, key, rs)
         h = r1(h, n, hh, ww, tb(r1), g, st)
         for res, att, us in self.up:
             for r, a in zip(res, att):
@@ -262,7 +271,7 @@ class UNet:
                 cat = K.concat_channels(h, h.shape[1], sk, sk.shape[1], n * hh * ww)
                 h = r(cat, n, hh, ww, tb(r), g, st)
                 if a is not None:
-                    h = a(h, n, hh * ww, g, st, self.ctx_len, key)
+                    h = a(h, n, hh * ww, g, st, self.ctx_len, key, rs)
             if us is not None:
                 h = K.upsample2x(h, n, hh, ww, h.shape[1])
                 hh, ww = hh * 2, ww * 2

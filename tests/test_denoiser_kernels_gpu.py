@@ -210,3 +210,37 @@ def test_gemm_fused_layernorm_cluster(M, N, Kd, bn):
     close(out, h_ref)
     ref_y = F.layer_norm(out.float(), (N,), g, be, eps=1e-5)      # LN of the stored bf16 rows
     close(y, ref_y, tol=2e-2)
+
+
+@pytest.mark.parametrize("M,C,Nc,act", [(2048, 1280, 3840, K.ACT_NONE), (8192, 640, 640, K.ACT_NONE),
+                                        (300, 320, 512, K.ACT_GEGLU), (2048, 1280, 2560, K.ACT_GEGLU)])
+def test_gemm_layernorm_fold(M, C, Nc, act):
+    """Producer GEMM (+residual) records row (mean, M2) per N tile; the consumer
+    GEMM applies LayerNorm(gamma, beta) in its epilogue from those partials
+    with gamma folded into its weights == GEMM(LayerNorm(h)) in fp32."""
+    torch.manual_seed(M + C)
+    a, w0 = rnd(M, C), rnd(C, C, s=C ** -0.5)
+    res = (torch.randn(M, C, device="cuda") * 3 + 1.5).bfloat16()      # off-centre residual stream
+    rs = K.RowStats(2 * M * C // 64, "cuda")
+    h = K.gemm(a, w0, residual=res, stats_out=rs)
+    # partials are exact statistics of the stored bf16 tile segments
+    seg = h.float().view(M, rs.parts, rs.part_n)
+    st = rs.buf[:2 * M * rs.parts].view(M, rs.parts, 2)
+    torch.testing.assert_close(st[..., 0], seg.mean(-1), rtol=1e-5, atol=1e-5)
+    m2 = ((seg - seg.mean(-1, keepdim=True)) ** 2).sum(-1)
+    torch.testing.assert_close(st[..., 1], m2, rtol=1e-4, atol=1e-3)
+    gamma = 1.0 + 0.2 * torch.randn(C, device="cuda")
+    beta = 0.1 * torch.randn(C, device="cuda")
+    w = torch.randn(Nc, C, device="cuda") * C ** -0.5
+    bias = torch.randn(Nc, device="cuda")
+    fold = K.FoldedLN(w, gamma, beta, bias=bias, eps=1e-5)
+    out = K.gemm(h, fold.w, bias=fold.bias, act=act, block_n=256 if act == K.ACT_GEGLU else 0, ln_fold=(rs, fold))
+    y = F.layer_norm(h.float(), (C,), gamma, beta, eps=1e-5)
+    pre = y @ w.t() + bias
+    if act == K.ACT_GEGLU:
+        # host interleaving convention of the GEGLU epilogue: per 256-wide tile, 128 hidden + 128 gate
+        pre = pre.view(M, Nc // 256, 2, 128)
+        ref = (pre[:, :, 0] * F.gelu(pre[:, :, 1])).reshape(M, Nc // 2)
+    else:
+        ref = pre
+    close(out, ref, tol=2e-2)

@@ -18,6 +18,8 @@ def main():
     reps = int(sys.argv[6]) if len(sys.argv) > 6 else 20
     eager = "eager" in sys.argv[7:]
     use_ln = "ln" in sys.argv[7:]
+    use_stats = "stats" in sys.argv[7:]
+    use_fold = "fold" in sys.argv[7:]
     a = torch.randn(M, Kd, device="cuda").bfloat16()
     w = (torch.randn(N, Kd, device="cuda") * Kd ** -0.5).bfloat16()
     bias = torch.randn(N, device="cuda")
@@ -27,7 +29,19 @@ def main():
         ln = (torch.ones(N, device="cuda"), torch.zeros(N, device="cuda"), 1e-5,
               torch.empty(M, N, device="cuda", dtype=torch.bfloat16))
     res = torch.randn(M, N, device="cuda").bfloat16() if use_ln else None
-    run = lambda: K.gemm(a, w, bias=bias, out=out, act=act, block_n=bn, residual=res, ln=ln)  # noqa: E731
+    kw = {}
+    if use_stats or use_fold:
+        rs = K.RowStats(2 * M * max(N, Kd) // 64, "cuda")
+        if use_stats:
+            kw["stats_out"] = rs
+        else:
+            rs.parts, rs.part_n = Kd // 160 if Kd % 160 == 0 else Kd // 128, 160 if Kd % 160 == 0 else 128
+            rs.buf[:2 * M * rs.parts].view(-1, 2)[:, 0] = 0.1
+            rs.buf[:2 * M * rs.parts].view(-1, 2)[:, 1] = float(rs.part_n)
+            fold = K.FoldedLN(w.float(), torch.ones(Kd, device="cuda"), torch.zeros(Kd, device="cuda"), bias=bias)
+            w, bias = fold.w, fold.bias
+            kw["ln_fold"] = (rs, fold)
+    run = lambda: K.gemm(a, w, bias=bias, out=out, act=act, block_n=bn, residual=res, ln=ln, **kw)  # noqa: E731
     for _ in range(3):
         run()
     torch.cuda.synchronize()
@@ -48,7 +62,7 @@ def main():
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
     print(f"gemm M={M} N={N} K={Kd} bn={bn} act={act} {'eager' if eager else 'graph'}: "
-          f"{' +LN' if use_ln else ''} {ms * 1e3:.1f} us {2.0 * M * N * Kd / ms / 1e9:.1f} TFLOP/s")
+          f"{' +LN' if use_ln else ''}{' +stats' if use_stats else ''}{' +fold' if use_fold else ''} {ms * 1e3:.1f} us {2.0 * M * N * Kd / ms / 1e9:.1f} TFLOP/s")
 
 
 if __name__ == "__main__":
