@@ -123,20 +123,34 @@ __device__ __forceinline__ void tmem_ld_x32_at(uint32_t taddr, uint32_t* r, cons
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kThreads, 1)
+// SINGLE: every key fits one 128-key block (cross-attention, skv <= 128). Then no
+// rescale exists, O_q reuses S_q's TMEM columns once the softmax has consumed S_q,
+// and one K/V stage suffices: 256 TMEM columns and 97 KB of smem, so two CTAs
+// share an SM and one's latency chain (TMA -> MMA -> softmax -> PV -> store)
+// overlaps the other's.
+template <bool SINGLE>
+__global__ void __launch_bounds__(kThreads, SINGLE ? 2 : 1)
 attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, AttnParams p) {
+  constexpr int kSt = SINGLE ? 1 : kStages;
+  constexpr uint32_t kCols = SINGLE ? 256 : kTmemCols;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                                  // 2 tiles
   uint8_t* sK = sQ + 2 * kTileBytes;
-  uint8_t* sV = sK + kStages * kTileBytes;
-  uint8_t* sP = sV + kStages * kTileBytes;            // 2 tiles (one P buffer per query tile)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
+  uint8_t* sV = sK + kSt * kTileBytes;
+  uint8_t* sP = sV + kSt * kTileBytes;                // 2 tiles (one P buffer per query tile)
+  // SINGLE: P_0 overwrites Q_0|Q_1 and P_1 overwrites K|X once both S MMAs are done
+  // (80 KB in all instead of 128 KB), so two CTAs fit an SM
+  uint64_t* bars = reinterpret_cast<uint64_t*>(SINGLE ? sP + kTileBytes : sP + 2 * kPBytes);
+  auto p_atom = [&](int q, int a) -> uint8_t* {       // 64-key SW128 atom a of P_q
+    if constexpr (SINGLE) return q == 0 ? sQ + a * kTileBytes : (a == 0 ? sK : sP);
+    return sP + q * kPBytes + a * (kBQ * 128);
+  };
   uint64_t* q_full = bars;
   uint64_t* kv_full = q_full + 1;
-  uint64_t* kv_empty = kv_full + kStages;
-  uint64_t* s_full = kv_empty + kStages;   // [2] per query tile
+  uint64_t* kv_empty = kv_full + kSt;
+  uint64_t* s_full = kv_empty + kSt;       // [2] per query tile
   uint64_t* p_full = s_full + 2;           // [2]
   uint64_t* o_done = p_full + 2;           // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
@@ -144,16 +158,16 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y, b = blockIdx.z;
   const int q0 = blockIdx.x * 2 * kBQ;
-  const int J = p.n_kv;
+  const int J = SINGLE ? 1 : p.n_kv;
 
   if (warp == 8 && lane == 0) {
     prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < kStages; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int s = 0; s < kSt; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1); }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 9) tmem_alloc<kCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -167,8 +181,8 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
       tma_load_3d(sQ, &tmQ, q_full, p.q_col0 + h * kD, q0, b);
       tma_load_3d(sQ + kTileBytes, &tmQ, q_full, p.q_col0 + h * kD, q0 + kBQ, b);
       for (int j = 0; j < J; ++j) {
-        const int s = j % kStages;
-        mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
+        const int s = j % kSt;
+        mbar_wait(&kv_empty[s], ((j / kSt) & 1) ^ 1);
         mbar_arrive_expect_tx(&kv_full[s], 2 * kTileBytes);
         tma_load_3d(sK + s * kTileBytes, &tmK, &kv_full[s], p.k_col0 + h * kD, j * kBK, b);
         tma_load_3d(sV + s * kTileBytes, &tmV, &kv_full[s], p.v_col0 + h * kD, j * kBK, b);
@@ -178,7 +192,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     if (lane == 0) {
       mbar_wait(q_full, 0);
       auto issue_s = [&](int q, int j) {
-        const int s = j % kStages;
+        const int s = j % kSt;
         const uint64_t dq = sdesc_sw128_kmajor(sQ + q * kTileBytes);
         const uint64_t dk = sdesc_sw128_kmajor(sK + s * kTileBytes);
 #pragma unroll
@@ -186,22 +200,22 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         umma_commit(&s_full[q]);
       };
       auto issue_pv = [&](int q, int j, bool wait) {
-        const int s = j % kStages;
+        const int s = j % kSt;
         if (wait) {
           mbar_wait(&p_full[q], j & 1);
           tc_fence_after();
         }
-        const uint32_t d_o = tmem + 256 + q * kD;
+        const uint32_t d_o = tmem + (SINGLE ? q * kBK : 256 + q * kD);
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k) {
-          const uint64_t da = sdesc_sw128_kmajor(sP + q * kPBytes + (k >> 2) * (kBQ * 128)) + 2 * (k & 3);
+          const uint64_t da = sdesc_sw128_kmajor(p_atom(q, k >> 2)) + 2 * (k & 3);
           const uint64_t dv = sdesc_sw128_mnmajor(sV + s * kTileBytes + k * 2048, 8192);
           umma_bf16(d_o, da, dv, kIdescO, (j > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&o_done[q]);
       };
       for (int j = 0; j < J; ++j) {
-        mbar_wait(&kv_full[j % kStages], (j / kStages) & 1);
+        mbar_wait(&kv_full[j % kSt], (j / kSt) & 1);
         tc_fence_after();
         for (int q = 0; q < 2; ++q) {
           if (j > 0) {
@@ -212,13 +226,13 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
           issue_s(q, j);
           if (j > 0) {
             issue_pv(q, j - 1, false);      // P_q(j-1) was waited for above
-            if (q == 1) umma_commit(&kv_empty[(j - 1) % kStages]);
+            if (q == 1) umma_commit(&kv_empty[(j - 1) % kSt]);
           }
         }
       }
       issue_pv(0, J - 1, true);
       issue_pv(1, J - 1, true);
-      umma_commit(&kv_empty[(J - 1) % kStages]);
+      umma_commit(&kv_empty[(J - 1) % kSt]);
     }
   } else {
     // ------------------------------ softmax ------------------------------
@@ -227,8 +241,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t t_s = tmem + lane_base + q * kBK;
-    const uint32_t t_o = tmem + lane_base + 256 + q * kD;
-    uint8_t* pbase = sP + q * kPBytes;
+    const uint32_t t_o = tmem + lane_base + (SINGLE ? q * kBK : 256 + q * kD);
     float m_run = -INFINITY, l_run = 0.f;
     const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
     for (int j = 0; j < J; ++j) {
@@ -253,7 +266,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
       const float m_blk = mx * p.scale_log2;
       // lazy rescale: move the reference max only when it grows by > 2^8
       const bool grow = (j == 0) || (m_blk > m_run + kRescaleThreshold);
-      if (j > 0) {
+      if (!SINGLE && j > 0) {
         // PV(j-1) must be complete before O is rescaled or P is overwritten
         mbar_wait(&o_done[q], (j - 1) & 1);
         tc_fence_after();
@@ -275,6 +288,14 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
       if (grow) m_run = fmaxf(m_run, m_blk);
       const uint64_t negm2 = pack2(-m_run, -m_run);
       uint64_t sum2 = 0ull;
+      if constexpr (SINGLE) {
+        // P overwrites Q and K: both tiles' score MMAs must have finished reading them
+        // (the commit behind S_1 covers S_0 too)
+        if (q == 0) {
+          mbar_wait(&s_full[1], 0);
+          tc_fence_after();
+        }
+      }
       // pass 2: P = 2^(s*scale - m) in packed fp32 pairs; 3 of 8 pairs on the FMA-pipe polynomial
 #pragma unroll
       for (int c = 0; c < kBK / 32; ++c) {
@@ -300,7 +321,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
           sum2 = fadd2(sum2, e2);
           packed[i / 2] = pack_bf16(lo2(e2), hi2(e2));
         }
-        uint8_t* atom = pbase + (c >> 1) * (kBQ * 128) + row * 128;
+        uint8_t* atom = p_atom(q, c >> 1) + row * 128;
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) {
           const int chunk = ((c & 1) * 4 + qq) ^ (row & 7);
@@ -339,7 +360,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 9) tmem_dealloc<kTmemCols>(tmem);
+  if (warp == 9) tmem_dealloc<kCols>(tmem);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -390,16 +411,29 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   p.o = static_cast<__nv_bfloat16*>(d->o); p.ldo = d->ldo;
   p.scale_log2 = d->scale * 1.4426950408889634f;
   p.n_kv = (d->skv + kBK - 1) / kBK;
+  dim3 grid((d->sq + 2 * kBQ - 1) / (2 * kBQ), d->heads, d->batch);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p.n_kv == 1) {
+    constexpr size_t smem = 1024 + kTileBytes * 5 + 256;
+    static bool attr1 = false;
+    if (!attr1) {
+      if (cudaFuncSetAttribute(attn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return HP_ERR_CUDA;
+      attr1 = true;
+    }
+    return hp_launch_pdl(attn_kernel<true>, grid, dim3(kThreads), smem, st, tq, tk, tv, p) == cudaSuccess
+               ? HP_OK : HP_ERR_CUDA;
+  }
   constexpr size_t smem = 1024 + kTileBytes * (2 + 2 * kStages) + 2 * kPBytes + 256;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(attn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
       return HP_ERR_CUDA;
     attr = true;
   }
-  dim3 grid((d->sq + 2 * kBQ - 1) / (2 * kBQ), d->heads, d->batch);
-  if (hp_launch_pdl(attn_kernel, grid, dim3(kThreads), smem, static_cast<cudaStream_t>(stream), tq, tk, tv, p) !=
-      cudaSuccess)
+  if (hp_launch_pdl(attn_kernel<false>, grid, dim3(kThreads), smem, st, tq, tk, tv, p) != cudaSuccess)
     return HP_ERR_CUDA;
   return HP_OK;
 }

@@ -551,7 +551,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   constexpr uint32_t kBHalfBytes = (BN / 2) * BK * 2;
   constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
-  constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  // as many TMEM accumulator buffers as fit: the epilogue of one tile may lag the MMAs by
+  // several tiles without stalling the tensor core
+  constexpr int kAcc = BN <= 128 ? 4 : (BN <= 170 ? 3 : 2);
+  constexpr uint32_t kTmemCols = (kAcc * BN <= 64) ? 64 : (kAcc * BN <= 128) ? 128 : (kAcc * BN <= 256) ? 256 : 512;
   constexpr uint32_t kIdesc = idesc_bf16_f32(2 * BM, BN);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -561,8 +564,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + kAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAcc);
   float* sbias = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);   // [2][BN]
   float* scolsum = sbias + 2 * BN;                                               // [2][BN]
 
@@ -577,7 +580,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    for (int a = 0; a < kAcc; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
@@ -640,8 +643,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       // ------------------------------ MMA issuer (leader) ------------------------------
       uint32_t it = 0, local = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++local) {
-        const uint32_t acc = local & 1;
-        const uint32_t use = local >> 1;
+        const uint32_t acc = local % kAcc;
+        const uint32_t use = local / kAcc;
         mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -668,12 +671,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const bool fold = p.ln_stats != nullptr;
     uint32_t local = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++local) {
-      const uint32_t acc = local & 1;
-      const uint32_t use = local >> 1;
+      const uint32_t acc = local % kAcc;
+      const uint32_t use = local / kAcc;
       int bt, m0, n0;
       decode(tile, bt, m0, n0);
-      float* sb = any_bias ? sbias + acc * BN : nullptr;
-      float* scs = scolsum + acc * BN;
+      float* sb = any_bias ? sbias + (local & 1) * BN : nullptr;      // staging stays double-buffered
+      float* scs = scolsum + (local & 1) * BN;
       if (any_bias || fold) {
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const long long img = p.batch > 1 ? (long long)bt : (long long)(m0 / p.bias2_div);
