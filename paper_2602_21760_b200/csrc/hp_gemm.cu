@@ -54,6 +54,8 @@ struct GemmParams {
   __nv_bfloat16* ln_y; long long ldy;
   const __nv_bfloat16* res; long long ldr;
   int act;
+  int probe_noepi;
+  int raster_n;                    // pair kernel tile order: 1 = N tiles fastest                 // dev probe (HP_GEMM_PROBE_NOEPI=1): skip the plain epilogue's stores
   float alpha;
   const float* colscale;
   int batch;                       // >= 1; plain mode only
@@ -592,10 +594,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   pdl_trigger();
 
   auto decode = [&](int tile, int& bt, int& m0, int& n0) {
-    const int mt = tile % mp_all;
+    int mt, nt;
+    if (p.raster_n) { nt = tile % p.num_n_tiles; mt = tile / p.num_n_tiles; }   // N fastest
+    else { mt = tile % mp_all; nt = tile / mp_all; }                              // M fastest
     bt = mt / p.num_m_tiles;
     m0 = (mt - bt * p.num_m_tiles) * (2 * BM) + (int)rank * BM;   // this CTA's 128 rows
-    n0 = (tile / mp_all) * BN;
+    n0 = nt * BN;
   };
 
   if (warp == 0) {
@@ -707,7 +711,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       } else if (p.stats_out) {
         epilogue_tile<BN, kEpiStats>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       } else {
-        epilogue_tile<BN, kEpiPlain>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+        if (!p.probe_noepi) epilogue_tile<BN, kEpiPlain>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       }
       tc_fence_before();
       __syncwarp();
@@ -849,12 +853,15 @@ int pick_bn(int64_t M, int64_t N, int act) {
   const bool pair = pair_enabled() && M > BM;
   const int64_t mt = pair ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM;
   const int sms = (g_num_sms ? g_num_sms : 148) / (pair ? 2 : 1);
+  // measured main-loop rate per SM relative to block_n 256 (pair kernel, B200): every MMA
+  // re-reads its 128-row A slab from shared memory, so wide N tiles amortise it best
+  auto rate = [](int bn) { return bn >= 256 ? 1.0 : bn >= 160 ? 0.72 : bn >= 128 ? 0.6 : 0.35; };
   for (int bn : cands) {
     if (N % bn) continue;
     if (act == HP_ACT_GEGLU && bn != 256 && bn != 128) continue;
     const int64_t tiles = mt * (N / bn);
     const int64_t waves = (tiles + sms - 1) / sms;
-    const double cost = (double)waves * (bn + 48);
+    const double cost = (double)waves * (bn / rate(bn) + 48);
     if (cost < best_cost - 1e-9) { best_cost = cost; best = bn; }
   }
   return best;
@@ -902,6 +909,8 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   p.vec256 = ((d->ldd % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->d) & 31) == 0) &&
              (!d->residual || (((d->ldr % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->residual) & 31) == 0))) &&
              (p.batch <= 1 || (((d->d_bstride | d->r_bstride) % 16) == 0));
+  p.probe_noepi = getenv("HP_GEMM_PROBE_NOEPI") != nullptr;
+  p.raster_n = getenv("HP_GEMM_RASTER_N") != nullptr;
   p.stats_out = reinterpret_cast<float2*>(d->stats_out);
   if (p.stats_out && (p.batch > 1 || d->act == HP_ACT_GEGLU || p.ln_mode || d->a_mode != HP_A_PLAIN ||
                       (reinterpret_cast<uintptr_t>(d->stats_out) & 7)))

@@ -12,6 +12,33 @@ from paper_2602_21760_b200.denoiser import kernels as K  # noqa: E402
 
 
 def main():
+    if sys.argv[1] == "conv":      # conv n h w cin cout stride [bn] [reps]
+        n, h, w, ci, co, st = (int(v) for v in sys.argv[2:8])
+        bn = int(sys.argv[8]) if len(sys.argv) > 8 else 0
+        reps = int(sys.argv[9]) if len(sys.argv) > 9 else 20
+        x = torch.randn(n * h * w, ci, device="cuda").bfloat16()
+        wt = (torch.randn(co, 9 * ci, device="cuda") * (9 * ci) ** -0.5).bfloat16()
+        bias = torch.randn(co, device="cuda")
+        M = n * (h // st) * (w // st)
+        out = torch.empty(M, co, device="cuda", dtype=torch.bfloat16)
+        run = lambda: K.gemm(x, wt, bias=bias, out=out, block_n=bn, conv=(n, h, w, ci, st))  # noqa: E731
+        for _ in range(3):
+            run()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                run()
+        g.replay()
+        torch.cuda.synchronize()
+        s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_.record()
+        g.replay()
+        e_.record()
+        torch.cuda.synchronize()
+        ms = s_.elapsed_time(e_) / reps
+        print(f"conv n={n} {h}x{w} {ci}->{co} s{st} bn={bn} graph: {ms * 1e3:.1f} us "
+              f"{2.0 * M * co * 9 * ci / ms / 1e9:.1f} TFLOP/s")
+        return
     M, N, Kd = (int(v) for v in sys.argv[1:4])
     bn = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     act = int(sys.argv[5]) if len(sys.argv) > 5 else 0
