@@ -80,12 +80,30 @@ gn_stats_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
     float sum[8] = {0}, sq[8] = {0};
     if (r < rows) {
       const int ch = j * 8;
-      for (int64_t p = p_begin + r; p < p_end; p += rows) {
-        float v[8];
-        if (ch < c1) load8(x1 + ((int64_t)n * hw + p) * c1 + ch, v);
-        else load8(x2 + ((int64_t)n * hw + p) * c2 + (ch - c1), v);
+      const bf16* src = ch < c1 ? x1 + (int64_t)n * hw * c1 + ch : x2 + (int64_t)n * hw * c2 + (ch - c1);
+      const int64_t st = ch < c1 ? c1 : c2;
+      int64_t p = p_begin + r;
+      // four 16-byte loads in flight per thread (the loop is latency-bound otherwise)
+      for (; p + 3 * rows < p_end; p += 4 * rows) {
+        uint4 u[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) { sum[i] += v[i]; sq[i] += v[i] * v[i]; }
+        for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(src + (p + k * rows) * st);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[k]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h[i]);
+            sum[2 * i] += f.x; sq[2 * i] = fmaf(f.x, f.x, sq[2 * i]);
+            sum[2 * i + 1] += f.y; sq[2 * i + 1] = fmaf(f.y, f.y, sq[2 * i + 1]);
+          }
+        }
+      }
+      for (; p < p_end; p += rows) {
+        float v[8];
+        load8(src + p * st, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { sum[i] += v[i]; sq[i] = fmaf(v[i], v[i], sq[i]); }
       }
     }
 #pragma unroll
@@ -176,7 +194,30 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
     const bool first = ch < c1;
     const bf16* src = first ? xa + ch : xb + (ch - c1);
     const int64_t sstride = first ? c1 : c2;
-    for (int64_t p = (int64_t)blockIdx.x * rows + r; p < hw; p += (int64_t)gridDim.x * rows) {
+    const int64_t step = (int64_t)gridDim.x * rows;
+    int64_t p = (int64_t)blockIdx.x * rows + r;
+    for (; p + 3 * step < hw; p += 4 * step) {         // four loads in flight
+      uint4 u[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(src + (p + k * step) * sstride);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[k]);
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          v[2 * i] = f.x; v[2 * i + 1] = f.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float o = fmaf(v[i], av[i], bv[i]);
+          v[i] = do_silu ? silu_fast(o) : o;
+        }
+        store8(yo + (p + k * step) * C + ch, v);
+      }
+    }
+    for (; p < hw; p += step) {
       float v[8];
       load8(src + p * sstride, v);
 #pragma unroll
