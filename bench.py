@@ -45,6 +45,19 @@ UNIT = "s/image"
 STEPS_T = 50
 
 
+def _forward_traffic():
+    """DRAM bytes of one forward from the committed ncu launch list (profiles/):
+    dram__bytes_read.sum + dram__bytes_write.sum summed over the forward's kernels."""
+    path = os.path.join(ROOT, "profiles", "r01", "forward_r1c_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        return {"traffic": t["dram_bytes"], "traffic_unit": "bytes per forward",
+                "traffic_source": os.path.relpath(path, ROOT) + " (ncu replay, cold caches per kernel: upper bound)"}
+    except Exception:
+        return {"traffic": None}
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -408,7 +421,7 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "denoiser forward (tcgen05 GEMM/conv + attention), B=2",
                      "achieved": achieved, "peak": bf16_sus, "unit": "TFLOP/s", "frac": achieved / bf16_sus,
                      "peak_kind": f"{peak_src} sustained", "frac_of_burst": achieved / bf16_burst,
-                     "flops_per_launch": fwd_flops, "forward_ms": fwd_s * 1e3, "traffic": None},
+                     "flops_per_launch": fwd_flops, "forward_ms": fwd_s * 1e3, **_forward_traffic()},
         "sampler_roofline": {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_src,
                              "sizes": list(samp.values())},
         "clocks": clocks.summary(),
