@@ -21,6 +21,7 @@
 #include <stdint.h>
 #include <math.h>
 #include <mutex>
+#include <stdlib.h>
 #include "hybridpar_b200_denoiser.h"
 #include "hp_common.cuh"
 #include "hp_tc.cuh"
@@ -128,21 +129,47 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // and one K/V stage suffices: 256 TMEM columns and 97 KB of smem, so two CTAs
 // share an SM and one's latency chain (TMA -> MMA -> softmax -> PV -> store)
 // overlaps the other's.
-template <bool SINGLE>
-__global__ void __launch_bounds__(kThreads, SINGLE ? 2 : 1)
+//
+// SOLO: one query tile per CTA (4 softmax warps + TMA + MMA warp, 256 TMEM
+// columns, 2 K/V stages, 112 KB smem), two CTAs per SM. Twice the units of the
+// two-tile CTA, so the last partial wave of a 160- or 320-unit grid on 148 SMs
+// is half as long, and a lone CTA in that wave runs its softmax without a
+// co-resident tile competing for MUFU/FMA.
+constexpr int kModePair = 0, kModeSingle = 1, kModeSolo = 2;
+template <int MODE> struct AttnCfg {
+  static constexpr bool kSingle = MODE == kModeSingle;
+  static constexpr int kNq = MODE == kModeSolo ? 1 : 2;
+  static constexpr int kThr = 32 * (4 * kNq + 2);
+  static constexpr int kMinBlocks = MODE == kModePair ? 1 : 2;
+  static constexpr int kSt = kSingle ? 1 : (MODE == kModeSolo ? 2 : kStages);
+  static constexpr uint32_t kCols = MODE == kModePair ? kTmemCols : 256;
+  static constexpr size_t kSmem = kSingle ? kTileBytes * 5 + 256
+                                          : (size_t)kTileBytes * (kNq + 2 * kSt) + kNq * kPBytes + 256;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(AttnCfg<MODE>::kThr, AttnCfg<MODE>::kMinBlocks)
 attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, AttnParams p) {
-  constexpr int kSt = SINGLE ? 1 : kStages;
-  constexpr uint32_t kCols = SINGLE ? 256 : kTmemCols;
+  using Cfg = AttnCfg<MODE>;
+  constexpr bool SINGLE = Cfg::kSingle;
+  constexpr int NQ = Cfg::kNq;
+  constexpr int kSt = Cfg::kSt;
+  constexpr uint32_t kCols = Cfg::kCols;
+  constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if constexpr (MODE == kModeSolo) {
+    // the launch requests no alignment slack (two CTAs must fit an SM)
+    if (smem_u32(smem_raw) & 1023) __trap();
+  }
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                                  // 2 tiles
-  uint8_t* sK = sQ + 2 * kTileBytes;
+  uint8_t* sQ = smem;                                  // NQ tiles
+  uint8_t* sK = sQ + NQ * kTileBytes;
   uint8_t* sV = sK + kSt * kTileBytes;
   uint8_t* sP = sV + kSt * kTileBytes;                // 2 tiles (one P buffer per query tile)
   // SINGLE: P_0 overwrites Q_0|Q_1 and P_1 overwrites K|X once both S MMAs are done
   // (80 KB in all instead of 128 KB), so two CTAs fit an SM
-  uint64_t* bars = reinterpret_cast<uint64_t*>(SINGLE ? sP + kTileBytes : sP + 2 * kPBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(SINGLE ? sP + kTileBytes : sP + NQ * kPBytes);
   auto p_atom = [&](int q, int a) -> uint8_t* {       // 64-key SW128 atom a of P_q
     if constexpr (SINGLE) return q == 0 ? sQ + a * kTileBytes : (a == 0 ? sK : sP);
     return sP + q * kPBytes + a * (kBQ * 128);
@@ -157,17 +184,17 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y, b = blockIdx.z;
-  const int q0 = blockIdx.x * 2 * kBQ;
+  const int q0 = blockIdx.x * NQ * kBQ;
   const int J = SINGLE ? 1 : p.n_kv;
 
-  if (warp == 8 && lane == 0) {
+  if (warp == kTmaWarp && lane == 0) {
     prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
     mbar_init(q_full, 1);
     for (int s = 0; s < kSt; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1); }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<kCols>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<kCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -175,11 +202,11 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
   pdl_wait();
   pdl_trigger();
 
-  if (warp == 8) {
+  if (warp == kTmaWarp) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
-      tma_load_3d(sQ, &tmQ, q_full, p.q_col0 + h * kD, q0, b);
-      tma_load_3d(sQ + kTileBytes, &tmQ, q_full, p.q_col0 + h * kD, q0 + kBQ, b);
+      mbar_arrive_expect_tx(q_full, NQ * kTileBytes);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) tma_load_3d(sQ + q * kTileBytes, &tmQ, q_full, p.q_col0 + h * kD, q0 + q * kBQ, b);
       for (int j = 0; j < J; ++j) {
         const int s = j % kSt;
         mbar_wait(&kv_empty[s], ((j / kSt) & 1) ^ 1);
@@ -188,7 +215,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         tma_load_3d(sV + s * kTileBytes, &tmV, &kv_full[s], p.v_col0 + h * kD, j * kBK, b);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     if (lane == 0) {
       mbar_wait(q_full, 0);
       auto issue_s = [&](int q, int j) {
@@ -205,7 +232,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
           mbar_wait(&p_full[q], j & 1);
           tc_fence_after();
         }
-        const uint32_t d_o = tmem + (SINGLE ? q * kBK : 256 + q * kD);
+        const uint32_t d_o = tmem + (SINGLE ? q * kBK : NQ * kBK + q * kD);
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k) {
           const uint64_t da = sdesc_sw128_kmajor(p_atom(q, k >> 2)) + 2 * (k & 3);
@@ -217,7 +244,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
       for (int j = 0; j < J; ++j) {
         mbar_wait(&kv_full[j % kSt], (j / kSt) & 1);
         tc_fence_after();
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < NQ; ++q) {
           if (j > 0) {
             // S_q(j) overwrites S_q(j-1): the softmax has consumed it once P_q(j-1) is out
             mbar_wait(&p_full[q], (j - 1) & 1);
@@ -226,12 +253,11 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
           issue_s(q, j);
           if (j > 0) {
             issue_pv(q, j - 1, false);      // P_q(j-1) was waited for above
-            if (q == 1) umma_commit(&kv_empty[(j - 1) % kSt]);
+            if (q == NQ - 1) umma_commit(&kv_empty[(j - 1) % kSt]);
           }
         }
       }
-      issue_pv(0, J - 1, true);
-      issue_pv(1, J - 1, true);
+      for (int q = 0; q < NQ; ++q) issue_pv(q, J - 1, true);
       umma_commit(&kv_empty[(J - 1) % kSt]);
     }
   } else {
@@ -241,7 +267,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t t_s = tmem + lane_base + q * kBK;
-    const uint32_t t_o = tmem + lane_base + (SINGLE ? q * kBK : 256 + q * kD);
+    const uint32_t t_o = tmem + lane_base + (SINGLE ? q * kBK : NQ * kBK + q * kD);
     float m_run = -INFINITY, l_run = 0.f;
     const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
     for (int j = 0; j < J; ++j) {
@@ -360,7 +386,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 9) tmem_dealloc<kCols>(tmem);
+  if (warp == kMmaWarp) tmem_dealloc<kCols>(tmem);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -392,6 +418,41 @@ bool map3(CUtensorMap* m, const void* base, long long ld, int rows, int batch) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int MODE>
+int launch_attn(dim3 grid, cudaStream_t st, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                const AttnParams& p, size_t slack) {
+  const size_t smem = AttnCfg<MODE>::kSmem + slack;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(attn_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return HP_ERR_CUDA;
+    attr = true;
+  }
+  return hp_launch_pdl(attn_kernel<MODE>, grid, dim3(AttnCfg<MODE>::kThr), smem, st, tq, tk, tv, p) == cudaSuccess
+             ? HP_OK : HP_ERR_CUDA;
+}
+
+int num_sms_attn() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+bool solo_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HP_ATTN_SOLO");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 }  // namespace
 
 extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
@@ -413,27 +474,14 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   p.n_kv = (d->skv + kBK - 1) / kBK;
   dim3 grid((d->sq + 2 * kBQ - 1) / (2 * kBQ), d->heads, d->batch);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p.n_kv == 1) {
-    constexpr size_t smem = 1024 + kTileBytes * 5 + 256;
-    static bool attr1 = false;
-    if (!attr1) {
-      if (cudaFuncSetAttribute(attn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
-        return HP_ERR_CUDA;
-      attr1 = true;
-    }
-    return hp_launch_pdl(attn_kernel<true>, grid, dim3(kThreads), smem, st, tq, tk, tv, p) == cudaSuccess
-               ? HP_OK : HP_ERR_CUDA;
+  if (p.n_kv == 1) return launch_attn<kModeSingle>(grid, st, tq, tk, tv, p, 1024);
+  // one query tile per CTA when the two-tile grid would leave a short last wave
+  const int pair_ctas = grid.x * grid.y * grid.z;
+  const int sms = num_sms_attn();
+  const int tail = pair_ctas % sms;
+  if (solo_enabled() && tail != 0 && tail * 2 < sms) {
+    dim3 g1((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
+    return launch_attn<kModeSolo>(g1, st, tq, tk, tv, p, 0);
   }
-  constexpr size_t smem = 1024 + kTileBytes * (2 + 2 * kStages) + 2 * kPBytes + 256;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(attn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return HP_ERR_CUDA;
-    attr = true;
-  }
-  if (hp_launch_pdl(attn_kernel<false>, grid, dim3(kThreads), smem, st, tq, tk, tv, p) != cudaSuccess)
-    return HP_ERR_CUDA;
-  return HP_OK;
+  return launch_attn<kModePair>(grid, st, tq, tk, tv, p, 1024);
 }
