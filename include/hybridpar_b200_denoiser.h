@@ -77,7 +77,7 @@ typedef struct hp_gemm_desc {
 
 int hp_gemm(const hp_gemm_desc* d, void* stream);
 /* block_n the auto heuristic would choose (0 if unsupported shape) */
-int32_t hp_gemm_pick_block_n(int64_t M, int64_t N, int32_t act);
+int32_t hp_gemm_pick_block_n(int64_t M, int64_t N, int64_t K, int32_t act);
 
 /* ---- fused multi-head attention (tcgen05 S = QK^T and O = PV) -------------- */
 /* q: [B, Sq, ldq] with head h at column h*64 (+q_col0); k/v likewise with

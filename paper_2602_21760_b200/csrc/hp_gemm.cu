@@ -553,11 +553,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   constexpr uint32_t kBHalfBytes = (BN / 2) * BK * 2;
   constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
+  // BN > 256 (320): two N=160 MMAs per K step into adjacent TMEM columns. Shared memory
+  // bandwidth (TMA writes + MMA operand reads) bounds narrow tiles; a 320-wide tile moves
+  // 88 KB per 640 MMA cycles per SM where two 160-wide tiles move 104 KB.
+  constexpr int kSub = BN > 256 ? 2 : 1;
+  constexpr int kSubN = BN / kSub;
+  constexpr uint32_t kSubBytes = (kSubN / 2) * BK * 2;
   // as many TMEM accumulator buffers as fit: the epilogue of one tile may lag the MMAs by
   // several tiles without stalling the tensor core
-  constexpr int kAcc = BN <= 128 ? 4 : (BN <= 170 ? 3 : 2);
+  constexpr int kAcc = BN > 256 ? 1 : (BN <= 128 ? 4 : (BN <= 170 ? 3 : 2));
   constexpr uint32_t kTmemCols = (kAcc * BN <= 64) ? 64 : (kAcc * BN <= 128) ? 128 : (kAcc * BN <= 256) ? 256 : 512;
-  constexpr uint32_t kIdesc = idesc_bf16_f32(2 * BM, BN);
+  constexpr uint32_t kIdesc = idesc_bf16_f32(2 * BM, kSubN);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -617,7 +623,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           y0 = rem / p.out_w;
           x0 = rem - y0 * p.out_w;
         }
-        const int nb = n0 + (int)rank * (BN / 2);
+        const int nb = n0 + (int)rank * (kSubN / 2);
         for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -638,7 +644,9 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, 2 * x0 + dx - 1, 2 * y0 + dy - 1, img);
             }
           }
-          tma_load_2d_pair(smB + s * kBHalfBytes, &tmB, fb, kb * BK, nb);
+#pragma unroll
+          for (int sub = 0; sub < kSub; ++sub)
+            tma_load_2d_pair(smB + s * kBHalfBytes + sub * kSubBytes, &tmB, fb, kb * BK, nb + sub * kSubN);
         }
       }
     }
@@ -658,10 +666,14 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint64_t da = sdesc_sw128_kmajor(smA + s * kABytes);
-          const uint64_t db = sdesc_sw128_kmajor(smB + s * kBHalfBytes);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16_pair(d_tmem, da + 2 * k, db + 2 * k, kIdesc, (kb | k) ? 1u : 0u);
+          for (int k = 0; k < BK / 16; ++k) {
+#pragma unroll
+            for (int sub = 0; sub < kSub; ++sub) {
+              const uint64_t db = sdesc_sw128_kmajor(smB + s * kBHalfBytes + sub * kSubBytes);
+              umma_bf16_pair(d_tmem + sub * kSubN, da + 2 * k, db + 2 * k, kIdesc, (kb | k) ? 1u : 0u);
+            }
+          }
           umma_commit_pair(&empty[s], 0x3);
         }
         umma_commit_pair(&tfull[acc], 0x3);
@@ -846,22 +858,30 @@ bool pair_enabled() {
   return on == 1;
 }
 
-int pick_bn(int64_t M, int64_t N, int act) {
-  const int cands[4] = {256, 160, 128, 64};
+// block_n for an M x N x K problem: whole-wave tile counts on the SMs (CTA pairs for
+// M > 128) times the per-tile time, k-blocks x N / (measured main-loop rate of that
+// width), plus exposed epilogues (~5 k-blocks' worth each). 320 keeps one accumulator
+// (no epilogue/MMA overlap), so each of its tiles exposes one.
+int pick_bn(int64_t M, int64_t N, int64_t K, int act) {
+  const int cands[5] = {320, 256, 160, 128, 64};
   int best = 0;
   double best_cost = 1e30;
   const bool pair = pair_enabled() && M > BM;
   const int64_t mt = pair ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM;
   const int sms = (g_num_sms ? g_num_sms : 148) / (pair ? 2 : 1);
+  const double kb = (double)((K + BK - 1) / BK);
   // measured main-loop rate per SM relative to block_n 256 (pair kernel, B200): every MMA
   // re-reads its 128-row A slab from shared memory, so wide N tiles amortise it best
   auto rate = [](int bn) { return bn >= 256 ? 1.0 : bn >= 160 ? 0.72 : bn >= 128 ? 0.6 : 0.35; };
   for (int bn : cands) {
     if (N % bn) continue;
+    if (bn > 256 && (!pair || act == HP_ACT_GEGLU)) continue;    // 320 = two N=160 MMAs, pair kernel only
     if (act == HP_ACT_GEGLU && bn != 256 && bn != 128) continue;
     const int64_t tiles = mt * (N / bn);
     const int64_t waves = (tiles + sms - 1) / sms;
-    const double cost = (double)waves * (bn / rate(bn) + 48);
+    // the last tile's epilogue is always exposed; with one accumulator (320) every tile's is
+    const double epi = 5.0 * bn;
+    const double cost = (double)waves * (kb * bn / rate(bn) + 48.0) + epi * (bn > 256 ? (double)waves : 1.0);
     if (cost < best_cost - 1e-9) { best_cost = cost; best = bn; }
   }
   return best;
@@ -871,7 +891,7 @@ int pick_bn(int64_t M, int64_t N, int act) {
 
 extern "C" {
 
-int32_t hp_gemm_pick_block_n(int64_t M, int64_t N, int32_t act) { return pick_bn(M, N, act); }
+int32_t hp_gemm_pick_block_n(int64_t M, int64_t N, int64_t K, int32_t act) { return pick_bn(M, N, K, act); }
 
 int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if (!d || !d->a || !d->b || !d->d) return HP_ERR_PARAMETER;
@@ -879,7 +899,7 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if ((d->K % 8) || (d->ldb % 8)) return HP_ERR_UNSUPPORTED;   // 16-byte TMA strides
   if ((reinterpret_cast<uintptr_t>(d->a) | reinterpret_cast<uintptr_t>(d->b)) & 15) return HP_ERR_UNSUPPORTED;
   num_sms();
-  const int bn = d->block_n ? d->block_n : pick_bn(d->M * (d->batch > 1 ? d->batch : 1), d->N, d->act);
+  const int bn = d->block_n ? d->block_n : pick_bn(d->M * (d->batch > 1 ? d->batch : 1), d->N, d->K, d->act);
   if (bn == 0 || d->N % bn) return HP_ERR_UNSUPPORTED;
   if (d->act == HP_ACT_GEGLU && (bn % 64)) return HP_ERR_UNSUPPORTED;
   const int64_t n_out = d->act == HP_ACT_GEGLU ? d->N / 2 : d->N;
@@ -971,13 +991,14 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   {
     const uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)d->N};
     const uint64_t str[1] = {(uint64_t)d->ldb * 2};
-    const uint32_t box[2] = {BK, (uint32_t)(pair ? bn / 2 : bn)};
+    const uint32_t box[2] = {BK, (uint32_t)(pair ? (bn > 256 ? bn / 4 : bn / 2) : bn)};
     if (!make_map(&tb, d->b, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (pair) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
     switch (bn) {
+      case 320: return launch_gemm_pair<320, 5>(ta, tb, p, st);
       case 256: return launch_gemm_pair<256, 6>(ta, tb, p, st);
       case 160: return launch_gemm_pair<160, 7>(ta, tb, p, st);
       case 128: return launch_gemm_pair<128, 8>(ta, tb, p, st);

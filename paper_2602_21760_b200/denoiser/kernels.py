@@ -66,7 +66,7 @@ class HpAttnDesc(C.Structure):
 
 SIGNATURES = {
     "hp_gemm": (C.c_int, [C.POINTER(HpGemmDesc), _VP]),
-    "hp_gemm_pick_block_n": (_I32, [_I64, _I64, _I32]),
+    "hp_gemm_pick_block_n": (_I32, [_I64, _I64, _I64, _I32]),
     "hp_attention": (C.c_int, [C.POINTER(HpAttnDesc), _VP]),
     "hp_group_norm": (C.c_int, [_VP, _I32, _VP, _I32, _I32, _I64, _I32, _F32, _VP, _VP, _I32, _VP, _VP, _VP]),
     "hp_layer_norm": (C.c_int, [_VP, _I64, _I32, _F32, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
@@ -193,7 +193,7 @@ def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, a
         g, b_, eps, y = ln
         d.ln_gamma, d.ln_beta, d.ln_eps, d.ln_y, d.ldy = _p(g), _p(b_), float(eps), _p(y), y.stride(-2)
     if stats_out is not None:
-        bn = int(block_n) or int(lib.hp_gemm_pick_block_n(M, Nn, int(act)))
+        bn = int(block_n) or int(lib.hp_gemm_pick_block_n(M, Nn, K, int(act)))
         if bn == 0 or Nn % bn or stats_out.buf.numel() < 2 * M * (Nn // bn):
             raise ShapeError(f"row stats: N={Nn} block_n={bn} capacity {stats_out.buf.numel()}")
         d.block_n = bn

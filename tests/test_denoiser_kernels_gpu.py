@@ -29,7 +29,8 @@ def rnd(*shape, s=1.0):
 @pytest.mark.parametrize("M,N,Kd,bn", [(128, 64, 64, 0), (256, 256, 128, 0), (2048, 1280, 1280, 0),
                                        (154, 640, 2048, 0), (8192, 320, 640, 0), (300, 128, 72, 0),
                                        (1024, 512, 256, 64), (1024, 512, 256, 128), (1024, 512, 256, 256),
-                                       (640, 320, 320, 160)])
+                                       (640, 320, 320, 160), (2048, 640, 640, 320), (8192, 1280, 640, 320),
+                                       (300, 640, 192, 320)])
 def test_gemm_plain(M, N, Kd, bn):
     torch.manual_seed(M + N + Kd)
     a, w = rnd(M, Kd), rnd(N, Kd, s=Kd ** -0.5)
@@ -74,7 +75,8 @@ def test_gemm_geglu(bn):
 @pytest.mark.parametrize("n,h,w,c,co,stride", [(2, 32, 32, 64, 128, 1), (1, 128, 128, 64, 64, 1),
                                                (2, 64, 64, 128, 256, 1), (1, 256, 256, 64, 64, 1),
                                                (2, 64, 64, 64, 64, 2), (2, 128, 128, 64, 128, 2),
-                                               (1, 16, 16, 192, 320, 1)])
+                                               (1, 16, 16, 192, 320, 1), (2, 64, 64, 128, 640, 1),
+                                               (2, 128, 128, 64, 320, 1)])
 def test_conv3x3_implicit_gemm(n, h, w, c, co, stride):
     torch.manual_seed(h + c)
     x = rnd(n, h, w, c)
