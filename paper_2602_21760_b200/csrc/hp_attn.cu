@@ -67,22 +67,6 @@ __device__ __forceinline__ float ex2f(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ uint64_t pack2(float a, float b) {
-  return ((uint64_t)__float_as_uint(b) << 32) | (uint64_t)__float_as_uint(a);
-}
-__device__ __forceinline__ uint64_t pack2u(uint32_t a, uint32_t b) { return ((uint64_t)b << 32) | (uint64_t)a; }
-__device__ __forceinline__ float lo2(uint64_t v) { return __uint_as_float((uint32_t)v); }
-__device__ __forceinline__ float hi2(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
 // 2^x for a pair (x <= 0) on the FMA pipe: x = i + f, |f| <= 1/2, 2^f by a degree-4
 // polynomial, then i added into the exponent field (t = x + 1.5*2^23 holds i in its mantissa)
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {

@@ -91,6 +91,16 @@ __device__ __forceinline__ void fold_row_stats(const GemmParams& p, int row, flo
   rstd = rsqrtf(fmaxf(m2, 0.f) / n + p.ln_fold_eps);
 }
 
+// pull this thread's residual row segment into L1 before the accumulator is ready
+template <int BN>
+__device__ __forceinline__ void prefetch_res_row(const GemmParams& p, int bt, int row, int n0) {
+  if (!p.res || row >= p.M || p.act == HP_ACT_GEGLU) return;
+  const char* r = reinterpret_cast<const char*>(p.res + (p.batch > 1 ? (long long)bt * p.r_bs : 0) +
+                                                (long long)row * p.ldr + n0);
+#pragma unroll
+  for (int off = 0; off < BN * 2; off += 128) asm volatile("prefetch.global.L1 [%0];" :: "l"(r + off));
+}
+
 // epilogue flavours (one template instance each, chosen per launch)
 constexpr int kEpiPlain = 0, kEpiStats = 1, kEpiFold = 2;
 
@@ -123,6 +133,30 @@ __device__ __forceinline__ float gelu_erf(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.44269504088896341f * z * z));
   const float h = 0.5f * x * (poly * t * e);    // 0.5 x (1 - erf(z))
   return x >= 0.f ? x - h : h;
+}
+
+// the same GELU on a packed pair: the polynomial / scaling on FFMA2/FMUL2, two MUFU each
+// for the reciprocal and the exponential (0.5 folded into the coefficients)
+__device__ __forceinline__ uint64_t gelu_erf2(uint64_t x2) {
+  const float x0 = lo2(x2), x1 = hi2(x2);
+  const uint64_t z2 = fmul2(pack2(fabsf(x0), fabsf(x1)), pack2(0.70710678118654752f, 0.70710678118654752f));
+  const uint64_t d2 = ffma2(pack2(0.3275911f, 0.3275911f), z2, pack2(1.0f, 1.0f));
+  float t0, t1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t0) : "f"(lo2(d2)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t1) : "f"(hi2(d2)));
+  const uint64_t t2 = pack2(t0, t1);
+  uint64_t poly = ffma2(t2, pack2(0.5307027145f, 0.5307027145f), pack2(-0.7265760135f, -0.7265760135f));
+  poly = ffma2(poly, t2, pack2(0.7107068705f, 0.7107068705f));
+  poly = ffma2(poly, t2, pack2(-0.142248368f, -0.142248368f));
+  poly = ffma2(poly, t2, pack2(0.127414796f, 0.127414796f));
+  poly = fmul2(poly, t2);
+  const uint64_t arg = fmul2(fmul2(z2, z2), pack2(-1.44269504088896341f, -1.44269504088896341f));
+  float e0, e1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(lo2(arg)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(hi2(arg)));
+  const uint64_t h = fmul2(x2, fmul2(poly, pack2(e0, e1)));     // 0.5 x (1 - erf(|x|/sqrt2))
+  const float h0 = lo2(h), h1 = hi2(h);
+  return pack2(x0 >= 0.f ? x0 - h0 : h0, x1 >= 0.f ? x1 - h1 : h1);
 }
 
 // 64 contiguous bytes of one output row: two 256-bit stores when 32-byte aligned
@@ -182,26 +216,30 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
       if (!row_ok) continue;
       const int ocol = out0 + c * 32;
       uint32_t packed[16];
+      const bool scale = p.alpha != 1.0f;
+      const uint64_t alpha2 = pack2(p.alpha, p.alpha);
+      const uint64_t nmean2 = pack2(-f_mean, -f_mean), rstd2 = pack2(f_rstd, f_rstd);
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
-        float a0 = __uint_as_float(ra[j]) * p.alpha, a1 = __uint_as_float(ra[j + 1]) * p.alpha;
-        float g0 = __uint_as_float(rg[j]) * p.alpha, g1 = __uint_as_float(rg[j + 1]) * p.alpha;
+        uint64_t a2 = pack2u(ra[j], ra[j + 1]), g2 = pack2u(rg[j], rg[j + 1]);
+        if (scale) { a2 = fmul2(a2, alpha2); g2 = fmul2(g2, alpha2); }
         if constexpr (EPI == kEpiFold) {
-          const float* cs = scs + c * 32 + j;
-          a0 = f_rstd * fmaf(-f_mean, cs[0], a0);
-          a1 = f_rstd * fmaf(-f_mean, cs[1], a1);
-          g0 = f_rstd * fmaf(-f_mean, cs[BN / 2], g0);
-          g1 = f_rstd * fmaf(-f_mean, cs[BN / 2 + 1], g1);
+          const float2 ca = *reinterpret_cast<const float2*>(scs + c * 32 + j);
+          const float2 cg = *reinterpret_cast<const float2*>(scs + BN / 2 + c * 32 + j);
+          a2 = fmul2(rstd2, ffma2(nmean2, pack2(ca.x, ca.y), a2));
+          g2 = fmul2(rstd2, ffma2(nmean2, pack2(cg.x, cg.y), g2));
         }
         if (sb) {
-          a0 += sb[c * 32 + j];
-          a1 += sb[c * 32 + j + 1];
-          g0 += sb[BN / 2 + c * 32 + j];
-          g1 += sb[BN / 2 + c * 32 + j + 1];
+          const float2 ba = *reinterpret_cast<const float2*>(sb + c * 32 + j);
+          const float2 bg = *reinterpret_cast<const float2*>(sb + BN / 2 + c * 32 + j);
+          a2 = fadd2(a2, pack2(ba.x, ba.y));
+          g2 = fadd2(g2, pack2(bg.x, bg.y));
         }
-        packed[j / 2] = pack_bf16(a0 * gelu_erf(g0), a1 * gelu_erf(g1));
+        const uint64_t o2 = fmul2(a2, gelu_erf2(g2));
+        packed[j / 2] = pack_bf16(lo2(o2), hi2(o2));
       }
-      st_row64(p.d + (long long)row * p.ldd + ocol, packed, p.vec256);
+      if (p.probe_noepi != 2) st_row64(p.d + (long long)row * p.ldd + ocol, packed, p.vec256);
+      else if (packed[0] == 0x7fc07fc0u) p.d[row] = __float2bfloat16(0.f);   // keep the math live
     }
     return;
   }
@@ -222,18 +260,23 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     tmem_ld_wait();
     if (!row_ok) continue;
     const int col = n0 + c * 32;
-    float v[32];
+    // packed fp32 pairs throughout: v2[q] = columns (2q, 2q+1) of this chunk
+    uint64_t v2[16];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+    for (int q = 0; q < 16; ++q) v2[q] = pack2u(r[2 * q], r[2 * q + 1]);
+    if (p.alpha != 1.0f) {
+      const uint64_t alpha2 = pack2(p.alpha, p.alpha);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v2[q] = fmul2(v2[q], alpha2);
+    }
     if constexpr (EPI == kEpiFold) {
+      const uint64_t nmean2 = pack2(-f_mean, -f_mean), rstd2 = pack2(f_rstd, f_rstd);
       const float4* c4 = reinterpret_cast<const float4*>(scs + c * 32);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float4 cs = c4[q];
-        v[4 * q] = f_rstd * fmaf(-f_mean, cs.x, v[4 * q]);
-        v[4 * q + 1] = f_rstd * fmaf(-f_mean, cs.y, v[4 * q + 1]);
-        v[4 * q + 2] = f_rstd * fmaf(-f_mean, cs.z, v[4 * q + 2]);
-        v[4 * q + 3] = f_rstd * fmaf(-f_mean, cs.w, v[4 * q + 3]);
+        v2[2 * q] = fmul2(rstd2, ffma2(nmean2, pack2(cs.x, cs.y), v2[2 * q]));
+        v2[2 * q + 1] = fmul2(rstd2, ffma2(nmean2, pack2(cs.z, cs.w), v2[2 * q + 1]));
       }
     }
     if (sb) {
@@ -241,36 +284,38 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float4 b = b4[q];
-        v[4 * q] += b.x; v[4 * q + 1] += b.y; v[4 * q + 2] += b.z; v[4 * q + 3] += b.w;
+        v2[2 * q] = fadd2(v2[2 * q], pack2(b.x, b.y));
+        v2[2 * q + 1] = fadd2(v2[2 * q + 1], pack2(b.z, b.w));
       }
     }
     if (p.act == HP_ACT_GELU) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+      for (int q = 0; q < 16; ++q) v2[q] = gelu_erf2(v2[q]);
     } else if (p.act == HP_ACT_SILU) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = silu_f(v[j]);
+      for (int q = 0; q < 16; ++q) v2[q] = pack2(silu_f(lo2(v2[q])), silu_f(hi2(v2[q])));
     }
     if (p.colscale) {
       const float4* g4 = reinterpret_cast<const float4*>(p.colscale + col);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float4 g = __ldg(g4 + q);
-        v[4 * q] *= g.x; v[4 * q + 1] *= g.y; v[4 * q + 2] *= g.z; v[4 * q + 3] *= g.w;
+        v2[2 * q] = fmul2(v2[2 * q], pack2(g.x, g.y));
+        v2[2 * q + 1] = fmul2(v2[2 * q + 1], pack2(g.z, g.w));
       }
     }
     if (has_res) {
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const float2 f = unpack_bf16(rc[q]);
-        v[2 * q] += f.x;
-        v[2 * q + 1] += f.y;
+        v2[q] = fadd2(v2[q], pack2(f.x, f.y));
       }
     }
     uint32_t w[16];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) w[q] = pack_bf16(v[2 * q], v[2 * q + 1]);
-    st_row64(p.d + (long long)row * p.ldd + col, w, p.vec256);
+    for (int q = 0; q < 16; ++q) w[q] = pack_bf16(lo2(v2[q]), hi2(v2[q]));
+    if (p.probe_noepi != 2) st_row64(p.d + (long long)row * p.ldd + col, w, p.vec256);
+    else if (w[0] == 0x7fc07fc0u) p.d[row] = __float2bfloat16(0.f);          // keep the math live
     if constexpr (EPI == kEpiStats) {
       if (c == 0) sh_k = unpack_bf16(w[0]).x;
 #pragma unroll
@@ -500,6 +545,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       float f_mean = 0.f, f_rstd = 1.f;
       const int my_row = m0 + quarter * 32 + lane;
       if (fold && my_row < p.M) fold_row_stats(p, my_row, f_mean, f_rstd);
+      prefetch_res_row<BN>(p, bt, my_row, n0);     // residual lines in flight while the MMAs finish
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       const uint32_t t_acc = tmem_base + acc * BN;
@@ -709,6 +755,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       float f_mean = 0.f, f_rstd = 1.f;
       const int my_row = m0 + quarter * 32 + lane;
       if (fold && my_row < p.M) fold_row_stats(p, my_row, f_mean, f_rstd);
+      prefetch_res_row<BN>(p, bt, my_row, n0);     // residual lines in flight while the MMAs finish
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       const uint32_t t_acc = tmem_base + acc * BN;
@@ -723,7 +770,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       } else if (p.stats_out) {
         epilogue_tile<BN, kEpiStats>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       } else {
-        if (!p.probe_noepi) epilogue_tile<BN, kEpiPlain>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+        if (p.probe_noepi != 1) epilogue_tile<BN, kEpiPlain>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       }
       tc_fence_before();
       __syncwarp();
@@ -929,7 +976,10 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   p.vec256 = ((d->ldd % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->d) & 31) == 0) &&
              (!d->residual || (((d->ldr % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->residual) & 31) == 0))) &&
              (p.batch <= 1 || (((d->d_bstride | d->r_bstride) % 16) == 0));
-  p.probe_noepi = getenv("HP_GEMM_PROBE_NOEPI") != nullptr;
+  {
+    const char* e = getenv("HP_GEMM_PROBE_NOEPI");   // 1: skip the plain epilogue, 2: skip its stores
+    p.probe_noepi = e ? (e[0] == '2' ? 2 : 1) : 0;
+  }
   p.raster_n = getenv("HP_GEMM_RASTER_N") != nullptr;
   p.stats_out = reinterpret_cast<float2*>(d->stats_out);
   if (p.stats_out && (p.batch > 1 || d->act == HP_ACT_GEGLU || p.ln_mode || d->a_mode != HP_A_PLAIN ||

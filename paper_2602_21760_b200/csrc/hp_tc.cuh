@@ -179,6 +179,29 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// ---- packed fp32 pairs (FFMA2 / FADD2 / FMUL2: two lanes of work per instruction) ----
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+  return ((uint64_t)__float_as_uint(b) << 32) | (uint64_t)__float_as_uint(a);
+}
+__device__ __forceinline__ uint64_t pack2u(uint32_t a, uint32_t b) { return ((uint64_t)b << 32) | (uint64_t)a; }
+__device__ __forceinline__ float lo2(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi2(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 // instruction descriptor: bf16 x bf16 -> f32, both operands K-major (b_mn_major=1: B is N-major)
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N, uint32_t b_mn_major = 0) {
   return (1u << 4)            // c_format = F32
