@@ -78,6 +78,10 @@ typedef struct hp_gemm_desc {
 int hp_gemm(const hp_gemm_desc* d, void* stream);
 /* block_n the auto heuristic would choose (0 if unsupported shape) */
 int32_t hp_gemm_pick_block_n(int64_t M, int64_t N, int64_t K, int32_t act);
+/* block_n for a GEMM that writes LayerNorm row statistics (stats_out): chosen so the
+ * statistics segment width (160 when N % 160 == 0) and the split-K decision depend on
+ * N and K only, never on M (batch invariance of the folded LayerNorm). */
+int32_t hp_gemm_stats_block_n(int64_t M, int64_t N, int64_t K);
 
 /* ---- fused multi-head attention (tcgen05 S = QK^T and O = PV) -------------- */
 /* q: [B, Sq, ldq] with head h at column h*64 (+q_col0); k/v likewise with

@@ -120,23 +120,9 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& 
 }
 
 // exact-erf GELU x * Phi(x) with erf from Abramowitz-Stegun 7.1.26 (|erf error| <= 1.5e-7,
-// GELU error <= 2.2e-7 abs): one MUFU.RCP + one MUFU.EX2 + 8 FMA-pipe ops instead of erff
-__device__ __forceinline__ float gelu_erf(float x) {
-  const float z = fabsf(x) * 0.70710678118654752f;
-  float t;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
-  float poly = fmaf(t, 1.061405429f, -1.453152027f);
-  poly = fmaf(poly, t, 1.421413741f);
-  poly = fmaf(poly, t, -0.284496736f);
-  poly = fmaf(poly, t, 0.254829592f);
-  float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.44269504088896341f * z * z));
-  const float h = 0.5f * x * (poly * t * e);    // 0.5 x (1 - erf(z))
-  return x >= 0.f ? x - h : h;
-}
-
-// the same GELU on a packed pair: the polynomial / scaling on FFMA2/FMUL2, two MUFU each
-// for the reciprocal and the exponential (0.5 folded into the coefficients)
+// GELU error <= 2.2e-7 abs): one MUFU.RCP + one MUFU.EX2 per value instead of erff.
+// Packed pair: the polynomial / scaling on FFMA2/FMUL2, two MUFU each for the
+// reciprocal and the exponential (0.5 folded into the coefficients).
 __device__ __forceinline__ uint64_t gelu_erf2(uint64_t x2) {
   const float x0 = lo2(x2), x1 = hi2(x2);
   const uint64_t z2 = fmul2(pack2(fabsf(x0), fabsf(x1)), pack2(0.70710678118654752f, 0.70710678118654752f));
@@ -196,10 +182,19 @@ __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)
 
 // Epilogue for one 128 x BN tile; thread = one output row. `sb` is the tile's
 // column bias (bias + per-image bias2 folded) staged in shared memory, or null.
+// Statistics segments (stats_out) are kStatW columns wide: the whole tile, except
+// 320-wide tiles, which report two 160-column segments (so a split-K pair, where
+// each CTA finalises one half, writes the same layout).
+template <int BN> struct StatW { static constexpr int value = BN > 256 ? BN / 2 : BN; };
+
+// Epilogue columns [c_begin, c_begin + c_count) of one 128 x BN tile (default: all);
+// `red` (split-K) holds the other K half's fp32 partial for these columns in shared
+// memory, laid out [column / 4][128 rows][4].
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
                                               int lane, const float* sb, float* row_stats, const float* scs,
-                                              float f_mean, float f_rstd) {
+                                              float f_mean, float f_rstd, int c_begin = 0, int c_count = BN,
+                                              const float4* red = nullptr) {
   const int row = m0 + quarter * 32 + lane;
   const bool row_ok = row < p.M;
   const uint32_t lane_addr = tmem_acc + ((uint32_t)(quarter * 32) << 16);
@@ -243,20 +238,23 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     }
     return;
   }
+  constexpr int kStatW = StatW<BN>::value;
   const bool has_res = p.res != nullptr && row_ok;
-  const __nv_bfloat16* res_row = has_res ? p.res + (long long)row * p.ldr + n0 : nullptr;
+  const __nv_bfloat16* res_row = has_res ? p.res + (long long)row * p.ldr + n0 + c_begin : nullptr;
   uint32_t rn[16];
   float st_sum = 0.f, st_sq = 0.f;            // LayerNorm partials of the stored (bf16) row
-  float sh_k = 0.f, sh_s1 = 0.f, sh_s2 = 0.f;   // stats_out: sums shifted by the row's first value
+  float sh_k = 0.f, sh_s1 = 0.f, sh_s2 = 0.f;   // stats_out: sums shifted by the segment's first value
   if (has_res) ld_row64(res_row, rn, p.vec256);
+  const int nch = c_count / 32;
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int cc = 0; cc < nch; ++cc) {
+    const int c = c_begin / 32 + cc;             // chunk index within the tile
     uint32_t r[32];
     tmem_ld_32x32b_x32(lane_addr + c * 32, r);
     uint32_t rc[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) rc[q] = rn[q];
-    if (has_res && c + 1 < BN / 32) ld_row64(res_row + (c + 1) * 32, rn, p.vec256);   // next chunk in flight
+    if (has_res && cc + 1 < nch) ld_row64(res_row + (cc + 1) * 32, rn, p.vec256);   // next chunk in flight
     tmem_ld_wait();
     if (!row_ok) continue;
     const int col = n0 + c * 32;
@@ -264,6 +262,15 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     uint64_t v2[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) v2[q] = pack2u(r[2 * q], r[2 * q + 1]);
+    if (red) {                                   // split-K: add the other K half's partial
+      const float4* rr = red + (size_t)(cc * 8) * 128 + quarter * 32 + lane;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = rr[q * 128];
+        v2[2 * q] = fadd2(v2[2 * q], pack2(f.x, f.y));
+        v2[2 * q + 1] = fadd2(v2[2 * q + 1], pack2(f.z, f.w));
+      }
+    }
     if (p.alpha != 1.0f) {
       const uint64_t alpha2 = pack2(p.alpha, p.alpha);
 #pragma unroll
@@ -317,13 +324,21 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     if (p.probe_noepi != 2) st_row64(p.d + (long long)row * p.ldd + col, w, p.vec256);
     else if (w[0] == 0x7fc07fc0u) p.d[row] = __float2bfloat16(0.f);          // keep the math live
     if constexpr (EPI == kEpiStats) {
-      if (c == 0) sh_k = unpack_bf16(w[0]).x;
+      if ((c * 32) % kStatW == 0) sh_k = unpack_bf16(w[0]).x;
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const float2 f = unpack_bf16(w[e]);
         const float d0 = f.x - sh_k, d1 = f.y - sh_k;
         sh_s1 += d0 + d1;
         sh_s2 = fmaf(d0, d0, fmaf(d1, d1, sh_s2));
+      }
+      if ((c * 32 + 32) % kStatW == 0) {          // segment complete: (mean, M2) of its kStatW values
+        const float inv_n = 1.0f / (float)kStatW;
+        const int nseg = p.N / kStatW;
+        p.stats_out[(long long)row * nseg + (n0 + c * 32) / kStatW] =
+            make_float2(fmaf(sh_s1, inv_n, sh_k), fmaxf(sh_s2 - sh_s1 * sh_s1 * inv_n, 0.f));
+        sh_s1 = 0.f;
+        sh_s2 = 0.f;
       }
     }
     if (row_stats) {
@@ -339,11 +354,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     row_stats[0] = st_sum;
     row_stats[1] = st_sq;
   }
-  if (EPI == kEpiStats && row_ok) {
-    const float inv_n = 1.0f / (float)BN;
-    p.stats_out[(long long)row * p.num_n_tiles + n0 / BN] =
-        make_float2(fmaf(sh_s1, inv_n, sh_k), fmaxf(sh_s2 - sh_s1 * sh_s1 * inv_n, 0.f));
-  }
+
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -784,6 +795,187 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
+// Split-K over two CTA pairs (cluster of 4): small-M GEMMs whose 256 x 320 tiles
+// number at most SMs/4 (SDXL level 2: M=2048, N=1280 -> 32 tiles). Pair kh = rank/2
+// runs K blocks [kh*kb/2, (kh+1)*kb/2) of the SAME tile at the efficient 320 width;
+// then each CTA ships the half of its accumulator it does not finalise (128 x 160
+// fp32) into its K-partner's (rank ^ 2) now idle smem ring through distributed
+// shared memory, and finalises its own half: acc + partner partial -> epilogue.
+template <int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  constexpr int BN = 320, kSubN = 160;
+  constexpr uint32_t kSubBytes = (kSubN / 2) * BK * 2;
+  constexpr uint32_t kBHalfBytes = 2 * kSubBytes;
+  constexpr uint32_t kStageBytes = kABytes + kBHalfBytes;
+  constexpr uint32_t kTmemCols = 512;
+  constexpr uint32_t kIdesc = idesc_bf16_f32(2 * BM, kSubN);
+  static_assert((size_t)STAGES * kABytes >= (size_t)kSubN * BM * 4, "partial must fit the A ring");
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + STAGES * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* sbias = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);   // [BN]
+  float* scolsum = sbias + BN;                                                   // [BN]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t pr = rank & 1, kh = rank >> 1;          // CTA within pair, K half
+  const bool leader = pr == 0;
+  const uint16_t pair_mask = (uint16_t)(0x3u << (rank & 2));
+  const int tile = blockIdx.x >> 2;
+  const int m0 = (tile % p.num_m_tiles) * (2 * BM) + (int)pr * BM;
+  const int n0 = (tile / p.num_m_tiles) * BN;
+  const int kb_half = p.num_kb / 2;
+  const int kb_lo = kh ? kb_half : 0, kb_hi = kh ? p.num_kb : kb_half;
+  const int h0 = (int)kh * kSubN;                        // the 160 columns this CTA finalises
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_barrier();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  float f_mean = 0.f, f_rstd = 1.f;
+  if (warp == 0) {
+    if (lane == 0) {
+      int img = 0, y0 = 0, x0 = 0;
+      if (p.mode != HP_A_PLAIN) {
+        const int hw = p.out_h * p.out_w;
+        img = m0 / hw;
+        const int rem = m0 - img * hw;
+        y0 = rem / p.out_w;
+        x0 = rem - y0 * p.out_w;
+      }
+      const uint32_t nb = n0 + pr * (kSubN / 2);
+      uint32_t it = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+        const uint32_t fb = mapa_shared(&full[s], rank & ~1u);
+        uint8_t* a_dst = smA + s * kABytes;
+        if (p.mode == HP_A_PLAIN) {
+          tma_load_2d_pair(a_dst, &tmA, fb, kb * BK, m0);
+        } else {
+          const int tap = kb / p.cin_blocks;
+          const int cb = kb - tap * p.cin_blocks;
+          const int dy = tap / 3, dx = tap - dy * 3;
+          if (p.mode == HP_A_CONV3X3) tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, x0 + dx - 1, y0 + dy - 1, img);
+          else tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, 2 * x0 + dx - 1, 2 * y0 + dy - 1, img);
+        }
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub)
+          tma_load_2d_pair(smB + s * kBHalfBytes + sub * kSubBytes, &tmB, fb, kb * BK, nb + sub * kSubN);
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      uint32_t it = 0;
+      for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        tc_fence_after();
+        const uint64_t da = sdesc_sw128_kmajor(smA + s * kABytes);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            const uint64_t db = sdesc_sw128_kmajor(smB + s * kBHalfBytes + sub * kSubBytes);
+            umma_bf16_pair(tmem_base + sub * kSubN, da + 2 * k, db + 2 * k, kIdesc, (it | k) ? 1u : 0u);
+          }
+        }
+        umma_commit_pair(&empty[s], pair_mask);
+      }
+      umma_commit_pair(tfull, pair_mask);
+    }
+  } else if (warp >= 4) {
+    const int et = threadIdx.x - 128;
+    const int quarter = warp & 3;
+    const bool any_bias = p.bias != nullptr || p.bias2 != nullptr;
+    const bool fold = p.ln_stats != nullptr;
+    const long long img = (long long)(m0 / p.bias2_div);
+    for (int i = et; i < BN; i += 128) {
+      if (any_bias) {
+        float b = p.bias ? __ldg(p.bias + n0 + i) : 0.0f;
+        if (p.bias2) b += __ldg(p.bias2 + img * p.bias2_ld + n0 + i);
+        sbias[i] = b;
+      }
+      if (fold) scolsum[i] = __ldg(p.ln_colsum + n0 + i);
+    }
+    const int my_row = m0 + quarter * 32 + lane;
+    if (fold && my_row < p.M) fold_row_stats(p, my_row, f_mean, f_rstd);
+    prefetch_res_row<BN>(p, 0, my_row, n0);
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster_barrier();                   // #1: every MMA of both pairs done, both rings idle
+  tc_fence_after();
+  if (warp >= 4) {
+    // ship the half this CTA does not finalise into the K-partner's A ring: [col/4][row][4]
+    const int quarter = warp & 3;
+    const int rloc = quarter * 32 + lane;
+    const uint32_t lane_addr = tmem_base + ((uint32_t)(quarter * 32) << 16);
+    const int oh0 = (int)(kh ^ 1) * kSubN;
+    const uint32_t dst = mapa_shared(smA, rank ^ 2u);
+#pragma unroll 1
+    for (int c = 0; c < kSubN / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(lane_addr + oh0 + c * 32, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t a = dst + (uint32_t)(((c * 8 + q) * 128 + rloc) * 16);
+        asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};"
+                     :: "r"(a), "f"(__uint_as_float(r[4 * q])), "f"(__uint_as_float(r[4 * q + 1])),
+                        "f"(__uint_as_float(r[4 * q + 2])), "f"(__uint_as_float(r[4 * q + 3])) : "memory");
+      }
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster_barrier();                   // #2: partials delivered
+  tc_fence_after();
+  if (warp >= 4) {
+    const int quarter = warp & 3;
+    const float* sb = (p.bias != nullptr || p.bias2 != nullptr) ? sbias : nullptr;
+    const float4* red = reinterpret_cast<const float4*>(smA);
+    if (p.ln_stats) {
+      epilogue_tile<BN, kEpiFold>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, scolsum, f_mean, f_rstd, h0,
+                                  kSubN, red);
+    } else if (p.stats_out) {
+      epilogue_tile<BN, kEpiStats>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f, h0, kSubN,
+                                   red);
+    } else {
+      epilogue_tile<BN, kEpiPlain>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f, h0, kSubN,
+                                   red);
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  cluster_barrier();                   // #3: nobody frees TMEM while its pair partner still reads
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------------------
 // host side: tensor maps (driver entry point, no -lcuda link dependency)
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -896,6 +1088,45 @@ int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPar
   return HP_OK;
 }
 
+template <int STAGES>
+int launch_gemm_splitk(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
+  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + 160 * BK * 2) + 256 + 2 * 320 * sizeof(float);
+  static_assert(smem <= 227 * 1024, "split-K GEMM smem");
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_splitk_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return HP_ERR_CUDA;
+    attr_set = true;
+  }
+  const int tiles = p.num_m_tiles * p.num_n_tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(4 * tiles);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = hp_pdl_enabled() ? 2 : 1;
+  if (cudaLaunchKernelEx(&cfg, gemm_splitk_kernel<STAGES>, ta, tb, p) != cudaSuccess) return HP_ERR_CUDA;
+  return HP_OK;
+}
+
+bool splitk_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HP_GEMM_SPLITK");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 bool pair_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -905,11 +1136,20 @@ bool pair_enabled() {
   return on == 1;
 }
 
+// split-K over two CTA pairs for wide-N, small-M layers (SDXL level 2: N = 1280).
+// Depends on N and K only, never on M, so one image's rows are computed identically
+// whatever else is in the batch (batch invariance: split-K changes the summation).
+bool splitk_ok(int64_t M, int64_t N, int64_t K, int act, int batch, int mode) {
+  if (!splitk_enabled() || !pair_enabled() || act == HP_ACT_GEGLU || batch > 1 || M <= BM) return false;
+  // the exchange + half epilogue costs ~4 us: worth it from K = 4096 on (ff2, 3x3 convs)
+  return N % 320 == 0 && N >= 1280 && K / BK >= 64;
+}
+
 // block_n for an M x N x K problem: whole-wave tile counts on the SMs (CTA pairs for
 // M > 128) times the per-tile time, k-blocks x N / (measured main-loop rate of that
 // width), plus exposed epilogues (~5 k-blocks' worth each). 320 keeps one accumulator
 // (no epilogue/MMA overlap), so each of its tiles exposes one.
-int pick_bn(int64_t M, int64_t N, int64_t K, int act) {
+int pick_bn(int64_t M, int64_t N, int64_t K, int act, int batch = 1, int mode = HP_A_PLAIN) {
   const int cands[5] = {320, 256, 160, 128, 64};
   int best = 0;
   double best_cost = 1e30;
@@ -920,6 +1160,7 @@ int pick_bn(int64_t M, int64_t N, int64_t K, int act) {
   // measured main-loop rate per SM relative to block_n 256 (pair kernel, B200): every MMA
   // re-reads its 128-row A slab from shared memory, so wide N tiles amortise it best
   auto rate = [](int bn) { return bn >= 256 ? 1.0 : bn >= 160 ? 0.72 : bn >= 128 ? 0.6 : 0.35; };
+  if (pair && splitk_ok(M, N, K, act, batch, mode)) return 320;   // fixed choice (see splitk_ok)
   for (int bn : cands) {
     if (N % bn) continue;
     if (bn > 256 && (!pair || act == HP_ACT_GEGLU)) continue;    // 320 = two N=160 MMAs, pair kernel only
@@ -940,13 +1181,21 @@ extern "C" {
 
 int32_t hp_gemm_pick_block_n(int64_t M, int64_t N, int64_t K, int32_t act) { return pick_bn(M, N, K, act); }
 
+int32_t hp_gemm_stats_block_n(int64_t M, int64_t N, int64_t K) {
+  num_sms();
+  const int bn = pick_bn(M, N, K, HP_ACT_NONE);
+  if (bn == 320 || N % 160) return bn;        // 320 (split or not) writes 160-wide segments
+  return 160;
+}
+
 int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if (!d || !d->a || !d->b || !d->d) return HP_ERR_PARAMETER;
   if (d->M <= 0 || d->N <= 0 || d->K <= 0) return HP_ERR_SHAPE;
   if ((d->K % 8) || (d->ldb % 8)) return HP_ERR_UNSUPPORTED;   // 16-byte TMA strides
   if ((reinterpret_cast<uintptr_t>(d->a) | reinterpret_cast<uintptr_t>(d->b)) & 15) return HP_ERR_UNSUPPORTED;
   num_sms();
-  const int bn = d->block_n ? d->block_n : pick_bn(d->M * (d->batch > 1 ? d->batch : 1), d->N, d->K, d->act);
+  const int bn = d->block_n ? d->block_n
+                            : pick_bn(d->M * (d->batch > 1 ? d->batch : 1), d->N, d->K, d->act, d->batch, d->a_mode);
   if (bn == 0 || d->N % bn) return HP_ERR_UNSUPPORTED;
   if (d->act == HP_ACT_GEGLU && (bn % 64)) return HP_ERR_UNSUPPORTED;
   const int64_t n_out = d->act == HP_ACT_GEGLU ? d->N / 2 : d->N;
@@ -1045,6 +1294,10 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
     if (!make_map(&tb, d->b, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (pair && bn == 320 && splitk_ok(d->M, d->N, d->K, d->act, p.batch, d->a_mode)) {
+    p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
+    return launch_gemm_splitk<5>(ta, tb, p, st);
+  }
   if (pair) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
     switch (bn) {

@@ -67,6 +67,7 @@ class HpAttnDesc(C.Structure):
 SIGNATURES = {
     "hp_gemm": (C.c_int, [C.POINTER(HpGemmDesc), _VP]),
     "hp_gemm_pick_block_n": (_I32, [_I64, _I64, _I64, _I32]),
+    "hp_gemm_stats_block_n": (_I32, [_I64, _I64, _I64]),
     "hp_attention": (C.c_int, [C.POINTER(HpAttnDesc), _VP]),
     "hp_group_norm": (C.c_int, [_VP, _I32, _VP, _I32, _I32, _I64, _I32, _F32, _VP, _VP, _I32, _VP, _VP, _VP]),
     "hp_layer_norm": (C.c_int, [_VP, _I64, _I32, _F32, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
@@ -193,12 +194,14 @@ def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, a
         g, b_, eps, y = ln
         d.ln_gamma, d.ln_beta, d.ln_eps, d.ln_y, d.ldy = _p(g), _p(b_), float(eps), _p(y), y.stride(-2)
     if stats_out is not None:
-        bn = int(block_n) or int(lib.hp_gemm_pick_block_n(M, Nn, K, int(act)))
-        if bn == 0 or Nn % bn or stats_out.buf.numel() < 2 * M * (Nn // bn):
+        # the statistics layout must not depend on M (batch invariance of the folded LayerNorm)
+        bn = int(block_n) or int(lib.hp_gemm_stats_block_n(M, Nn, K))
+        seg = bn // 2 if bn > 256 else bn            # statistics segment width (hp_gemm.cu StatW)
+        if bn == 0 or Nn % bn or stats_out.buf.numel() < 2 * M * (Nn // seg):
             raise ShapeError(f"row stats: N={Nn} block_n={bn} capacity {stats_out.buf.numel()}")
         d.block_n = bn
         d.stats_out = _p(stats_out.buf)
-        stats_out.parts, stats_out.part_n = Nn // bn, bn
+        stats_out.parts, stats_out.part_n = Nn // seg, seg
     if ln_fold is not None:
         st, fold = ln_fold
         d.ln_stats, d.ln_parts, d.ln_part_n = _p(st.buf), st.parts, st.part_n

@@ -76,7 +76,7 @@ def test_gemm_geglu(bn):
                                                (2, 64, 64, 128, 256, 1), (1, 256, 256, 64, 64, 1),
                                                (2, 64, 64, 64, 64, 2), (2, 128, 128, 64, 128, 2),
                                                (1, 16, 16, 192, 320, 1), (2, 64, 64, 128, 640, 1),
-                                               (2, 128, 128, 64, 320, 1)])
+                                               (2, 128, 128, 64, 320, 1), (2, 32, 32, 1280, 1280, 1)])
 def test_conv3x3_implicit_gemm(n, h, w, c, co, stride):
     torch.manual_seed(h + c)
     x = rnd(n, h, w, c)
@@ -246,3 +246,24 @@ def test_gemm_layernorm_fold(M, C, Nc, act):
     else:
         ref = pre
     close(out, ref, tol=2e-2)
+
+
+@pytest.mark.parametrize("N,Kd,stats", [(1280, 1280, False), (1280, 5120, True), (640, 640, True)])
+def test_gemm_rows_batch_invariant(N, Kd, stats):
+    """An image's rows come out bit-identical whatever else is in the batch: tile width,
+    split-K and the statistics layout depend on N and K only (serial CFG-batched and
+    condition-partitioned runs then produce the same latents)."""
+    torch.manual_seed(N + Kd)
+    a, w = rnd(2048, Kd), rnd(N, Kd, s=Kd ** -0.5)
+    res = rnd(2048, N)
+    kw = {}
+    outs = []
+    for rows in (2048, 1024):
+        rs = K.RowStats(2 * rows * N // 64, "cuda") if stats else None
+        out = K.gemm(a[:rows], w, residual=res[:rows], stats_out=rs)
+        outs.append((out, rs))
+    (o2, r2), (o1, r1) = outs
+    assert torch.equal(o2[:1024], o1)
+    if stats:
+        assert r2.parts == r1.parts and r2.part_n == r1.part_n
+        assert torch.equal(r2.buf[:2 * 1024 * r1.parts], r1.buf[:2 * 1024 * r1.parts])
