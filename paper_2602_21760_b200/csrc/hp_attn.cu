@@ -15,6 +15,16 @@
 // exp2 split between MUFU.EX2 and a degree-4 polynomial on the FMA pipe (P is
 // rounded to bf16 anyway). P goes to shared memory as the SW128 K-major A
 // operand of the PV MMA; V is consumed MN-major straight from its TMA tile.
+//
+// Launch variants (hp_attention picks one):
+//   S_kv <= 128        single-block kernel, 2 CTAs/SM (cross-attention)
+//   short last wave    split-KV kernel: one query tile per CTA, its key range cut
+//                      in two halves processed by the two warpgroups and merged
+//                      (fixed split point: batch-invariant)
+//   otherwise          the two-tile kernel above
+// (Measured and dropped: P kept in TMEM as the A operand of a TS-MMA with the
+// whole S row in 200 registers: 180 us vs 169 us at S=4096; 64-key blocks with
+// double-buffered S: slower; 2 threads per score row: slower.)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -373,6 +383,242 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
   if (warp == kMmaWarp) tmem_dealloc<kCols>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// Split-KV CTA: ONE query tile, its key range cut in two halves that the two
+// softmax warpgroups ("streams") process concurrently against their own K/V rings,
+// S / P buffers and O accumulators; the halves are merged in the CTA at the end
+// (m = max(m0, m1), O = sum_h 2^(m_h - m) O_h, l likewise). Units are query tiles,
+// twice as many as two-tile CTAs, so the last partial wave on 148 SMs is half as
+// long. The split point depends on S_kv only: an image's rows are computed
+// identically whatever else is in the batch.
+constexpr int kStSplit = 2;
+
+__global__ void __launch_bounds__(kThreads, 1)
+attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, AttnParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                                        // 1 tile
+  uint8_t* sK = sQ + kTileBytes;                             // [stream][stage]
+  uint8_t* sV = sK + 2 * kStSplit * kTileBytes;              // [stream][stage]
+  uint8_t* sP = sV + 2 * kStSplit * kTileBytes;              // [stream]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = q_full + 1;                            // [stream][stage]
+  uint64_t* kv_empty = kv_full + 2 * kStSplit;
+  uint64_t* s_full = kv_empty + 2 * kStSplit;                // [stream]
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  float* s_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // [stream][2][128]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int q0 = blockIdx.x * kBQ;
+  const int J = p.n_kv;
+  const int jh = (J + 1) / 2;
+  const int jb[2] = {0, jh}, nj[2] = {jh, J - jh};
+
+  if (warp == 8 && lane == 0) {
+    prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2 * kStSplit; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1); }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  auto k_at = [&](int q, int s) { return sK + (q * kStSplit + s) * kTileBytes; };
+  auto v_at = [&](int q, int s) { return sV + (q * kStSplit + s) * kTileBytes; };
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, kTileBytes);
+      tma_load_3d(sQ, &tmQ, q_full, p.q_col0 + h * kD, q0, b);
+      for (int i = 0; i < jh; ++i) {
+        for (int q = 0; q < 2; ++q) {
+          if (i >= nj[q]) continue;
+          const int s = i % kStSplit, bi = q * kStSplit + s, g = jb[q] + i;
+          mbar_wait(&kv_empty[bi], ((i / kStSplit) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[bi], 2 * kTileBytes);
+          tma_load_3d(k_at(q, s), &tmK, &kv_full[bi], p.k_col0 + h * kD, g * kBK, b);
+          tma_load_3d(v_at(q, s), &tmV, &kv_full[bi], p.v_col0 + h * kD, g * kBK, b);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      mbar_wait(q_full, 0);
+      const uint64_t dq = sdesc_sw128_kmajor(sQ);
+      auto issue_s = [&](int q, int i) {
+        const uint64_t dk = sdesc_sw128_kmajor(k_at(q, i % kStSplit));
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem + q * kBK, dq + 2 * k, dk + 2 * k, kIdescS, k > 0 ? 1u : 0u);
+        umma_commit(&s_full[q]);
+      };
+      auto issue_pv = [&](int q, int i) {
+        const uint8_t* v = v_at(q, i % kStSplit);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          const uint64_t da = sdesc_sw128_kmajor(sP + q * kPBytes + (k >> 2) * (kBQ * 128)) + 2 * (k & 3);
+          const uint64_t dv = sdesc_sw128_mnmajor(v + k * 2048, 8192);
+          umma_bf16(tmem + 256 + q * kD, da, dv, kIdescO, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&o_done[q]);
+        umma_commit(&kv_empty[q * kStSplit + i % kStSplit]);
+      };
+      for (int i = 0; i < jh; ++i) {
+        for (int q = 0; q < 2; ++q) {
+          if (i >= nj[q]) continue;
+          const int bi = q * kStSplit + i % kStSplit;
+          mbar_wait(&kv_full[bi], (i / kStSplit) & 1);
+          tc_fence_after();
+          if (i > 0) {                       // S_q(i) overwrites S_q(i-1): P_q(i-1) is out
+            mbar_wait(&p_full[q], (i - 1) & 1);
+            tc_fence_after();
+          }
+          issue_s(q, i);
+          if (i > 0) issue_pv(q, i - 1);
+        }
+      }
+      for (int q = 0; q < 2; ++q) {
+        mbar_wait(&p_full[q], (nj[q] - 1) & 1);
+        tc_fence_after();
+        issue_pv(q, nj[q] - 1);
+      }
+    }
+  } else {
+    // ------------------------------ softmax: stream q over key blocks jb[q] .. ------------------------------
+    const int q = warp >> 2;
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t t_s = tmem + lane_base + q * kBK;
+    const uint32_t t_o = tmem + lane_base + 256 + q * kD;
+    uint8_t* pbase = sP + q * kPBytes;
+    float m_run = -INFINITY, l_run = 0.f;
+    const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
+    const int n = nj[q];
+    for (int i = 0; i < n; ++i) {
+      mbar_wait(&s_full[q], i & 1);
+      tc_fence_after();
+      const int valid = min(kBK, p.skv - (jb[q] + i) * kBK);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kBK / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_s + c * 32, r);
+        tmem_ld_wait();
+        if (valid < kBK) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c * 32 + e >= valid) r[e] = __float_as_uint(-INFINITY);
+        }
+#pragma unroll
+        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(r[e]));
+      }
+      const float m_blk = mx * p.scale_log2;
+      const bool grow = (i == 0) || (m_blk > m_run + kRescaleThreshold);
+      if (i > 0) {
+        mbar_wait(&o_done[q], (i - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, grow)) {
+          const float alpha = grow ? ex2f(m_run - fmaxf(m_run, m_blk)) : 1.0f;
+          uint32_t o[32];
+#pragma unroll
+          for (int c = 0; c < kD / 32; ++c) {
+            tmem_ld_32x32b_x32(t_o + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st_32x32b_x32(t_o + c * 32, o);
+          }
+          tmem_st_wait();
+          if (grow) l_run *= alpha;
+        }
+      }
+      if (grow) m_run = fmaxf(m_run, m_blk);
+      const uint64_t negm2 = pack2(-m_run, -m_run);
+      uint64_t sum2 = 0ull;
+#pragma unroll
+      for (int c = 0; c < kBK / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_s + c * 32, r);
+        tmem_ld_wait();
+        if (valid < kBK) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c * 32 + e >= valid) r[e] = __float_as_uint(-INFINITY);
+        }
+        uint32_t packed[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const uint64_t x2 = ffma2(pack2u(r[e], r[e + 1]), scale2, negm2);
+          uint64_t e2;
+          const int pr = (e >> 1) & 7;
+          if (pr == 2 || pr == 5 || pr == 7) e2 = exp2_poly2(x2);
+          else e2 = pack2(ex2f(lo2(x2)), ex2f(hi2(x2)));
+          sum2 = fadd2(sum2, e2);
+          packed[e / 2] = pack_bf16(lo2(e2), hi2(e2));
+        }
+        uint8_t* atom = pbase + (c >> 1) * (kBQ * 128) + row * 128;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          const int chunk = ((c & 1) * 4 + qq) ^ (row & 7);
+          *reinterpret_cast<uint4*>(atom + chunk * 16) =
+              make_uint4(packed[4 * qq], packed[4 * qq + 1], packed[4 * qq + 2], packed[4 * qq + 3]);
+        }
+      }
+      l_run += lo2(sum2) + hi2(sum2);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[q]);
+    }
+    mbar_wait(&o_done[q], (n - 1) & 1);
+    tc_fence_after();
+    // merge the two halves: both warpgroups reach every O column of their rows
+    s_ml[(q * 2 + 0) * kBQ + row] = m_run;
+    s_ml[(q * 2 + 1) * kBQ + row] = l_run;
+    tc_fence_before();
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    tc_fence_after();
+    const float m0 = s_ml[0 * kBQ + row], l0 = s_ml[1 * kBQ + row];
+    const float m1 = s_ml[2 * kBQ + row], l1 = s_ml[3 * kBQ + row];
+    const float m = fmaxf(m0, m1);
+    const float a0 = ex2f(m0 - m), a1 = ex2f(m1 - m);
+    const float inv = 1.0f / (a0 * l0 + a1 * l1);
+    const float w0 = a0 * inv, w1 = a1 * inv;
+    const int qrow = q0 + row;
+    // warpgroup q writes output columns [32q, 32q + 32)
+    uint32_t o0[32], o1[32];
+    tmem_ld_32x32b_x32(tmem + lane_base + 256 + q * 32, o0);
+    tmem_ld_32x32b_x32(tmem + lane_base + 256 + kD + q * 32, o1);
+    tmem_ld_wait();
+    if (qrow < p.sq) {
+      __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + q * 32;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          v[e] = fmaf(__uint_as_float(o0[8 * qq + e]), w0, __uint_as_float(o1[8 * qq + e]) * w1);
+        reinterpret_cast<uint4*>(dst)[qq] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                                                       pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 9) tmem_dealloc<kTmemCols>(tmem);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -428,6 +674,15 @@ int num_sms_attn() {
   return n;
 }
 
+bool splitkv_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HP_ATTN_SPLITKV");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 bool solo_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -463,6 +718,19 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   const int pair_ctas = grid.x * grid.y * grid.z;
   const int sms = num_sms_attn();
   const int tail = pair_ctas % sms;
+  if (splitkv_enabled() && tail != 0 && tail * 2 < sms) {
+    constexpr size_t smem = 1024 + (size_t)kTileBytes * (1 + 4 * kStSplit) + 2 * kPBytes + 256 + 4 * kBQ * 4;
+    static bool attr_s = false;
+    if (!attr_s) {
+      if (cudaFuncSetAttribute(attn_splitkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+        return HP_ERR_CUDA;
+      attr_s = true;
+    }
+    dim3 g1((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
+    return hp_launch_pdl(attn_splitkv_kernel, g1, dim3(kThreads), smem, st, tq, tk, tv, p) == cudaSuccess
+               ? HP_OK : HP_ERR_CUDA;
+  }
   if (solo_enabled() && tail != 0 && tail * 2 < sms) {
     dim3 g1((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
     return launch_attn<kModeSolo>(g1, st, tq, tk, tv, p, 0);
