@@ -122,6 +122,11 @@ int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, voi
 /* channel concat NHWC: y[..., 0:c1] = a, y[..., c1:c1+c2] = b */
 int hp_concat_channels(const void* a, int32_t c1, const void* b, int32_t c2, int64_t pixels,
                        void* y, void* stream);
+/* per-row channel window copy, bf16: y[r, j] = j < c_src ? x[r, j] : 0 for j < c_dst
+ * (zero-pads conv_in's 4 latent channels to the 64 the implicit-GEMM conv needs,
+ * and slices conv_out's 4 channels out of its 64-wide padded GEMM output).     */
+int hp_copy_cols(const void* x, int64_t ldx, int32_t c_src, int64_t rows, void* y, int64_t ldy, int32_t c_dst,
+                 void* stream);
 /* direct 3x3 conv for tiny channel counts (conv_in / conv_out): NHWC bf16 in,
  * weights fp32 [cout, 3, 3, cin], bias fp32; out either bf16 NHWC or fp32  */
 int hp_conv3x3_small(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin,

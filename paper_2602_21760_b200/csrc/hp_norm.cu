@@ -472,19 +472,27 @@ __global__ void linear_small_kernel(const float* __restrict__ x, int M, int K, c
   for (int n = warp; n < N; n += nwarps) {
     float acc[kSmallMaxM] = {0};
     const bf16* wr = w + (int64_t)n * K;
-    for (int k = lane * 8; k < K; k += 256) {
-      float wv[8];
-      load8(wr + k, wv);
-      for (int m = 0; m < M; ++m) {
-        const float* xr = x + (int64_t)m * K + k;
-        float a = acc[m];
+    // four 16-byte weight loads in flight per lane (the GEMV is weight-bandwidth bound)
+    for (int k0 = lane * 8; k0 < K; k0 += 4 * 256) {
+      float wv[4][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float xv = xr[i];
-          if (act_in == HP_ACT_SILU) xv = silu(xv);
-          a = fmaf(xv, wv[i], a);
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u * 256 < K) load8(wr + k0 + u * 256, wv[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * 256;
+        if (k >= K) break;
+        for (int m = 0; m < M; ++m) {
+          const float* xr = x + (int64_t)m * K + k;
+          float a = acc[m];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float xv = xr[i];
+            if (act_in == HP_ACT_SILU) xv = silu(xv);
+            a = fmaf(xv, wv[u][i], a);
+          }
+          acc[m] = a;
         }
-        acc[m] = a;
       }
     }
     for (int m = 0; m < M; ++m) {
@@ -555,6 +563,18 @@ __global__ void gated_residual_kernel(bf16* __restrict__ x, const bf16* __restri
 #pragma unroll
     for (int k = 0; k < 8; ++k) a[k] += g[k] * v[k];
     store8(x + r * c + j * 8, a);
+  }
+}
+
+__global__ void copy_cols_kernel(const bf16* __restrict__ x, int64_t ldx, int c_src, int64_t rows,
+                                 bf16* __restrict__ y, int64_t ldy, int c_dst) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = rows * c_dst;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / c_dst;
+    const int j = (int)(i - r * c_dst);
+    y[r * ldy + j] = j < c_src ? x[r * ldx + j] : __float2bfloat16_rn(0.f);
   }
 }
 
@@ -634,6 +654,16 @@ int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, voi
   const int64_t total = (int64_t)n * 4 * h * w * (c / 8);
   hp_launch_pdl(upsample2x_kernel, dim3(nblocks(total, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(x), n, h, w, c, static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
+  return ok();
+}
+
+int hp_copy_cols(const void* x, int64_t ldx, int32_t c_src, int64_t rows, void* y, int64_t ldy, int32_t c_dst,
+                 void* stream) {
+  if (!x || !y || c_src < 0 || c_dst < 1 || rows < 0 || ldx < c_src || ldy < c_dst) return HP_ERR_PARAMETER;
+  const int64_t total = rows * c_dst;
+  hp_launch_pdl(copy_cols_kernel, dim3(nblocks(total, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                static_cast<const bf16*>(x), ldx, c_src, rows, static_cast<bf16*>(y), ldy, c_dst);
   if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }

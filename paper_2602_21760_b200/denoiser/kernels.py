@@ -75,6 +75,7 @@ SIGNATURES = {
     "hp_silu": (C.c_int, [_VP, _VP, _I64, _VP]),
     "hp_upsample2x": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP]),
     "hp_concat_channels": (C.c_int, [_VP, _I32, _VP, _I32, _I64, _VP, _VP]),
+    "hp_copy_cols": (C.c_int, [_VP, _I64, _I32, _I64, _VP, _I64, _I32, _VP]),
     "hp_conv3x3_small": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP, _I32, _VP, _I32, _VP]),
     "hp_timestep_embedding": (C.c_int, [_VP, _I32, _I32, _F32, _VP, _VP]),
     "hp_linear_small": (C.c_int, [_VP, _I32, _I32, _VP, _VP, _I32, _I32, _I32, _VP, _VP]),
@@ -276,6 +277,17 @@ def concat_channels(a, c1, b, c2, pixels):
     lib = N.load()
     out = torch.empty((pixels, c1 + c2), dtype=torch.bfloat16, device=a.device)
     check(lib.hp_concat_channels(_p(a), c1, _p(b), c2, pixels, _p(out), _s()), "hp_concat_channels")
+    return out
+
+
+def copy_cols(x, c_dst, *, c_src=None, out=None):
+    """Per-row channel window: zero-pad or slice the last dim of a 2-D bf16 view."""
+    lib = N.load()
+    rows, ldx = x.shape[0], x.stride(0)
+    c_src = x.shape[1] if c_src is None else c_src
+    if out is None:
+        out = torch.empty((rows, c_dst), dtype=torch.bfloat16, device=x.device)
+    check(lib.hp_copy_cols(_p(x), ldx, c_src, rows, _p(out), out.stride(0), c_dst, _s()), "hp_copy_cols")
     return out
 
 

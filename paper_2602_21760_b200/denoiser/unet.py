@@ -160,7 +160,13 @@ class UNet:
         dev = torch.device(device)
         self.dev = dev
         ch = s.block_out
-        self.conv_in_w = _f32(W["conv_in.weight"].to(dev).permute(0, 2, 3, 1))
+        # conv_in / conv_out on the tensor-core implicit-GEMM conv: the 4 latent
+        # channels are zero-padded to 64 (conv_in's input, conv_out's output)
+        wi = W["conv_in.weight"].to(dev)                                   # [320, 4, 3, 3]
+        self.cin_pad = 64
+        wpad = torch.zeros(wi.shape[0], 3, 3, self.cin_pad, device=dev)
+        wpad[..., :wi.shape[1]] = wi.permute(0, 2, 3, 1)
+        self.conv_in_w = _bf(wpad.reshape(wi.shape[0], 9 * self.cin_pad))
         self.conv_in_b = _f32(W["conv_in.bias"].to(dev))
         self.t1, self.t2 = _Lin(W, "time_embedding.linear_1", dev=dev), _Lin(W, "time_embedding.linear_2", dev=dev)
         self.a1, self.a2 = _Lin(W, "add_embedding.linear_1", dev=dev), _Lin(W, "add_embedding.linear_2", dev=dev)
@@ -184,8 +190,14 @@ class UNet:
             us = _Conv(W, f"up_blocks.{u}.upsamplers.0.conv", dev) if u < len(ch) - 1 else None
             self.up.append((res, att, us))
         self.norm_out = _Norm(W, "conv_norm_out", dev)
-        self.conv_out_w = _f32(W["conv_out.weight"].to(dev).permute(0, 2, 3, 1))
-        self.conv_out_b = _f32(W["conv_out.bias"].to(dev))
+        wo = W["conv_out.weight"].to(dev)                                  # [4, 320, 3, 3]
+        self.cout_pad = 64
+        wpad = torch.zeros(self.cout_pad, 3, 3, wo.shape[1], device=dev)
+        wpad[:wo.shape[0]] = wo.permute(0, 2, 3, 1)
+        self.conv_out_w = _bf(wpad.reshape(self.cout_pad, 9 * wo.shape[1]))
+        bpad = torch.zeros(self.cout_pad, device=dev)
+        bpad[:wo.shape[0]] = W["conv_out.bias"].to(dev)
+        self.conv_out_b = _f32(bpad)
         self.stats = torch.empty(2 * 64 * 64 * 32, dtype=torch.float32, device=dev)
         self.aug = {}
         self.ctx_len = s.context_len
@@ -248,7 +260,8 @@ class UNet:
         def tb(r):
             off, co = self.tproj_slot[id(r)]
             return tb_all[:, off:off + co]             # row stride sum(co): GEMM bias2_ld
-        h = K.conv3x3_small(x, n, H, Wd, s.in_channels, self.conv_in_w, self.conv_in_b, s.block_out[0])
+        xp = K.copy_cols(x.view(n * H * Wd, s.in_channels), self.cin_pad)
+        h = K.gemm(xp, self.conv_in_w, bias=self.conv_in_b, conv=(n, H, Wd, self.cin_pad, 1))
         skips = [h]
         hh, ww = H, Wd
         for res, att, ds in self.down:
@@ -277,7 +290,8 @@ class UNet:
                 hh, ww = hh * 2, ww * 2
                 h = us(h, n, hh, ww)
         y = K.group_norm(h, n, hh * ww, s.block_out[0], self.norm_out.g, self.norm_out.b, groups=g, silu=True, stats=st)
-        eps = K.conv3x3_small(y, n, hh, ww, s.block_out[0], self.conv_out_w, self.conv_out_b, s.out_channels)
+        e64 = K.gemm(y, self.conv_out_w, bias=self.conv_out_b, conv=(n, hh, ww, s.block_out[0], 1))
+        eps = K.copy_cols(e64, s.out_channels)
         return eps.view(n, hh, ww, s.out_channels)
 
 
