@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <math.h>
 #include "hybridpar_b200_denoiser.h"
 #include "hp_common.cuh"
@@ -60,17 +61,14 @@ inline bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) ==
 constexpr int kGnThreads = 256;
 constexpr int kMaxC = 2560;
 
-__global__ void __launch_bounds__(kGnThreads)
-gn_stats_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
-                int groups, int splits, float* __restrict__ part) {
-  pdl_wait();
-  pdl_trigger();
-  // fixed-order reduction (no float atomics): deterministic, batch-invariant
-  __shared__ float s_sum[kMaxC], s_sq[kMaxC];
-  __shared__ float p_sum[kGnThreads * 8], p_sq[kGnThreads * 8];
+// GroupNorm partial sums of one (image n, pixel split) block: fixed-order
+// reduction (no float atomics): deterministic, batch-invariant
+__device__ __forceinline__ void gn_stats_block(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2,
+                                               int c2, int64_t hw, int groups, int splits,
+                                               float* __restrict__ part, int n, int split, float* s_sum,
+                                               float* s_sq, float* p_sum, float* p_sq) {
   const int C = c1 + c2;
   const int V = C / 8;
-  const int n = blockIdx.y, split = blockIdx.x;
   const int64_t p_begin = hw * split / splits, p_end = hw * (split + 1) / splits;
   for (int j0 = 0; j0 < V; j0 += kGnThreads) {
     const int vecs = min(V - j0, kGnThreads);
@@ -128,21 +126,27 @@ gn_stats_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
   }
 }
 
-// GroupNorm pass 2: grid (chunks, n); stats folded per block in fixed order.
 __global__ void __launch_bounds__(kGnThreads)
-gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
-                int groups, int splits, const float* __restrict__ part, float eps,
-                const float* __restrict__ gamma, const float* __restrict__ beta, int do_silu,
-                bf16* __restrict__ y) {
+gn_stats_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
+                int groups, int splits, float* __restrict__ part) {
   pdl_wait();
   pdl_trigger();
-  // per-channel affine folded once per block: y = x * sa[c] + sb[c]
-  __shared__ float s_mean[64], s_rstd[64];
-  __shared__ double s_pa[kGnThreads], s_pb[kGnThreads];
-  __shared__ __align__(16) float sa[kMaxC], sb[kMaxC];
+  __shared__ float s_sum[kMaxC], s_sq[kMaxC];
+  __shared__ float p_sum[kGnThreads * 8], p_sq[kGnThreads * 8];
+  gn_stats_block(x1, c1, x2, c2, hw, groups, splits, part, blockIdx.y, blockIdx.x, s_sum, s_sq, p_sum, p_sq);
+}
+
+// GroupNorm pass 2 for image n: fold the per-split partials (fixed order), then
+// y = x * sa[c] + sb[c] (+ SiLU) over pixels p_first + r, stepping p_mul * rows
+__device__ __forceinline__ void gn_apply_block(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2,
+                                               int c2, int64_t hw, int groups, int splits,
+                                               const float* __restrict__ part, float eps,
+                                               const float* __restrict__ gamma, const float* __restrict__ beta,
+                                               int do_silu, bf16* __restrict__ y, int n, int64_t p_first,
+                                               int64_t p_mul, int64_t p_end, float* s_mean, float* s_rstd,
+                                               double* s_pa, double* s_pb, float* sa, float* sb) {
   const int C = c1 + c2;
   const int V = C / 8;
-  const int n = blockIdx.y;
   const int cg = C / groups;
   {
     // fold the per-split partials: kGnThreads/groups threads per group, fixed order
@@ -194,9 +198,9 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
     const bool first = ch < c1;
     const bf16* src = first ? xa + ch : xb + (ch - c1);
     const int64_t sstride = first ? c1 : c2;
-    const int64_t step = (int64_t)gridDim.x * rows;
-    int64_t p = (int64_t)blockIdx.x * rows + r;
-    for (; p + 3 * step < hw; p += 4 * step) {         // four loads in flight
+    const int64_t step = p_mul * rows;
+    int64_t p = p_first + r;
+    for (; p + 3 * step < p_end; p += 4 * step) {         // four loads in flight
       uint4 u[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(src + (p + k * step) * sstride);
@@ -217,7 +221,7 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
         store8(yo + (p + k * step) * C + ch, v);
       }
     }
-    for (; p < hw; p += step) {
+    for (; p < p_end; p += step) {
       float v[8];
       load8(src + p * sstride, v);
 #pragma unroll
@@ -228,6 +232,58 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
       store8(yo + p * C + ch, v);
     }
   }
+}
+
+__global__ void __launch_bounds__(kGnThreads)
+gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
+                int groups, int splits, const float* __restrict__ part, float eps,
+                const float* __restrict__ gamma, const float* __restrict__ beta, int do_silu,
+                bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float s_mean[64], s_rstd[64];
+  __shared__ double s_pa[kGnThreads], s_pb[kGnThreads];
+  __shared__ __align__(16) float sa[kMaxC], sb[kMaxC];
+  gn_apply_block(x1, c1, x2, c2, hw, groups, splits, part, eps, gamma, beta, do_silu, y, blockIdx.y,
+                 (int64_t)blockIdx.x * (kGnThreads / min((c1 + c2) / 8, kGnThreads)), gridDim.x, hw, s_mean, s_rstd,
+                 s_pa, s_pb, sa, sb);
+}
+
+// Single-launch GroupNorm: the statistics CTAs of an image meet at a
+// sense-reversing barrier (every CTA of the grid is resident: the launcher checks
+// occupancy), fold the partials and normalise the pixels they just reduced (an
+// L2 hit). Same partition and fold as the two-kernel path: bit-identical output.
+__device__ __forceinline__ void image_barrier(unsigned* cnt, unsigned* gen, unsigned expected) {
+  const unsigned g = *reinterpret_cast<volatile unsigned*>(gen);
+  __threadfence();
+  if (atomicAdd(cnt, 1u) == expected - 1) {
+    atomicExch(cnt, 0u);
+    __threadfence();
+    atomicAdd(gen, 1u);
+  } else {
+    while (*reinterpret_cast<volatile unsigned*>(gen) == g) __nanosleep(32);
+  }
+  __threadfence();
+}
+
+__global__ void __launch_bounds__(kGnThreads)
+gn_fused_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
+                int groups, int splits, float* __restrict__ part, float eps, const float* __restrict__ gamma,
+                const float* __restrict__ beta, int do_silu, bf16* __restrict__ y, unsigned* __restrict__ bar) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ __align__(16) float sm[2 * kMaxC + 2 * kGnThreads * 8];
+  const int n = blockIdx.y, split = blockIdx.x;
+  gn_stats_block(x1, c1, x2, c2, hw, groups, splits, part, n, split, sm, sm + kMaxC, sm + 2 * kMaxC,
+                 sm + 2 * kMaxC + kGnThreads * 8);
+  __syncthreads();
+  if (threadIdx.x == 0) image_barrier(bar + 2 * n, bar + 2 * n + 1, (unsigned)splits);
+  __syncthreads();
+  const int64_t p_begin = hw * split / splits, p_end = hw * (split + 1) / splits;
+  double* dp = reinterpret_cast<double*>(sm + 2 * kMaxC);              // [2][kGnThreads] doubles
+  float* s_mean = sm + 2 * kMaxC + 4 * kGnThreads;
+  gn_apply_block(x1, c1, x2, c2, hw, groups, splits, part, eps, gamma, beta, do_silu, y, n, p_begin, 1, p_end,
+                 s_mean, s_mean + 64, dp, dp + kGnThreads, sm, sm + kMaxC);
 }
 
 // ---------------------------------------------------------------------------
@@ -585,6 +641,32 @@ __global__ void cast_kernel(const bf16* __restrict__ x, float* __restrict__ y, i
 
 inline int ok() { return cudaGetLastError() == cudaSuccess ? HP_OK : HP_ERR_CUDA; }
 
+// barrier words of the single-launch GroupNorm: [image][count, generation], zeroed
+// once, never reset by the host (the last arriver resets the count)
+constexpr int kGnMaxImages = 64;
+unsigned* g_gn_bar = nullptr;
+
+bool gn_fused_ok(int ctas, cudaStream_t st) {
+  static int capacity = -1;
+  static bool disabled = getenv("HP_GN_FUSED") && getenv("HP_GN_FUSED")[0] == '0';
+  if (disabled) return false;
+  if (!g_gn_bar) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+    if (cudaMalloc(&g_gn_bar, 2 * kGnMaxImages * sizeof(unsigned)) != cudaSuccess) { g_gn_bar = nullptr; return false; }
+    if (cudaMemset(g_gn_bar, 0, 2 * kGnMaxImages * sizeof(unsigned)) != cudaSuccess) return false;
+  }
+  if (capacity < 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gn_fused_kernel, kGnThreads, 0) != cudaSuccess)
+      per_sm = 0;
+    capacity = per_sm * sms;
+  }
+  return ctas <= capacity;    // every CTA resident: the in-kernel barrier cannot deadlock
+}
+
 }  // namespace
 
 extern "C" {
@@ -600,6 +682,13 @@ int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_
   // the pixel partition depends on hw only (never on the batch size n), so one
   // image's statistics are bit-identical whatever else is in the batch
   int splits = hw < 128 ? (int)hw : 128;
+  if (n <= kGnMaxImages && gn_fused_ok(n * splits, st)) {
+    hp_launch_pdl(gn_fused_kernel, dim3(splits, n), dim3(kGnThreads), 0, st, static_cast<const bf16*>(x1), c1,
+                  static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups, splits, stats, eps, gamma, beta, do_silu,
+                  static_cast<bf16*>(y), g_gn_bar);
+    if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
+    return ok();
+  }
   hp_launch_pdl(gn_stats_kernel, dim3(splits, n), dim3(kGnThreads), 0, st, static_cast<const bf16*>(x1), c1,
                                                           static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups,
                                                           splits, stats);

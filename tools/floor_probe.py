@@ -25,13 +25,14 @@ def graph_time(fn, reps=100):
     return s.elapsed_time(e) / reps * 1e3
 
 
-x = torch.randn(256, device="cuda").bfloat16()
-print(f"silu 256 elems: {graph_time(lambda: K.silu(x, out=x)):.2f} us/launch")
-a = torch.randn(128, 64, device="cuda").bfloat16()
-w = torch.randn(64, 64, device="cuda").bfloat16()
-o = torch.empty(128, 64, device="cuda", dtype=torch.bfloat16)
-print(f"gemm 128x64x64: {graph_time(lambda: K.gemm(a, w, out=o)):.2f} us/launch")
-a2 = torch.randn(2048, 64, device="cuda").bfloat16()
-w2 = torch.randn(1280, 64, device="cuda").bfloat16()
-o2 = torch.empty(2048, 1280, device="cuda", dtype=torch.bfloat16)
-print(f"gemm 2048x1280x64: {graph_time(lambda: K.gemm(a2, w2, out=o2)):.2f} us/launch")
+if __name__ == "__main__":
+    x = torch.randn(256, device="cuda").bfloat16()
+    print(f"silu 256 elems: {graph_time(lambda: K.silu(x, out=x)):.2f} us/launch")
+    a = torch.randn(128, 64, device="cuda").bfloat16()
+    w = torch.randn(64, 64, device="cuda").bfloat16()
+    o = torch.empty(128, 64, device="cuda", dtype=torch.bfloat16)
+    print(f"gemm 128x64x64: {graph_time(lambda: K.gemm(a, w, out=o)):.2f} us/launch")
+    a2 = torch.randn(2048, 64, device="cuda").bfloat16()
+    w2 = torch.randn(1280, 64, device="cuda").bfloat16()
+    o2 = torch.empty(2048, 1280, device="cuda", dtype=torch.bfloat16)
+    print(f"gemm 2048x1280x64: {graph_time(lambda: K.gemm(a2, w2, out=o2)):.2f} us/launch")
