@@ -24,6 +24,7 @@ __global__ void signal_kernel(uint32_t* flag, uint32_t value) {
 __global__ void wait_kernel(const volatile uint32_t* flag, uint32_t value, int32_t* status,
                             uint64_t timeout_ns) {
   const uint64_t start = hp_globaltimer();
+  if (status && *reinterpret_cast<volatile int32_t*>(status) == HP_ERR_TIMEOUT) return;   // run already lost
   while (hp_ld_acquire_sys_u32(flag) < value) {
     if (timeout_ns && hp_globaltimer() - start > timeout_ns) {
       if (status) *status = HP_ERR_TIMEOUT;

@@ -225,7 +225,10 @@ sampler_step_kernel(const XT* x, const ET* eps_c, const ET* eps_u, XT* x_out,
     if (threadIdx.x == 0) {
       s_timeout = 0;
       const uint64_t t0 = hp_globaltimer();
-      while (hp_ld_acquire_sys_u32(wait_flag) < wait_value) {
+      // fail fast once a previous wait of this run timed out (sticky status): the run is
+      // already lost, do not spend another 20 s per step
+      const bool dead = ctrl != nullptr && *reinterpret_cast<volatile int32_t*>(&ctrl->status) == HP_ERR_TIMEOUT;
+      while (!dead && hp_ld_acquire_sys_u32(wait_flag) < wait_value) {
         __nanosleep(64);
         if (hp_globaltimer() - t0 > 20000000000ull) { s_timeout = 1; break; }
       }
