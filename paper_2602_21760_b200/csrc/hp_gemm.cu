@@ -1225,11 +1225,15 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   p.vec256 = ((d->ldd % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->d) & 31) == 0) &&
              (!d->residual || (((d->ldr % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->residual) & 31) == 0))) &&
              (p.batch <= 1 || (((d->d_bstride | d->r_bstride) % 16) == 0));
-  {
-    const char* e = getenv("HP_GEMM_PROBE_NOEPI");   // 1: skip the plain epilogue, 2: skip its stores
-    p.probe_noepi = e ? (e[0] == '2' ? 2 : 1) : 0;
-  }
-  p.raster_n = getenv("HP_GEMM_RASTER_N") != nullptr;
+  // development probes, read once: HP_GEMM_PROBE_NOEPI=1 skips the plain epilogue, =2 only
+  // its stores (isolates the main loop); HP_GEMM_RASTER_N=1 walks N tiles fastest
+  static const int probe = [] {
+    const char* e = getenv("HP_GEMM_PROBE_NOEPI");
+    return e ? (e[0] == '2' ? 2 : 1) : 0;
+  }();
+  static const bool raster_n = getenv("HP_GEMM_RASTER_N") != nullptr;
+  p.probe_noepi = probe;
+  p.raster_n = raster_n;
   p.stats_out = reinterpret_cast<float2*>(d->stats_out);
   if (p.stats_out && (p.batch > 1 || d->act == HP_ACT_GEGLU || p.ln_mode || d->a_mode != HP_A_PLAIN ||
                       (reinterpret_cast<uintptr_t>(d->stats_out) & 7)))
