@@ -122,6 +122,11 @@ int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, voi
 /* channel concat NHWC: y[..., 0:c1] = a, y[..., c1:c1+c2] = b */
 int hp_concat_channels(const void* a, int32_t c1, const void* b, int32_t c2, int64_t pixels,
                        void* y, void* stream);
+/* row softmax, bf16 in / bf16 out: y[r, :] = softmax(scale * x[r, :]) over `cols`
+ * values, fp32 math, fixed-order reductions (the VAE decoder's single-head
+ * 512-dim attention runs as GEMM -> this -> GEMM; cols <= 32768).            */
+int hp_softmax_rows(const void* x, int64_t ldx, int64_t rows, int32_t cols, float scale, void* y, int64_t ldy,
+                    void* stream);
 /* per-row channel window copy, bf16: y[r, j] = j < c_src ? x[r, j] : 0 for j < c_dst
  * (zero-pads conv_in's 4 latent channels to the 64 the implicit-GEMM conv needs,
  * and slices conv_out's 4 channels out of its 64-wide padded GEMM output).     */

@@ -634,6 +634,69 @@ __global__ void copy_cols_kernel(const bf16* __restrict__ x, int64_t ldx, int c_
   }
 }
 
+// one CTA per row; the row stays in registers between the max, sum and write passes
+constexpr int kSmThreads = 512;
+constexpr int kSmMaxPerThread = 64;     // cols <= 512 * 64 = 32768
+__global__ void __launch_bounds__(kSmThreads)
+softmax_rows_kernel(const bf16* __restrict__ x, int64_t ldx, int cols, float scale2, bf16* __restrict__ y,
+                    int64_t ldy) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[kSmThreads / 32];
+  const bf16* xr = x + (int64_t)blockIdx.x * ldx;
+  bf16* yr = y + (int64_t)blockIdx.x * ldy;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float v[kSmMaxPerThread];
+  const int nv = cols / 8;                           // 8-element vectors, thread t owns t, t + 512, ...
+  float mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < kSmMaxPerThread / 8; ++k) {
+    const int j = threadIdx.x + k * kSmThreads;
+    if (j < nv) {
+      load8(xr + j * 8, v + k * 8);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        v[k * 8 + e] *= scale2;                      // log2 domain
+        mx = fmaxf(mx, v[k * 8 + e]);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int w = 1; w < kSmThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < kSmMaxPerThread / 8; ++k) {
+    const int j = threadIdx.x + k * kSmThreads;
+    if (j < nv) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        v[k * 8 + e] = exp2f(v[k * 8 + e] - mx);
+        sum += v[k * 8 + e];
+      }
+    }
+  }
+  sum = hp_warp_sum_f(sum);
+  if (lane == 0) red[warp] = sum;
+  __syncthreads();
+  float tot = 0.f;
+  for (int w = 0; w < kSmThreads / 32; ++w) tot += red[w];   // fixed order
+  const float inv = 1.0f / tot;
+#pragma unroll
+  for (int k = 0; k < kSmMaxPerThread / 8; ++k) {
+    const int j = threadIdx.x + k * kSmThreads;
+    if (j < nv) {
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = v[k * 8 + e] * inv;
+      store8(yr + j * 8, o);
+    }
+  }
+}
+
 __global__ void cast_kernel(const bf16* __restrict__ x, float* __restrict__ y, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = __bfloat162float(x[i]);
@@ -743,6 +806,18 @@ int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, voi
   const int64_t total = (int64_t)n * 4 * h * w * (c / 8);
   hp_launch_pdl(upsample2x_kernel, dim3(nblocks(total, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(x), n, h, w, c, static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
+  return ok();
+}
+
+int hp_softmax_rows(const void* x, int64_t ldx, int64_t rows, int32_t cols, float scale, void* y, int64_t ldy,
+                    void* stream) {
+  if (!x || !y || rows < 0 || cols < 8 || cols % 8 || cols > kSmThreads * kSmMaxPerThread || ldx % 8 || ldy % 8)
+    return HP_ERR_PARAMETER;
+  if (!a16(x) || !a16(y)) return HP_ERR_UNSUPPORTED;
+  if (rows == 0) return HP_OK;
+  hp_launch_pdl(softmax_rows_kernel, dim3((unsigned)rows), dim3(kSmThreads), 0, static_cast<cudaStream_t>(stream),
+                static_cast<const bf16*>(x), ldx, cols, scale * 1.4426950408889634f, static_cast<bf16*>(y), ldy);
   if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }

@@ -76,6 +76,7 @@ SIGNATURES = {
     "hp_upsample2x": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP]),
     "hp_concat_channels": (C.c_int, [_VP, _I32, _VP, _I32, _I64, _VP, _VP]),
     "hp_copy_cols": (C.c_int, [_VP, _I64, _I32, _I64, _VP, _I64, _I32, _VP]),
+    "hp_softmax_rows": (C.c_int, [_VP, _I64, _I64, _I32, _F32, _VP, _I64, _VP]),
     "hp_conv3x3_small": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP, _I32, _VP, _I32, _VP]),
     "hp_timestep_embedding": (C.c_int, [_VP, _I32, _I32, _F32, _VP, _VP]),
     "hp_linear_small": (C.c_int, [_VP, _I32, _I32, _VP, _VP, _I32, _I32, _I32, _VP, _VP]),
@@ -277,6 +278,17 @@ def concat_channels(a, c1, b, c2, pixels):
     lib = N.load()
     out = torch.empty((pixels, c1 + c2), dtype=torch.bfloat16, device=a.device)
     check(lib.hp_concat_channels(_p(a), c1, _p(b), c2, pixels, _p(out), _s()), "hp_concat_channels")
+    return out
+
+
+def softmax_rows(x, scale=1.0, out=None):
+    """Row softmax of a 2-D bf16 matrix (fp32 math), e.g. attention scores."""
+    lib = N.load()
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty((rows, cols), dtype=torch.bfloat16, device=x.device)
+    check(lib.hp_softmax_rows(_p(x), x.stride(0), rows, cols, float(scale), _p(out), out.stride(0), _s()),
+          "hp_softmax_rows")
     return out
 
 

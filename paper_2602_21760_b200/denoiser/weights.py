@@ -208,6 +208,70 @@ def _fan_in(shape):
     return int(math.prod(shape[1:])) if len(shape) > 1 else 1
 
 
+@dataclass(frozen=True)
+class VAESpec:
+    """SDXL-style AutoencoderKL decoder (latent -> pixels): the step after the
+    denoising loop."""
+    name: str = "sdxl-vae"
+    latent_channels: int = 4
+    out_channels: int = 3
+    block_out: tuple = (128, 256, 512, 512)
+    layers_per_block: int = 2
+    groups: int = 32
+    scaling_factor: float = 0.13025
+    latent_hw: int = 128
+
+
+VAE_SDXL = VAESpec()
+VAE_TINY = VAESpec(name="vae-tiny", block_out=(64, 64, 128, 128), latent_hw=16)
+
+
+def vae_decoder_param_specs(s: VAESpec) -> list:
+    """(name, shape, kind) of the decoder half of AutoencoderKL (diffusers naming)."""
+    P = []
+
+    def lin(name, o, i):
+        P.append((name + ".weight", (o, i), ("lin", 1.0)))
+        P.append((name + ".bias", (o,), ("bias", 0.0)))
+
+    def conv(name, o, i, k=3, scale=1.0):
+        P.append((name + ".weight", (o, i, k, k), ("lin", scale)))
+        P.append((name + ".bias", (o,), ("bias", 0.0)))
+
+    def norm(name, c):
+        P.append((name + ".weight", (c,), ("one", 0.0)))
+        P.append((name + ".bias", (c,), ("zero", 0.0)))
+
+    def resnet(name, ci, co):
+        norm(name + ".norm1", ci)
+        conv(name + ".conv1", co, ci)
+        norm(name + ".norm2", co)
+        conv(name + ".conv2", co, co, scale=0.5)
+        if ci != co:
+            conv(name + ".conv_shortcut", co, ci, k=1)
+
+    rev = list(reversed(s.block_out))
+    conv("post_quant_conv", s.latent_channels, s.latent_channels, k=1)
+    conv("decoder.conv_in", rev[0], s.latent_channels)
+    resnet("decoder.mid_block.resnets.0", rev[0], rev[0])
+    a = "decoder.mid_block.attentions.0"
+    norm(a + ".group_norm", rev[0])
+    for nm in ("to_q", "to_k", "to_v"):
+        lin(f"{a}.{nm}", rev[0], rev[0])
+    lin(f"{a}.to_out.0", rev[0], rev[0])
+    resnet("decoder.mid_block.resnets.1", rev[0], rev[0])
+    prev = rev[0]
+    for u, co in enumerate(rev):
+        for j in range(s.layers_per_block + 1):
+            resnet(f"decoder.up_blocks.{u}.resnets.{j}", prev if j == 0 else co, co)
+        prev = co
+        if u < len(rev) - 1:
+            conv(f"decoder.up_blocks.{u}.upsamplers.0.conv", co, co)
+    norm("decoder.conv_norm_out", rev[-1])
+    conv("decoder.conv_out", s.out_channels, rev[-1])
+    return P
+
+
 def init_weights(specs, seed: int = 0, device="cpu", dtype=torch.float32) -> dict:
     """Deterministic random init; identical values for a given (seed, device type)."""
     out = {}

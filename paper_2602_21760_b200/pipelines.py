@@ -7,7 +7,10 @@ network on this package's kernels, plugged in at the reference's seam:
   schedule), CFG; configs 1 (tiny, 64^2 latent, 20 steps), 2 (1024^2) and
   4 (2048^2);
 * ``sd3_plan``   — SD3-shaped MMDiT, 28-step flow-matching Euler, CFG;
-  configs 3 and 5.
+  configs 3 and 5;
+* ``build_sdxl_vae`` / ``decode_latents`` — the step after the loop: x0
+  latents to 1024^2 pixels with an SDXL-style VAE decoder (no reference
+  counterpart; parity against ``oracle/vae_ref.py``).
 
 The latent prior is a mixture with one zero-mean unit-variance component per
 prompt (dimension = latent numel), so ``initial_latents`` (engine.py:147-161
@@ -117,3 +120,19 @@ def sdxl_plan(spec, *, variant="serial", steps=50, n_prompts=1, seed=0, guidance
     key = switch_key or ("tiny" if spec.name == "tiny" else "sdxl")
     return make_plan(variant=variant, denoiser=denoiser, schedule=sdxl_schedule(steps), numel=numel,
                      n_prompts=n_prompts, seed=seed, guidance=guidance, switch=SWITCH[key], **kw)
+
+
+def build_sdxl_vae(spec=None, seed: int = 0, weights=None):
+    """Random-init SDXL-style VAE decoder on this package's kernels (the step
+    after the loop)."""
+    from .denoiser.vae import build_vae
+    from .denoiser.weights import VAE_SDXL
+    return build_vae(spec or VAE_SDXL, seed=seed, weights=weights)
+
+
+def decode_latents(vae, x0, latent_hw: int, channels: int = 4):
+    """x0 of a RunResult (flat [B, h*w*C] NHWC latents, numpy or torch) -> images
+    [B, 8h, 8w, 3] fp32 torch tensor on the GPU."""
+    import torch
+    x = torch.as_tensor(np.asarray(x0) if not isinstance(x0, torch.Tensor) else x0)
+    return vae.decode(x.reshape(-1, latent_hw, latent_hw, channels))
