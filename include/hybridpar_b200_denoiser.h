@@ -30,6 +30,7 @@ extern "C" {
 #define HP_ACT_GELU   1       /* exact erf GELU                                     */
 #define HP_ACT_SILU   2
 #define HP_ACT_GEGLU  3       /* weight rows interleaved per 2*BN/2 tile: out = a*gelu(b) */
+#define HP_ACT_QGELU  4       /* quick GELU x * sigmoid(1.702 x) (CLIP ViT-L text encoder) */
 
 typedef struct hp_gemm_desc {
     const void* a;     int64_t lda;            /* bf16                           */
@@ -93,6 +94,7 @@ typedef struct hp_attn_desc {
     void* o;       int64_t ldo;
     int32_t batch, heads, sq, skv;
     float scale;
+    int32_t causal;    /* 1: key j masked for query i when j > i (text encoders; skv <= 128) */
 } hp_attn_desc;
 int hp_attention(const hp_attn_desc* d, void* stream);
 
@@ -122,6 +124,10 @@ int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, voi
 /* channel concat NHWC: y[..., 0:c1] = a, y[..., c1:c1+c2] = b */
 int hp_concat_channels(const void* a, int32_t c1, const void* b, int32_t c2, int64_t pixels,
                        void* y, void* stream);
+/* token + position embedding: y[r, :] = tok[ids[r], :] + pos[r % seq, :] (fp32
+ * tables, bf16 out), the text encoders' input layer.                        */
+int hp_embed_tokens(const int64_t* ids, int64_t rows, int32_t seq, const float* tok, const float* pos, int32_t dim,
+                    void* y, void* stream);
 /* row softmax, bf16 in / bf16 out: y[r, :] = softmax(scale * x[r, :]) over `cols`
  * values, fp32 math, fixed-order reductions (the VAE decoder's single-head
  * 512-dim attention runs as GEMM -> this -> GEMM; cols <= 32768).            */

@@ -52,6 +52,7 @@ constexpr float kRescaleThreshold = 8.0f;            // log2 units
 
 struct AttnParams {
   int sq, skv, heads;
+  int causal;
   int q_col0, k_col0, v_col0;
   __nv_bfloat16* o; long long ldo;
   float scale_log2;
@@ -267,7 +268,10 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     for (int j = 0; j < J; ++j) {
       mbar_wait(&s_full[q], j & 1);
       tc_fence_after();
-      const int valid = min(kBK, p.skv - j * kBK);
+      // keys of this block this row may see: the sequence end and, when causal (single
+      // block), the row's own position
+      const int valid = p.causal ? min(min(kBK, p.skv - j * kBK), q0 + q * kBQ + row - j * kBK + 1)
+                                 : min(kBK, p.skv - j * kBK);
       // pass 1: block row max straight from TMEM (32 columns at a time)
       float mx = -INFINITY;
 #pragma unroll
@@ -707,6 +711,8 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
     return HP_ERR_CUDA;
   AttnParams p{};
   p.sq = d->sq; p.skv = d->skv; p.heads = d->heads;
+  p.causal = d->causal ? 1 : 0;
+  if (p.causal && d->skv > kBK) return HP_ERR_UNSUPPORTED;    // single key block only (text encoders)
   p.q_col0 = (int)d->q_col0; p.k_col0 = (int)d->k_col0; p.v_col0 = (int)d->v_col0;
   p.o = static_cast<__nv_bfloat16*>(d->o); p.ldo = d->ldo;
   p.scale_log2 = d->scale * 1.4426950408889634f;

@@ -697,6 +697,19 @@ softmax_rows_kernel(const bf16* __restrict__ x, int64_t ldx, int cols, float sca
   }
 }
 
+__global__ void embed_tokens_kernel(const int64_t* __restrict__ ids, int64_t rows, int seq,
+                                    const float* __restrict__ tok, const float* __restrict__ pos, int dim,
+                                    bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = rows * dim;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / dim;
+    const int c = (int)(i - r * dim);
+    y[i] = __float2bfloat16_rn(tok[ids[r] * dim + c] + pos[(r % seq) * dim + c]);
+  }
+}
+
 __global__ void cast_kernel(const bf16* __restrict__ x, float* __restrict__ y, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = __bfloat162float(x[i]);
@@ -806,6 +819,16 @@ int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, voi
   const int64_t total = (int64_t)n * 4 * h * w * (c / 8);
   hp_launch_pdl(upsample2x_kernel, dim3(nblocks(total, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
       static_cast<const bf16*>(x), n, h, w, c, static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
+  return ok();
+}
+
+int hp_embed_tokens(const int64_t* ids, int64_t rows, int32_t seq, const float* tok, const float* pos, int32_t dim,
+                    void* y, void* stream) {
+  if (!ids || !tok || !pos || !y || rows < 0 || seq < 1 || dim < 1) return HP_ERR_PARAMETER;
+  if (rows == 0) return HP_OK;
+  hp_launch_pdl(embed_tokens_kernel, dim3(nblocks(rows * dim, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                ids, rows, seq, tok, pos, dim, static_cast<bf16*>(y));
   if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }

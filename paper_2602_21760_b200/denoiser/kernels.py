@@ -29,7 +29,7 @@ def check(rc, what):
 _VP, _I32, _I64, _F32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
 
 HP_A_PLAIN, HP_A_CONV3X3, HP_A_CONV3X3_S2 = 0, 1, 2
-ACT_NONE, ACT_GELU, ACT_SILU, ACT_GEGLU = 0, 1, 2, 3
+ACT_NONE, ACT_GELU, ACT_SILU, ACT_GEGLU, ACT_QGELU = 0, 1, 2, 3, 4
 
 
 class HpGemmDesc(C.Structure):
@@ -60,7 +60,7 @@ class HpAttnDesc(C.Structure):
         ("v", _VP), ("ldv", _I64), ("v_col0", _I64),
         ("o", _VP), ("ldo", _I64),
         ("batch", _I32), ("heads", _I32), ("sq", _I32), ("skv", _I32),
-        ("scale", _F32),
+        ("scale", _F32), ("causal", _I32),
     ]
 
 
@@ -77,6 +77,7 @@ SIGNATURES = {
     "hp_concat_channels": (C.c_int, [_VP, _I32, _VP, _I32, _I64, _VP, _VP]),
     "hp_copy_cols": (C.c_int, [_VP, _I64, _I32, _I64, _VP, _I64, _I32, _VP]),
     "hp_softmax_rows": (C.c_int, [_VP, _I64, _I64, _I32, _F32, _VP, _I64, _VP]),
+    "hp_embed_tokens": (C.c_int, [_VP, _I64, _I32, _VP, _VP, _I32, _VP, _VP]),
     "hp_conv3x3_small": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP, _I32, _VP, _I32, _VP]),
     "hp_timestep_embedding": (C.c_int, [_VP, _I32, _I32, _F32, _VP, _VP]),
     "hp_linear_small": (C.c_int, [_VP, _I32, _I32, _VP, _VP, _I32, _I32, _I32, _VP, _VP]),
@@ -212,7 +213,7 @@ def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, a
     return out
 
 
-def attention(q, k, v, out, *, batch, heads, sq, skv, scale, q_col0=0, k_col0=0, v_col0=0):
+def attention(q, k, v, out, *, batch, heads, sq, skv, scale, q_col0=0, k_col0=0, v_col0=0, causal=False):
     """Multi-head attention, head_dim 64; q/k/v/out are 2-D [batch*rows, ld] views."""
     lib = N.load()
     d = HpAttnDesc()
@@ -221,6 +222,7 @@ def attention(q, k, v, out, *, batch, heads, sq, skv, scale, q_col0=0, k_col0=0,
     d.v, d.ldv, d.v_col0 = _p(v), v.stride(0), v_col0
     d.o, d.ldo = _p(out), out.stride(0)
     d.batch, d.heads, d.sq, d.skv, d.scale = batch, heads, sq, skv, float(scale)
+    d.causal = 1 if causal else 0
     check(lib.hp_attention(C.byref(d), _s()), "hp_attention")
     return out
 
@@ -278,6 +280,17 @@ def concat_channels(a, c1, b, c2, pixels):
     lib = N.load()
     out = torch.empty((pixels, c1 + c2), dtype=torch.bfloat16, device=a.device)
     check(lib.hp_concat_channels(_p(a), c1, _p(b), c2, pixels, _p(out), _s()), "hp_concat_channels")
+    return out
+
+
+def embed_tokens(ids, tok, pos, out=None):
+    """ids [n, seq] int64 -> [n*seq, dim] bf16 = tok[ids] + pos[position]."""
+    lib = N.load()
+    n, seq = ids.shape
+    dim = tok.shape[1]
+    if out is None:
+        out = torch.empty((n * seq, dim), dtype=torch.bfloat16, device=ids.device)
+    check(lib.hp_embed_tokens(_p(ids), n * seq, seq, _p(tok), _p(pos), dim, _p(out), _s()), "hp_embed_tokens")
     return out
 
 
