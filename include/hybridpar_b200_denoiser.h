@@ -30,7 +30,6 @@ extern "C" {
 #define HP_ACT_GELU   1       /* exact erf GELU                                     */
 #define HP_ACT_SILU   2
 #define HP_ACT_GEGLU  3       /* weight rows interleaved per 2*BN/2 tile: out = a*gelu(b) */
-#define HP_ACT_QGELU  4       /* quick GELU x * sigmoid(1.702 x) (CLIP ViT-L text encoder) */
 
 typedef struct hp_gemm_desc {
     const void* a;     int64_t lda;            /* bf16                           */
@@ -119,6 +118,9 @@ int hp_layer_norm_joint(const void* x, int64_t rows, int32_t c, float eps, const
                         int64_t rows_per_batch, int64_t split, void* y, void* stream);
 /* y = silu(x) elementwise, bf16 */
 int hp_silu(const void* x, void* y, int64_t n, void* stream);
+/* y = x * sigmoid(1.702 x) (quick GELU, CLIP ViT-L MLP) elementwise, bf16; kept out
+ * of the GEMM epilogue, whose unrolled code every denoiser GEMM shares */
+int hp_quick_gelu(const void* x, void* y, int64_t n, void* stream);
 /* nearest 2x upsample NHWC bf16: [n, h, w, c] -> [n, 2h, 2w, c] */
 int hp_upsample2x(const void* x, int32_t n, int32_t h, int32_t w, int32_t c, void* y, void* stream);
 /* channel concat NHWC: y[..., 0:c1] = a, y[..., c1:c1+c2] = b */

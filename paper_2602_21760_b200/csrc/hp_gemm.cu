@@ -301,11 +301,6 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     } else if (p.act == HP_ACT_SILU) {
 #pragma unroll
       for (int q = 0; q < 16; ++q) v2[q] = pack2(silu_f(lo2(v2[q])), silu_f(hi2(v2[q])));
-    } else if (p.act == HP_ACT_QGELU) {
-#pragma unroll
-      for (int q = 0; q < 16; ++q)
-        v2[q] = pack2(lo2(v2[q]) / (1.0f + __expf(-1.702f * lo2(v2[q]))),
-                      hi2(v2[q]) / (1.0f + __expf(-1.702f * hi2(v2[q]))));
     }
     if (p.colscale) {
       const float4* g4 = reinterpret_cast<const float4*>(p.colscale + col);

@@ -361,6 +361,18 @@ ln_kernel(const bf16* __restrict__ x, int64_t rows, int c, float eps, const floa
 }
 
 // ---------------------------------------------------------------------------
+__global__ void quick_gelu_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, int64_t n8) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float v[8];
+    load8(x + i * 8, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = v[k] / (1.0f + __expf(-1.702f * v[k]));
+    store8(y + i * 8, v);
+  }
+}
+
 __global__ void silu_kernel(const bf16* __restrict__ x, bf16* __restrict__ y, int64_t n8) {
   pdl_wait();
   pdl_trigger();
@@ -802,6 +814,14 @@ int hp_layer_norm_joint(const void* x, int64_t rows, int32_t c, float eps, const
   hp_launch_pdl(ln_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream),
       static_cast<const bf16*>(x), rows, c, eps, (const float*)nullptr, (const float*)nullptr, shift, scale, ldm,
       rows_per_batch, static_cast<bf16*>(y), shift2, scale2, split);
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
+  return ok();
+}
+
+int hp_quick_gelu(const void* x, void* y, int64_t n, void* stream) {
+  if (!x || !y || n % 8) return HP_ERR_PARAMETER;
+  hp_launch_pdl(quick_gelu_kernel, dim3(nblocks(n / 8, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                static_cast<const bf16*>(x), static_cast<bf16*>(y), n / 8);
   if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }

@@ -29,7 +29,7 @@ def check(rc, what):
 _VP, _I32, _I64, _F32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
 
 HP_A_PLAIN, HP_A_CONV3X3, HP_A_CONV3X3_S2 = 0, 1, 2
-ACT_NONE, ACT_GELU, ACT_SILU, ACT_GEGLU, ACT_QGELU = 0, 1, 2, 3, 4
+ACT_NONE, ACT_GELU, ACT_SILU, ACT_GEGLU = 0, 1, 2, 3
 
 
 class HpGemmDesc(C.Structure):
@@ -78,6 +78,7 @@ SIGNATURES = {
     "hp_copy_cols": (C.c_int, [_VP, _I64, _I32, _I64, _VP, _I64, _I32, _VP]),
     "hp_softmax_rows": (C.c_int, [_VP, _I64, _I64, _I32, _F32, _VP, _I64, _VP]),
     "hp_embed_tokens": (C.c_int, [_VP, _I64, _I32, _VP, _VP, _I32, _VP, _VP]),
+    "hp_quick_gelu": (C.c_int, [_VP, _VP, _I64, _VP]),
     "hp_conv3x3_small": (C.c_int, [_VP, _I32, _I32, _I32, _I32, _VP, _VP, _I32, _VP, _I32, _VP]),
     "hp_timestep_embedding": (C.c_int, [_VP, _I32, _I32, _F32, _VP, _VP]),
     "hp_linear_small": (C.c_int, [_VP, _I32, _I32, _VP, _VP, _I32, _I32, _I32, _VP, _VP]),
@@ -259,6 +260,13 @@ def layer_norm_joint(x, c, rows_per_batch, split, shift, scale, shift2, scale2, 
         out = torch.empty_like(x)
     check(lib.hp_layer_norm_joint(_p(x), rows, c, eps, _p(shift), _p(scale), _p(shift2), _p(scale2), int(ldm),
                                   int(rows_per_batch), int(split), _p(out), _s()), "hp_layer_norm_joint")
+    return out
+
+
+def quick_gelu(x, out=None):
+    lib = N.load()
+    out = torch.empty_like(x) if out is None else out
+    check(lib.hp_quick_gelu(_p(x), _p(out), x.numel(), _s()), "hp_quick_gelu")
     return out
 
 

@@ -11,8 +11,9 @@ reference has no text encoders; parity is against the plain-torch
 restatement ``oracle/text_ref.py``.
 
 Kernels: token+position embedding gather, LayerNorm, fused-QKV / out / MLP
-GEMMs (tcgen05 CTA pairs; quick-GELU and GELU fused in the epilogue, residual
-adds in the epilogue), single-block causal attention (head_dim 64).
+GEMMs (tcgen05 CTA pairs; GELU and residual adds fused in the epilogue;
+quick-GELU as a separate elementwise pass), single-block causal attention
+(head_dim 64).
 """
 from __future__ import annotations
 
@@ -101,7 +102,7 @@ class CLIPTextEncoder:
         self.lnf = (W[f"{t}.final_layer_norm.weight"].to(dev).float().contiguous(),
                     W[f"{t}.final_layer_norm.bias"].to(dev).float().contiguous())
         self.proj = W["text_projection.weight"].to(dev).to(torch.bfloat16).contiguous() if s.proj else None
-        self.act = K.ACT_QGELU if s.act == "quick_gelu" else K.ACT_GELU
+        self.quick = s.act == "quick_gelu"
 
     def _layer(self, x, n, L):
         s = self.s
@@ -113,7 +114,10 @@ class CLIPTextEncoder:
                     q_col0=0, k_col0=H, v_col0=2 * H, causal=True)
         x = K.gemm(att, L["o_w"], bias=L["o_b"], residual=x)
         y = K.layer_norm(x, H, gamma=L["ln2"][0], beta=L["ln2"][1], eps=1e-5)
-        h = K.gemm(y, L["fc1_w"], bias=L["fc1_b"], act=self.act)
+        if self.quick:                        # quick GELU as its own pass (keeps the GEMM epilogue lean)
+            h = K.quick_gelu(K.gemm(y, L["fc1_w"], bias=L["fc1_b"]))
+        else:
+            h = K.gemm(y, L["fc1_w"], bias=L["fc1_b"], act=K.ACT_GELU)
         return K.gemm(h, L["fc2_w"], bias=L["fc2_b"], residual=x)
 
     def encode(self, ids: torch.Tensor):
