@@ -190,7 +190,12 @@ template <int BN> struct StatW { static constexpr int value = BN > 256 ? BN / 2 
 // Epilogue columns [c_begin, c_begin + c_count) of one 128 x BN tile (default: all);
 // `red` (split-K) holds the other K half's fp32 partial for these columns in shared
 // memory, laid out [column / 4][128 rows][4].
-template <int BN, int EPI>
+// Activation code compiled into an epilogue instance: the unrolled epilogue is
+// shared by every denoiser GEMM, and each runtime activation branch it carries
+// costs the activation-free GEMMs time (measured: GELU + SiLU branches 0.4 ms
+// per U-Net forward), so the CTA-pair kernel is instantiated per mode.
+constexpr int kAmNone = 0, kAmGeglu = 1, kAmPoint = 2, kAmAny = 3;
+template <int BN, int EPI, int AM = kAmAny>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
                                               int lane, const float* sb, float* row_stats, const float* scs,
                                               float f_mean, float f_rstd, int c_begin = 0, int c_count = BN,
@@ -198,7 +203,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
   const int row = m0 + quarter * 32 + lane;
   const bool row_ok = row < p.M;
   const uint32_t lane_addr = tmem_acc + ((uint32_t)(quarter * 32) << 16);
-  if (p.act == HP_ACT_GEGLU) {
+  if (AM == kAmGeglu || (AM == kAmAny && p.act == HP_ACT_GEGLU)) {
     // tile columns [0, BN/2) are the linear halves, [BN/2, BN) the gates of
     // the same BN/2 outputs (weights interleaved on the host)
     const int out0 = n0 / 2;
@@ -295,12 +300,14 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         v2[2 * q + 1] = fadd2(v2[2 * q + 1], pack2(b.z, b.w));
       }
     }
-    if (p.act == HP_ACT_GELU) {
+    if constexpr (AM == kAmPoint || AM == kAmAny) {
+      if (p.act == HP_ACT_GELU) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v2[q] = gelu_erf2(v2[q]);
-    } else if (p.act == HP_ACT_SILU) {
+        for (int q = 0; q < 16; ++q) v2[q] = gelu_erf2(v2[q]);
+      } else if (p.act == HP_ACT_SILU) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v2[q] = pack2(silu_f(lo2(v2[q])), silu_f(hi2(v2[q])));
+        for (int q = 0; q < 16; ++q) v2[q] = pack2(silu_f(lo2(v2[q])), silu_f(hi2(v2[q])));
+      }
     }
     if (p.colscale) {
       const float4* g4 = reinterpret_cast<const float4*>(p.colscale + col);
@@ -605,7 +612,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 // work: the 1-CTA kernel is L2-bandwidth-bound on B200 (LTS cap), this is not.
 //   warp 0  TMA producer (both CTAs)   warp 1  MMA issuer (leader CTA)
 //   warp 2  TMEM allocator (both)      warps 4..7  epilogue (both, own rows)
-template <int BN, int STAGES>
+template <int BN, int STAGES, int AM>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   constexpr uint32_t kBHalfBytes = (BN / 2) * BK * 2;
@@ -775,13 +782,13 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         q.d += (long long)bt * p.d_bs;
         if (q.res) q.res += (long long)bt * p.r_bs;
         if (q.colscale) q.colscale += (long long)bt * p.cs_bs;
-        epilogue_tile<BN, kEpiPlain>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+        epilogue_tile<BN, kEpiPlain, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       } else if (fold) {
-        epilogue_tile<BN, kEpiFold>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
+        epilogue_tile<BN, kEpiFold, AM>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
       } else if (p.stats_out) {
-        epilogue_tile<BN, kEpiStats>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+        epilogue_tile<BN, kEpiStats, AM>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       } else {
-        if (p.probe_noepi != 1) epilogue_tile<BN, kEpiPlain>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+        if (p.probe_noepi != 1) epilogue_tile<BN, kEpiPlain, AM>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       }
       tc_fence_before();
       __syncwarp();
@@ -958,13 +965,13 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const float* sb = (p.bias != nullptr || p.bias2 != nullptr) ? sbias : nullptr;
     const float4* red = reinterpret_cast<const float4*>(smA);
     if (p.ln_stats) {
-      epilogue_tile<BN, kEpiFold>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, scolsum, f_mean, f_rstd, h0,
+      epilogue_tile<BN, kEpiFold, kAmNone>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, scolsum, f_mean, f_rstd, h0,
                                   kSubN, red);
     } else if (p.stats_out) {
-      epilogue_tile<BN, kEpiStats>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f, h0, kSubN,
+      epilogue_tile<BN, kEpiStats, kAmNone>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f, h0, kSubN,
                                    red);
     } else {
-      epilogue_tile<BN, kEpiPlain>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f, h0, kSubN,
+      epilogue_tile<BN, kEpiPlain, kAmNone>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f, h0, kSubN,
                                    red);
     }
   }
@@ -1056,13 +1063,13 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& 
   return HP_OK;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int AM>
 int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
   constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + (BN / 2) * BK * 2) + 256 + 4 * BN * sizeof(float);
   static_assert(smem <= 227 * 1024, "pair GEMM smem");
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_pair_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_pair_kernel<BN, STAGES, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
       return HP_ERR_CUDA;
     attr_set = true;
@@ -1084,7 +1091,7 @@ int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPar
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = hp_pdl_enabled() ? 2 : 1;
-  if (cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BN, STAGES>, ta, tb, p) != cudaSuccess) return HP_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BN, STAGES, AM>, ta, tb, p) != cudaSuccess) return HP_ERR_CUDA;
   return HP_OK;
 }
 
@@ -1140,7 +1147,7 @@ bool pair_enabled() {
 // Depends on N and K only, never on M, so one image's rows are computed identically
 // whatever else is in the batch (batch invariance: split-K changes the summation).
 bool splitk_ok(int64_t M, int64_t N, int64_t K, int act, int batch, int mode) {
-  if (!splitk_enabled() || !pair_enabled() || act == HP_ACT_GEGLU || batch > 1 || M <= BM) return false;
+  if (!splitk_enabled() || !pair_enabled() || act != HP_ACT_NONE || batch > 1 || M <= BM) return false;
   // the exchange + half epilogue costs ~4 us: worth it from K = 4096 on (ff2, 3x3 convs)
   return N % 320 == 0 && N >= 1280 && K / BK >= 64;
 }
@@ -1304,12 +1311,29 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   }
   if (pair) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
+    if (d->act == HP_ACT_GEGLU) {
+      switch (bn) {
+        case 256: return launch_gemm_pair<256, 6, kAmGeglu>(ta, tb, p, st);
+        case 128: return launch_gemm_pair<128, 8, kAmGeglu>(ta, tb, p, st);
+        default: return HP_ERR_UNSUPPORTED;
+      }
+    }
+    if (d->act != HP_ACT_NONE) {
+      switch (bn) {
+        case 320: return launch_gemm_pair<320, 5, kAmPoint>(ta, tb, p, st);
+        case 256: return launch_gemm_pair<256, 6, kAmPoint>(ta, tb, p, st);
+        case 160: return launch_gemm_pair<160, 7, kAmPoint>(ta, tb, p, st);
+        case 128: return launch_gemm_pair<128, 8, kAmPoint>(ta, tb, p, st);
+        case 64: return launch_gemm_pair<64, 8, kAmPoint>(ta, tb, p, st);
+        default: return HP_ERR_UNSUPPORTED;
+      }
+    }
     switch (bn) {
-      case 320: return launch_gemm_pair<320, 5>(ta, tb, p, st);
-      case 256: return launch_gemm_pair<256, 6>(ta, tb, p, st);
-      case 160: return launch_gemm_pair<160, 7>(ta, tb, p, st);
-      case 128: return launch_gemm_pair<128, 8>(ta, tb, p, st);
-      case 64: return launch_gemm_pair<64, 8>(ta, tb, p, st);
+      case 320: return launch_gemm_pair<320, 5, kAmNone>(ta, tb, p, st);
+      case 256: return launch_gemm_pair<256, 6, kAmNone>(ta, tb, p, st);
+      case 160: return launch_gemm_pair<160, 7, kAmNone>(ta, tb, p, st);
+      case 128: return launch_gemm_pair<128, 8, kAmNone>(ta, tb, p, st);
+      case 64: return launch_gemm_pair<64, 8, kAmNone>(ta, tb, p, st);
       default: return HP_ERR_UNSUPPORTED;
     }
   }
