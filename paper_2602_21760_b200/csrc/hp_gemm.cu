@@ -190,16 +190,20 @@ template <int BN> struct StatW { static constexpr int value = BN > 256 ? BN / 2 
 // Epilogue columns [c_begin, c_begin + c_count) of one 128 x BN tile (default: all);
 // `red` (split-K) holds the other K half's fp32 partial for these columns in shared
 // memory, laid out [column / 4][128 rows][4].
-// Activation code compiled into an epilogue instance: the unrolled epilogue is
-// shared by every denoiser GEMM, and each runtime activation branch it carries
-// costs the activation-free GEMMs time (measured: GELU + SiLU branches 0.4 ms
-// per U-Net forward), so the CTA-pair kernel is instantiated per mode.
-constexpr int kAmNone = 0, kAmGeglu = 1, kAmPoint = 2, kAmAny = 3;
+// Epilogue modes compiled into an instance: the unrolled epilogue is shared by
+// every denoiser GEMM, and each runtime branch it carries costs the common case
+// time (measured per U-Net forward: GELU + SiLU branches 0.4 ms; alpha, column
+// gate and the 16-byte store fallback another 0.2 ms). "Lean" modes (no
+// activation or GEGLU; alpha 1, no column gate, 32-byte-aligned rows) carry
+// none of that; kAmAny handles everything at run time.
+constexpr int kAmNone = 0, kAmGeglu = 1, kAmAny = 3;
 template <int BN, int EPI, int AM = kAmAny>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
                                               int lane, const float* sb, float* row_stats, const float* scs,
                                               float f_mean, float f_rstd, int c_begin = 0, int c_count = BN,
                                               const float4* red = nullptr) {
+  constexpr bool kLean = AM == kAmNone || AM == kAmGeglu;
+  const bool v8 = kLean ? true : p.vec256;
   const int row = m0 + quarter * 32 + lane;
   const bool row_ok = row < p.M;
   const uint32_t lane_addr = tmem_acc + ((uint32_t)(quarter * 32) << 16);
@@ -216,7 +220,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
       if (!row_ok) continue;
       const int ocol = out0 + c * 32;
       uint32_t packed[16];
-      const bool scale = p.alpha != 1.0f;
+      const bool scale = !kLean && p.alpha != 1.0f;
       const uint64_t alpha2 = pack2(p.alpha, p.alpha);
       const uint64_t nmean2 = pack2(-f_mean, -f_mean), rstd2 = pack2(f_rstd, f_rstd);
 #pragma unroll
@@ -238,7 +242,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         const uint64_t o2 = fmul2(a2, gelu_erf2(g2));
         packed[j / 2] = pack_bf16(lo2(o2), hi2(o2));
       }
-      if (p.probe_noepi != 2) st_row64(p.d + (long long)row * p.ldd + ocol, packed, p.vec256);
+      if (kLean || p.probe_noepi != 2) st_row64(p.d + (long long)row * p.ldd + ocol, packed, v8);
       else if (packed[0] == 0x7fc07fc0u) p.d[row] = __float2bfloat16(0.f);   // keep the math live
     }
     return;
@@ -249,7 +253,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
   uint32_t rn[16];
   float st_sum = 0.f, st_sq = 0.f;            // LayerNorm partials of the stored (bf16) row
   float sh_k = 0.f, sh_s1 = 0.f, sh_s2 = 0.f;   // stats_out: sums shifted by the segment's first value
-  if (has_res) ld_row64(res_row, rn, p.vec256);
+  if (has_res) ld_row64(res_row, rn, v8);
   const int nch = c_count / 32;
 #pragma unroll 1
   for (int cc = 0; cc < nch; ++cc) {
@@ -259,7 +263,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     uint32_t rc[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) rc[q] = rn[q];
-    if (has_res && cc + 1 < nch) ld_row64(res_row + (cc + 1) * 32, rn, p.vec256);   // next chunk in flight
+    if (has_res && cc + 1 < nch) ld_row64(res_row + (cc + 1) * 32, rn, v8);   // next chunk in flight
     tmem_ld_wait();
     if (!row_ok) continue;
     const int col = n0 + c * 32;
@@ -276,7 +280,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         v2[2 * q + 1] = fadd2(v2[2 * q + 1], pack2(f.z, f.w));
       }
     }
-    if (p.alpha != 1.0f) {
+    if (!kLean && p.alpha != 1.0f) {
       const uint64_t alpha2 = pack2(p.alpha, p.alpha);
 #pragma unroll
       for (int q = 0; q < 16; ++q) v2[q] = fmul2(v2[q], alpha2);
@@ -300,7 +304,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         v2[2 * q + 1] = fadd2(v2[2 * q + 1], pack2(b.z, b.w));
       }
     }
-    if constexpr (AM == kAmPoint || AM == kAmAny) {
+    if constexpr (AM == kAmAny) {
       if (p.act == HP_ACT_GELU) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) v2[q] = gelu_erf2(v2[q]);
@@ -309,7 +313,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         for (int q = 0; q < 16; ++q) v2[q] = pack2(silu_f(lo2(v2[q])), silu_f(hi2(v2[q])));
       }
     }
-    if (p.colscale) {
+    if (!kLean && p.colscale) {
       const float4* g4 = reinterpret_cast<const float4*>(p.colscale + col);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -328,7 +332,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     uint32_t w[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) w[q] = pack_bf16(lo2(v2[q]), hi2(v2[q]));
-    if (p.probe_noepi != 2) st_row64(p.d + (long long)row * p.ldd + col, w, p.vec256);
+    if (kLean || p.probe_noepi != 2) st_row64(p.d + (long long)row * p.ldd + col, w, v8);
     else if (w[0] == 0x7fc07fc0u) p.d[row] = __float2bfloat16(0.f);          // keep the math live
     if constexpr (EPI == kEpiStats) {
       if ((c * 32) % kStatW == 0) sh_k = unpack_bf16(w[0]).x;
@@ -1305,26 +1309,29 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
     if (!make_map(&tb, d->b, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (pair && bn == 320 && splitk_ok(d->M, d->N, d->K, d->act, p.batch, d->a_mode)) {
+  // lean epilogue: no activation code, alpha 1, no column gate, 32-byte rows, no probe
+  const bool lean = p.alpha == 1.0f && !p.colscale && p.vec256 && p.probe_noepi == 0 &&
+                    (d->act == HP_ACT_NONE || d->act == HP_ACT_GEGLU);
+  if (pair && lean && bn == 320 && splitk_ok(d->M, d->N, d->K, d->act, p.batch, d->a_mode)) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
     return launch_gemm_splitk<5>(ta, tb, p, st);
   }
   if (pair) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
-    if (d->act == HP_ACT_GEGLU) {
+    if (lean && d->act == HP_ACT_GEGLU) {
       switch (bn) {
         case 256: return launch_gemm_pair<256, 6, kAmGeglu>(ta, tb, p, st);
         case 128: return launch_gemm_pair<128, 8, kAmGeglu>(ta, tb, p, st);
         default: return HP_ERR_UNSUPPORTED;
       }
     }
-    if (d->act != HP_ACT_NONE) {
+    if (!lean || d->act != HP_ACT_NONE) {
       switch (bn) {
-        case 320: return launch_gemm_pair<320, 5, kAmPoint>(ta, tb, p, st);
-        case 256: return launch_gemm_pair<256, 6, kAmPoint>(ta, tb, p, st);
-        case 160: return launch_gemm_pair<160, 7, kAmPoint>(ta, tb, p, st);
-        case 128: return launch_gemm_pair<128, 8, kAmPoint>(ta, tb, p, st);
-        case 64: return launch_gemm_pair<64, 8, kAmPoint>(ta, tb, p, st);
+        case 320: return launch_gemm_pair<320, 5, kAmAny>(ta, tb, p, st);
+        case 256: return launch_gemm_pair<256, 6, kAmAny>(ta, tb, p, st);
+        case 160: return launch_gemm_pair<160, 7, kAmAny>(ta, tb, p, st);
+        case 128: return launch_gemm_pair<128, 8, kAmAny>(ta, tb, p, st);
+        case 64: return launch_gemm_pair<64, 8, kAmAny>(ta, tb, p, st);
         default: return HP_ERR_UNSUPPORTED;
       }
     }

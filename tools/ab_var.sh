@@ -1,1 +1,1 @@
-for v in "" var_noact "" var_noact; do echo "== ${v:-current}"; HP_LIB_VARIANT=$v python tools/time_unet.py | grep forward; done
+for v in "" var_lean "" var_lean; do echo "== ${v:-current}"; HP_LIB_VARIANT=$v python tools/time_unet.py | grep forward; done
