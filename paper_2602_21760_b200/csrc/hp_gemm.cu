@@ -616,7 +616,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 // work: the 1-CTA kernel is L2-bandwidth-bound on B200 (LTS cap), this is not.
 //   warp 0  TMA producer (both CTAs)   warp 1  MMA issuer (leader CTA)
 //   warp 2  TMEM allocator (both)      warps 4..7  epilogue (both, own rows)
-template <int BN, int STAGES, int AM>
+constexpr int kEpRuntime = -1;   // epilogue flavour chosen per tile at run time (kAmAny instances)
+template <int BN, int STAGES, int AM, int EP>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   constexpr uint32_t kBHalfBytes = (BN / 2) * BK * 2;
@@ -752,7 +753,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int quarter = warp & 3;
     const int et = threadIdx.x - 128;
     const bool any_bias = p.bias != nullptr || p.bias2 != nullptr;
-    const bool fold = p.ln_stats != nullptr;
+    const bool fold = EP == kEpiFold || (EP == kEpRuntime && p.ln_stats != nullptr);
     uint32_t local = 0;
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++local) {
       const uint32_t acc = local % kAcc;
@@ -781,7 +782,9 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       const uint32_t t_acc = tmem_base + acc * BN;
-      if (p.batch > 1) {
+      if constexpr (EP != kEpRuntime) {            // one epilogue flavour compiled in (batch 1)
+        epilogue_tile<BN, EP, AM>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
+      } else if (p.batch > 1) {
         GemmParams q = p;
         q.d += (long long)bt * p.d_bs;
         if (q.res) q.res += (long long)bt * p.r_bs;
@@ -1067,13 +1070,13 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& 
   return HP_OK;
 }
 
-template <int BN, int STAGES, int AM>
+template <int BN, int STAGES, int AM, int EP = kEpRuntime>
 int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
   constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + (BN / 2) * BK * 2) + 256 + 4 * BN * sizeof(float);
   static_assert(smem <= 227 * 1024, "pair GEMM smem");
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_pair_kernel<BN, STAGES, AM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(gemm_pair_kernel<BN, STAGES, AM, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
       return HP_ERR_CUDA;
     attr_set = true;
@@ -1095,7 +1098,7 @@ int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPar
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = hp_pdl_enabled() ? 2 : 1;
-  if (cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BN, STAGES, AM>, ta, tb, p) != cudaSuccess) return HP_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BN, STAGES, AM, EP>, ta, tb, p) != cudaSuccess) return HP_ERR_CUDA;
   return HP_OK;
 }
 
@@ -1310,7 +1313,7 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // lean epilogue: no activation code, alpha 1, no column gate, 32-byte rows, no probe
-  const bool lean = p.alpha == 1.0f && !p.colscale && p.vec256 && p.probe_noepi == 0 &&
+  const bool lean = p.alpha == 1.0f && !p.colscale && p.vec256 && p.probe_noepi == 0 && p.batch == 1 &&
                     (d->act == HP_ACT_NONE || d->act == HP_ACT_GEGLU);
   if (pair && lean && bn == 320 && splitk_ok(d->M, d->N, d->K, d->act, p.batch, d->a_mode)) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
@@ -1319,9 +1322,12 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if (pair) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
     if (lean && d->act == HP_ACT_GEGLU) {
+      const bool f = p.ln_stats != nullptr;
       switch (bn) {
-        case 256: return launch_gemm_pair<256, 6, kAmGeglu>(ta, tb, p, st);
-        case 128: return launch_gemm_pair<128, 8, kAmGeglu>(ta, tb, p, st);
+        case 256: return f ? launch_gemm_pair<256, 6, kAmGeglu, kEpiFold>(ta, tb, p, st)
+                           : launch_gemm_pair<256, 6, kAmGeglu, kEpiPlain>(ta, tb, p, st);
+        case 128: return f ? launch_gemm_pair<128, 8, kAmGeglu, kEpiFold>(ta, tb, p, st)
+                           : launch_gemm_pair<128, 8, kAmGeglu, kEpiPlain>(ta, tb, p, st);
         default: return HP_ERR_UNSUPPORTED;
       }
     }
@@ -1335,14 +1341,20 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
         default: return HP_ERR_UNSUPPORTED;
       }
     }
+    const int ep = p.ln_stats ? kEpiFold : (p.stats_out ? kEpiStats : kEpiPlain);
+#define HP_PAIR_LEAN(BN_, ST_)                                                                          \
+  return ep == kEpiFold ? launch_gemm_pair<BN_, ST_, kAmNone, kEpiFold>(ta, tb, p, st)                 \
+       : ep == kEpiStats ? launch_gemm_pair<BN_, ST_, kAmNone, kEpiStats>(ta, tb, p, st)               \
+                         : launch_gemm_pair<BN_, ST_, kAmNone, kEpiPlain>(ta, tb, p, st)
     switch (bn) {
-      case 320: return launch_gemm_pair<320, 5, kAmNone>(ta, tb, p, st);
-      case 256: return launch_gemm_pair<256, 6, kAmNone>(ta, tb, p, st);
-      case 160: return launch_gemm_pair<160, 7, kAmNone>(ta, tb, p, st);
-      case 128: return launch_gemm_pair<128, 8, kAmNone>(ta, tb, p, st);
-      case 64: return launch_gemm_pair<64, 8, kAmNone>(ta, tb, p, st);
+      case 320: HP_PAIR_LEAN(320, 5);
+      case 256: HP_PAIR_LEAN(256, 6);
+      case 160: HP_PAIR_LEAN(160, 7);
+      case 128: HP_PAIR_LEAN(128, 8);
+      case 64: HP_PAIR_LEAN(64, 8);
       default: return HP_ERR_UNSUPPORTED;
     }
+#undef HP_PAIR_LEAN
   }
   switch (bn) {
     case 256: return launch_gemm<256, 4>(ta, tb, p, st);
