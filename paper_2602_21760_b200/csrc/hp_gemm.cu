@@ -815,7 +815,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 // then each CTA ships the half of its accumulator it does not finalise (128 x 160
 // fp32) into its K-partner's (rank ^ 2) now idle smem ring through distributed
 // shared memory, and finalises its own half: acc + partner partial -> epilogue.
-template <int STAGES>
+template <int STAGES, int EP>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   constexpr int BN = 320, kSubN = 160;
@@ -922,7 +922,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const int et = threadIdx.x - 128;
     const int quarter = warp & 3;
     const bool any_bias = p.bias != nullptr || p.bias2 != nullptr;
-    const bool fold = p.ln_stats != nullptr;
+    const bool fold = EP == kEpiFold;
     const long long img = (long long)(m0 / p.bias2_div);
     for (int i = et; i < BN; i += 128) {
       if (any_bias) {
@@ -971,16 +971,8 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const int quarter = warp & 3;
     const float* sb = (p.bias != nullptr || p.bias2 != nullptr) ? sbias : nullptr;
     const float4* red = reinterpret_cast<const float4*>(smA);
-    if (p.ln_stats) {
-      epilogue_tile<BN, kEpiFold, kAmNone>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, scolsum, f_mean, f_rstd, h0,
-                                  kSubN, red);
-    } else if (p.stats_out) {
-      epilogue_tile<BN, kEpiStats, kAmNone>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f, h0, kSubN,
-                                   red);
-    } else {
-      epilogue_tile<BN, kEpiPlain, kAmNone>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f, h0, kSubN,
-                                   red);
-    }
+    epilogue_tile<BN, EP, kAmNone>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, scolsum, f_mean, f_rstd, h0,
+                                   kSubN, red);
   }
   __syncwarp();
   tc_fence_before();
@@ -1102,13 +1094,13 @@ int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPar
   return HP_OK;
 }
 
-template <int STAGES>
+template <int STAGES, int EP>
 int launch_gemm_splitk(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
   constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + 160 * BK * 2) + 256 + 2 * 320 * sizeof(float);
   static_assert(smem <= 227 * 1024, "split-K GEMM smem");
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_splitk_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(gemm_splitk_kernel<STAGES, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return HP_ERR_CUDA;
     attr_set = true;
@@ -1128,7 +1120,7 @@ int launch_gemm_splitk(const CUtensorMap& ta, const CUtensorMap& tb, const GemmP
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = hp_pdl_enabled() ? 2 : 1;
-  if (cudaLaunchKernelEx(&cfg, gemm_splitk_kernel<STAGES>, ta, tb, p) != cudaSuccess) return HP_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, gemm_splitk_kernel<STAGES, EP>, ta, tb, p) != cudaSuccess) return HP_ERR_CUDA;
   return HP_OK;
 }
 
@@ -1317,7 +1309,9 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
                     (d->act == HP_ACT_NONE || d->act == HP_ACT_GEGLU);
   if (pair && lean && bn == 320 && splitk_ok(d->M, d->N, d->K, d->act, p.batch, d->a_mode)) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
-    return launch_gemm_splitk<5>(ta, tb, p, st);
+    return p.ln_stats ? launch_gemm_splitk<5, kEpiFold>(ta, tb, p, st)
+         : p.stats_out ? launch_gemm_splitk<5, kEpiStats>(ta, tb, p, st)
+                       : launch_gemm_splitk<5, kEpiPlain>(ta, tb, p, st);
   }
   if (pair) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
