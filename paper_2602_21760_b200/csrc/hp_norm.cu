@@ -154,10 +154,11 @@ __device__ __forceinline__ void gn_apply_block(const bf16* __restrict__ x1, int 
     const int g = threadIdx.x % groups, k = threadIdx.x / groups;
     double a = 0.0, b = 0.0;
     if (k < per) {
-      for (int s = k; s < splits; s += per) {
-        const float* o = part + (((int64_t)n * splits + s) * groups + g) * 2;
-        a += (double)o[0];
-        b += (double)o[1];
+#pragma unroll 4
+      for (int s = k; s < splits; s += per) {               // several partials in flight
+        const float2 o = *reinterpret_cast<const float2*>(part + (((int64_t)n * splits + s) * groups + g) * 2);
+        a += (double)o.x;
+        b += (double)o.y;
       }
     }
     s_pa[threadIdx.x] = a;
