@@ -196,13 +196,13 @@ template <int BN> struct StatW { static constexpr int value = BN > 256 ? BN / 2 
 // gate and the 16-byte store fallback another 0.2 ms). "Lean" modes (no
 // activation or GEGLU; alpha 1, no column gate, 32-byte-aligned rows) carry
 // none of that; kAmAny handles everything at run time.
-constexpr int kAmNone = 0, kAmGeglu = 1, kAmAny = 3;
+constexpr int kAmNone = 0, kAmGeglu = 1, kAmGelu = 2, kAmAny = 3, kAmGate = 4;
 template <int BN, int EPI, int AM = kAmAny>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
                                               int lane, const float* sb, float* row_stats, const float* scs,
                                               float f_mean, float f_rstd, int c_begin = 0, int c_count = BN,
                                               const float4* red = nullptr) {
-  constexpr bool kLean = AM == kAmNone || AM == kAmGeglu;
+  constexpr bool kLean = AM != kAmAny;
   const bool v8 = kLean ? true : p.vec256;
   const int row = m0 + quarter * 32 + lane;
   const bool row_ok = row < p.M;
@@ -304,7 +304,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         v2[2 * q + 1] = fadd2(v2[2 * q + 1], pack2(b.z, b.w));
       }
     }
-    if constexpr (AM == kAmAny) {
+    if constexpr (AM == kAmGelu) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v2[q] = gelu_erf2(v2[q]);
+    } else if constexpr (AM == kAmAny) {
       if (p.act == HP_ACT_GELU) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) v2[q] = gelu_erf2(v2[q]);
@@ -313,7 +316,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         for (int q = 0; q < 16; ++q) v2[q] = pack2(silu_f(lo2(v2[q])), silu_f(hi2(v2[q])));
       }
     }
-    if (!kLean && p.colscale) {
+    if (AM == kAmGate || (!kLean && p.colscale)) {
       const float4* g4 = reinterpret_cast<const float4*>(p.colscale + col);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -782,8 +785,14 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       const uint32_t t_acc = tmem_base + acc * BN;
-      if constexpr (EP != kEpRuntime) {            // one epilogue flavour compiled in (batch 1)
-        epilogue_tile<BN, EP, AM>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
+      if constexpr (EP != kEpRuntime) {            // one epilogue flavour compiled in
+        GemmParams q = p;                          // batched: this tile's image
+        if (p.batch > 1) {
+          q.d += (long long)bt * p.d_bs;
+          if (q.res) q.res += (long long)bt * p.r_bs;
+          if (q.colscale) q.colscale += (long long)bt * p.cs_bs;
+        }
+        epilogue_tile<BN, EP, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
       } else if (p.batch > 1) {
         GemmParams q = p;
         q.d += (long long)bt * p.d_bs;
@@ -1307,6 +1316,10 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   // lean epilogue: no activation code, alpha 1, no column gate, 32-byte rows, no probe
   const bool lean = p.alpha == 1.0f && !p.colscale && p.vec256 && p.probe_noepi == 0 && p.batch == 1 &&
                     (d->act == HP_ACT_NONE || d->act == HP_ACT_GEGLU);
+  // lean batched / gated / GELU instances (the MMDiT's joint blocks): plain epilogue flavour
+  const bool lean2 = p.alpha == 1.0f && p.vec256 && p.probe_noepi == 0 && !p.ln_stats && !p.stats_out &&
+                     !p.ln_mode && (bn == 256 || bn == 128 || bn == 64) &&
+                     ((d->act == HP_ACT_GELU && !p.colscale) || (d->act == HP_ACT_NONE && (p.colscale || p.batch > 1)));
   if (pair && lean && bn == 320 && splitk_ok(d->M, d->N, d->K, d->act, p.batch, d->a_mode)) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
     return p.ln_stats ? launch_gemm_splitk<5, kEpiFold>(ta, tb, p, st)
@@ -1324,6 +1337,21 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
                            : launch_gemm_pair<128, 8, kAmGeglu, kEpiPlain>(ta, tb, p, st);
         default: return HP_ERR_UNSUPPORTED;
       }
+    }
+    if (lean2 && pair) {
+      const bool gelu = d->act == HP_ACT_GELU;
+      const bool gate = p.colscale != nullptr;
+#define HP_PAIR_LEAN2(BN_, ST_)                                                                         \
+  return gelu ? launch_gemm_pair<BN_, ST_, kAmGelu, kEpiPlain>(ta, tb, p, st)                          \
+       : gate ? launch_gemm_pair<BN_, ST_, kAmGate, kEpiPlain>(ta, tb, p, st)                          \
+              : launch_gemm_pair<BN_, ST_, kAmNone, kEpiPlain>(ta, tb, p, st)
+      switch (bn) {
+        case 256: HP_PAIR_LEAN2(256, 6);
+        case 128: HP_PAIR_LEAN2(128, 8);
+        case 64: HP_PAIR_LEAN2(64, 8);
+        default: break;
+      }
+#undef HP_PAIR_LEAN2
     }
     if (!lean || d->act != HP_ACT_NONE) {
       switch (bn) {
