@@ -12,7 +12,7 @@
 // Softmax (per row, fp32, log2 domain): one TMEM pass over S, block max, lazy
 // rescale of O in TMEM only when the running max grows by more than 2^8
 // (otherwise the stale max is kept: p <= 2^8, exact after the final 1/l), and
-// exp2 split between MUFU.EX2 and a degree-4 polynomial on the FMA pipe (P is
+// exp2 split between MUFU.EX2 and a degree-3 polynomial on the FMA pipe (P is
 // rounded to bf16 anyway). P goes to shared memory as the SW128 K-major A
 // operand of the PV MMA; V is consumed MN-major straight from its TMA tile.
 //
@@ -58,20 +58,6 @@ struct AttnParams {
   float scale_log2;
   int n_kv;
 };
-
-__device__ __forceinline__ float exp2_poly(float x) {
-  // 2^x for x <= 0 on the FMA pipe: x = i + f, f in [-0.5, 0.5], 2^f by a degree-4 polynomial
-  x = fmaxf(x, -126.0f);
-  const float t = x + 12582912.0f;                   // 1.5 * 2^23: round to integer in the mantissa
-  const float fi = t - 12582912.0f;
-  const int i = __float_as_int(t) - 0x4B400000;
-  const float f = x - fi;
-  float p = fmaf(0.0096181291f, f, 0.0555041087f);
-  p = fmaf(p, f, 0.2402265070f);
-  p = fmaf(p, f, 0.6931471806f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (i << 23));
-}
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
