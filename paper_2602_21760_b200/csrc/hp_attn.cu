@@ -128,7 +128,7 @@ template <int MODE> struct AttnCfg {
                                           : (size_t)kTileBytes * (kNq + 2 * kSt) + kNq * kPBytes + 256;
 };
 
-template <int MODE>
+template <int MODE, bool MASK>     // MASK: some key block is partial (or causal)
 __global__ void __launch_bounds__(AttnCfg<MODE>::kThr, AttnCfg<MODE>::kMinBlocks)
 attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
             const __grid_constant__ CUtensorMap tmV, AttnParams p) {
@@ -265,7 +265,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_s + c * 32, r);
         tmem_ld_wait();
-        if (valid < kBK) {
+        if (MASK && valid < kBK) {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
@@ -312,7 +312,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_s + c * 32, r);
         tmem_ld_wait();
-        if (valid < kBK) {
+        if (MASK && valid < kBK) {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
@@ -383,6 +383,7 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 // identically whatever else is in the batch.
 constexpr int kStSplit = 2;
 
+template <bool MASK>             // MASK: S_kv is not a multiple of the 128-key block
 __global__ void __launch_bounds__(kThreads, 1)
 attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, AttnParams p) {
@@ -504,7 +505,7 @@ attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_s + c * 32, r);
         tmem_ld_wait();
-        if (valid < kBK) {
+        if (MASK && valid < kBK) {
 #pragma unroll
           for (int e = 0; e < 32; ++e)
             if (c * 32 + e >= valid) r[e] = __float_as_uint(-INFINITY);
@@ -540,7 +541,7 @@ attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_s + c * 32, r);
         tmem_ld_wait();
-        if (valid < kBK) {
+        if (MASK && valid < kBK) {
 #pragma unroll
           for (int e = 0; e < 32; ++e)
             if (c * 32 + e >= valid) r[e] = __float_as_uint(-INFINITY);
@@ -638,18 +639,19 @@ bool map3(CUtensorMap* m, const void* base, long long ld, int rows, int batch) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE>
+template <int MODE, bool MASK>
 int launch_attn(dim3 grid, cudaStream_t st, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                 const AttnParams& p, size_t slack) {
   const size_t smem = AttnCfg<MODE>::kSmem + slack;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(attn_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(attn_kernel<MODE, MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return HP_ERR_CUDA;
     attr = true;
   }
-  return hp_launch_pdl(attn_kernel<MODE>, grid, dim3(AttnCfg<MODE>::kThr), smem, st, tq, tk, tv, p) == cudaSuccess
+  return hp_launch_pdl(attn_kernel<MODE, MASK>, grid, dim3(AttnCfg<MODE>::kThr), smem, st, tq, tk, tv, p) ==
+                 cudaSuccess
              ? HP_OK : HP_ERR_CUDA;
 }
 
@@ -705,7 +707,8 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   p.n_kv = (d->skv + kBK - 1) / kBK;
   dim3 grid((d->sq + 2 * kBQ - 1) / (2 * kBQ), d->heads, d->batch);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p.n_kv == 1) return launch_attn<kModeSingle>(grid, st, tq, tk, tv, p, 1024);
+  if (p.n_kv == 1) return launch_attn<kModeSingle, true>(grid, st, tq, tk, tv, p, 1024);
+  const bool mask = (d->skv % kBK) != 0;
   // one query tile per CTA when the two-tile grid would leave a short last wave
   const int pair_ctas = grid.x * grid.y * grid.z;
   const int sms = num_sms_attn();
@@ -714,18 +717,22 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
     constexpr size_t smem = 1024 + (size_t)kTileBytes * (1 + 4 * kStSplit) + 2 * kPBytes + 256 + 4 * kBQ * 4;
     static bool attr_s = false;
     if (!attr_s) {
-      if (cudaFuncSetAttribute(attn_splitkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
+      if (cudaFuncSetAttribute(attn_splitkv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+              cudaSuccess ||
+          cudaFuncSetAttribute(attn_splitkv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+              cudaSuccess)
         return HP_ERR_CUDA;
       attr_s = true;
     }
     dim3 g1((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
-    return hp_launch_pdl(attn_splitkv_kernel, g1, dim3(kThreads), smem, st, tq, tk, tv, p) == cudaSuccess
-               ? HP_OK : HP_ERR_CUDA;
+    const auto kern = (d->skv % kBK) ? attn_splitkv_kernel<true> : attn_splitkv_kernel<false>;
+    return hp_launch_pdl(kern, g1, dim3(kThreads), smem, st, tq, tk, tv, p) == cudaSuccess ? HP_OK : HP_ERR_CUDA;
   }
   if (solo_enabled() && tail != 0 && tail * 2 < sms) {
     dim3 g1((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
-    return launch_attn<kModeSolo>(g1, st, tq, tk, tv, p, 0);
+    return mask ? launch_attn<kModeSolo, true>(g1, st, tq, tk, tv, p, 0)
+                : launch_attn<kModeSolo, false>(g1, st, tq, tk, tv, p, 0);
   }
-  return launch_attn<kModePair>(grid, st, tq, tk, tv, p, 1024);
+  return mask ? launch_attn<kModePair, true>(grid, st, tq, tk, tv, p, 1024)
+              : launch_attn<kModePair, false>(grid, st, tq, tk, tv, p, 1024);
 }
