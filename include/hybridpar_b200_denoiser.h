@@ -149,7 +149,8 @@ int hp_conv3x3_small(const void* x, int32_t n, int32_t h, int32_t w, int32_t cin
 int hp_timestep_embedding(const float* t, int32_t b, int32_t dim, float max_period, float* out,
                           void* stream);
 /* small-M linear for embeddings: y[M, N] = act_out(act_in(x)[M, K] W[N, K]^T + bias), fp32 io,
- * bf16 weights; act_* in {HP_ACT_NONE, HP_ACT_SILU}                         */
+ * bf16 weights; act_* in {HP_ACT_NONE, HP_ACT_SILU}; M <= 8, K % 8 == 0,
+ * M * K <= 40960 (x is staged in shared memory, act_in applied once)       */
 int hp_linear_small(const float* x, int32_t M, int32_t K, const void* w, const float* bias,
                     int32_t N, int32_t act_in, int32_t act_out, float* y, void* stream);
 /* patchify (inverse = 0): NHWC latent [n,h,w,c] -> tokens [n, (h/p)(w/p), p*p*c]

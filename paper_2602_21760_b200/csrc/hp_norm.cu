@@ -116,10 +116,22 @@ __device__ __forceinline__ void gn_stats_block(const bf16* __restrict__ x1, int 
     }
     __syncthreads();
   }
+  // per-group sums: `per` threads per group over strided channels, then one thread per
+  // group folds them in fixed order (p_sum / p_sq are free again here)
   const int cg = C / groups;
+  const int per = kGnThreads / groups;
+  {
+    const int g = threadIdx.x / per, k = threadIdx.x % per;
+    float a = 0.f, b = 0.f;
+    if (g < groups)
+      for (int c = g * cg + k; c < (g + 1) * cg; c += per) { a += s_sum[c]; b += s_sq[c]; }
+    p_sum[threadIdx.x] = a;
+    p_sq[threadIdx.x] = b;
+  }
+  __syncthreads();
   for (int g = threadIdx.x; g < groups; g += kGnThreads) {
     float a = 0.f, b = 0.f;
-    for (int c = g * cg; c < (g + 1) * cg; ++c) { a += s_sum[c]; b += s_sq[c]; }
+    for (int k = 0; k < per; ++k) { a += p_sum[g * per + k]; b += p_sq[g * per + k]; }
     float* o = part + (((int64_t)n * splits + split) * groups + g) * 2;
     o[0] = a;
     o[1] = b;
@@ -149,14 +161,23 @@ __device__ __forceinline__ void gn_apply_block(const bf16* __restrict__ x1, int 
   const int V = C / 8;
   const int cg = C / groups;
   {
-    // fold the per-split partials: kGnThreads/groups threads per group, fixed order
+    // fold the per-split partials: kGnThreads/groups threads per group, fixed order;
+    // a warp's loads cover consecutive groups of one split (coalesced), 8 in flight
     const int per = kGnThreads / groups;
     const int g = threadIdx.x % groups, k = threadIdx.x / groups;
     double a = 0.0, b = 0.0;
     if (k < per) {
-#pragma unroll 4
-      for (int s = k; s < splits; s += per) {               // several partials in flight
-        const float2 o = *reinterpret_cast<const float2*>(part + (((int64_t)n * splits + s) * groups + g) * 2);
+      const float* base = part + ((int64_t)n * splits * groups + g) * 2;
+      int s = k;
+      for (; s + 7 * per < splits; s += 8 * per) {
+        float2 o[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) o[u] = *reinterpret_cast<const float2*>(base + (int64_t)(s + u * per) * groups * 2);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { a += (double)o[u].x; b += (double)o[u].y; }
+      }
+      for (; s < splits; s += per) {
+        const float2 o = *reinterpret_cast<const float2*>(base + (int64_t)s * groups * 2);
         a += (double)o.x;
         b += (double)o.y;
       }
@@ -531,40 +552,58 @@ __global__ void timestep_emb_kernel(const float* __restrict__ t, int b, int dim,
 
 // y[m, n] = act_out(sum_k act_in(x[m, k]) * W[n, k] + bias[n]); one warp per (n), all M rows
 constexpr int kSmallMaxM = 8;
-__global__ void linear_small_kernel(const float* __restrict__ x, int M, int K, const bf16* __restrict__ w,
+__global__ void __launch_bounds__(256, 4) linear_small_kernel(const float* __restrict__ x, int M, int K, const bf16* __restrict__ w,
                                     const float* __restrict__ bias, int N, int act_in, int act_out,
                                     float* __restrict__ y) {
+  extern __shared__ __align__(16) float xs[];          // [M][K] inputs, act_in applied once per block
   pdl_wait();
   pdl_trigger();
+  for (int i = threadIdx.x; i < M * K; i += blockDim.x) {
+    const float v = x[i];
+    xs[i] = act_in == HP_ACT_SILU ? silu(v) : v;
+  }
+  __syncthreads();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int n = warp; n < N; n += nwarps) {
     float acc[kSmallMaxM] = {0};
     const bf16* wr = w + (int64_t)n * K;
-    // four 16-byte weight loads in flight per lane (the GEMV is weight-bandwidth bound)
-    for (int k0 = lane * 8; k0 < K; k0 += 4 * 256) {
-      float wv[4][8];
+    // up to eight 16-byte weight loads in flight per lane (kept packed: 4 registers each):
+    // a K <= 2048 row is one round trip
+    for (int k0 = lane * 8; k0 < K; k0 += 8 * 256) {
+      uint4 wq[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (k0 + u * 256 < K) load8(wr + k0 + u * 256, wv[u]);
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u * 256 < K) wq[u] = *reinterpret_cast<const uint4*>(wr + k0 + u * 256);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int k = k0 + u * 256;
         if (k >= K) break;
-        for (int m = 0; m < M; ++m) {
-          const float* xr = x + (int64_t)m * K + k;
-          float a = acc[m];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&wq[u]);
+        float wv[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float xv = xr[i];
-            if (act_in == HP_ACT_SILU) xv = silu(xv);
-            a = fmaf(xv, wv[u][i], a);
-          }
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          wv[2 * i] = f.x;
+          wv[2 * i + 1] = f.y;
+        }
+#pragma unroll
+        for (int m = 0; m < kSmallMaxM; ++m) {
+          if (m >= M) break;
+          const float4 a0 = *reinterpret_cast<const float4*>(xs + m * K + k);
+          const float4 a1 = *reinterpret_cast<const float4*>(xs + m * K + k + 4);
+          float a = acc[m];
+          a = fmaf(a0.x, wv[0], a); a = fmaf(a0.y, wv[1], a);
+          a = fmaf(a0.z, wv[2], a); a = fmaf(a0.w, wv[3], a);
+          a = fmaf(a1.x, wv[4], a); a = fmaf(a1.y, wv[5], a);
+          a = fmaf(a1.z, wv[6], a); a = fmaf(a1.w, wv[7], a);
           acc[m] = a;
         }
       }
     }
-    for (int m = 0; m < M; ++m) {
+#pragma unroll
+    for (int m = 0; m < kSmallMaxM; ++m) {
+      if (m >= M) break;
       float r = hp_warp_sum_f(acc[m]);
       if (lane == 0) {
         r += bias ? bias[n] : 0.f;
@@ -930,8 +969,18 @@ int hp_linear_small(const float* x, int32_t M, int32_t K, const void* w, const f
                     int32_t act_in, int32_t act_out, float* y, void* stream) {
   if (!x || !w || !y) return HP_ERR_PARAMETER;
   if (M < 1 || M > kSmallMaxM || K % 8) return HP_ERR_SHAPE;
-  hp_launch_pdl(linear_small_kernel, dim3(nblocks((int64_t)N * 32, 256, 148 * 8)), dim3(256), 0, static_cast<cudaStream_t>(stream), 
-      x, M, K, static_cast<const bf16*>(w), bias, N, act_in, act_out, y);
+  const size_t smem = (size_t)M * K * sizeof(float);
+  constexpr size_t kMaxSmem = 160 * 1024;
+  if (smem > kMaxSmem) return HP_ERR_SHAPE;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(linear_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem) !=
+        cudaSuccess)
+      return HP_ERR_CUDA;
+    attr = true;
+  }
+  hp_launch_pdl(linear_small_kernel, dim3(nblocks((int64_t)N * 32, 256, 148 * 8)), dim3(256), smem,
+                static_cast<cudaStream_t>(stream), x, M, K, static_cast<const bf16*>(w), bias, N, act_in, act_out, y);
   if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }

@@ -1,1 +1,8 @@
-for v in "" var_nomask "" var_nomask; do echo "== ${v:-current}"; for a in "4096 10 20" "1024 20 50"; do HP_LIB_VARIANT=$v python tools/prof_attn.py $a; done; done
+# A/B: in-tree lib vs lib/$VAR.so (HP_LIB_VARIANT) on the U-Net / SD3 forward and GroupNorm shapes
+VAR=${VAR:-var_gn}
+for v in "" $VAR "" $VAR; do
+  echo "== ${v:-current}"
+  HP_LIB_VARIANT=$v python tools/time_unet.py | grep forward
+  HP_LIB_VARIANT=$v timeout 120 python tools/gn_probe.py
+done
+

@@ -18,3 +18,10 @@ for hw, c, c2 in [(16384, 320, 0), (4096, 640, 0), (1024, 1280, 0), (1024, 1280,
                     reps=20)
     mb = n * hw * (c + c2) * 2 * 3 / 1e6
     print(f"GN n={n} hw={hw} c={c}+{c2}: {us:.1f} us, {mb / us * 1e-3 * 1e3:.2f} TB/s (3 passes of {mb / 3:.1f} MB)")
+
+# the per-step embedding GEMV (all resnets' time-embedding projections in one launch)
+xe = torch.randn(2, 1280, device="cuda")
+we = (torch.randn(13824, 1280, device="cuda") * 0.03).bfloat16()
+ye = torch.empty(2, 13824, device="cuda")
+us = graph_time(lambda: K.linear_small(xe, we, None, act_in=K.ACT_SILU, out=ye), reps=20)
+print(f"linear_small 2x1280 -> 13824 (silu in): {us:.1f} us, {we.numel() * 2 / us / 1e6:.2f} TB/s")
