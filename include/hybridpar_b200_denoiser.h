@@ -25,6 +25,13 @@ extern "C" {
 #define HP_A_PLAIN        0   /* A is [M, K] row-major (lda elements)            */
 #define HP_A_CONV3X3      1   /* A is NHWC [n, h, w, c]; K = 9*c; pad 1, stride 1  */
 #define HP_A_CONV3X3_S2   2   /* same, stride 2 (output h/2 x w/2)                 */
+/* HP_A_UPCONV: nearest 2x upsample then 3x3 conv (pad 1), computed as four
+ * sub-pixel 2x2 convs on the LOW-res NHWC input [n, h, w, c] (one per output
+ * phase (py, px), all in one launch): b = [4 * N, 4 * c], phase-major, tap
+ * (ty, tx) of a phase = the sum of the 3x3 taps that read the same input
+ * pixel; K = 4 * c; M = n * h * w; d = the 2x output [n, 2h, 2w, N] with row
+ * stride ldd. 16 instead of 36 taps of MMA work per output pixel.          */
+#define HP_A_UPCONV       3
 
 #define HP_ACT_NONE   0
 #define HP_ACT_GELU   1       /* exact erf GELU                                     */

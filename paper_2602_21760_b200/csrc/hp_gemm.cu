@@ -60,6 +60,11 @@ struct GemmParams {
   const float* colscale;
   int batch;                       // >= 1; plain mode only
   long long a_bs, d_bs, r_bs, cs_bs;  // element strides between batches
+  // HP_A_UPCONV: batch index = output phase (py, px) = (bt >> 1, bt & 1), D offset
+  // py * d_bs + px * d_bs2; rows map to the 2x grid: row = q * row_w + j ->
+  // q * ld_hi + j * ldd (row_w = 0: ordinary rows)
+  long long d_bs2, ld_hi;
+  int row_w;
   // LayerNorm folding: producer writes per-(row, N tile) (mean, M2); consumer folds
   bool vec256;                     // output (and residual) rows 32-byte aligned: 256-bit accesses
   float2* stats_out;
@@ -187,6 +192,23 @@ __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)
 // each CTA finalises one half, writes the same layout).
 template <int BN> struct StatW { static constexpr int value = BN > 256 ? BN / 2 : BN; };
 
+// element offset of output row `row` (once per thread and tile, not per element)
+__device__ __forceinline__ long long d_row_off(const GemmParams& p, int row) {
+  if (p.row_w == 0) return (long long)row * p.ldd;
+  const int q = row / p.row_w;
+  return (long long)q * p.ld_hi + (long long)(row - q * p.row_w) * p.ldd;
+}
+// the per-batch (per-phase) operand offsets of batch index bt
+__device__ __forceinline__ void batch_offsets(GemmParams& q, int bt) {
+  if (q.mode == HP_A_UPCONV) {
+    q.d += (long long)(bt >> 1) * q.d_bs + (long long)(bt & 1) * q.d_bs2;
+    return;
+  }
+  q.d += (long long)bt * q.d_bs;
+  if (q.res) q.res += (long long)bt * q.r_bs;
+  if (q.colscale) q.colscale += (long long)bt * q.cs_bs;
+}
+
 // Epilogue columns [c_begin, c_begin + c_count) of one 128 x BN tile (default: all);
 // `red` (split-K) holds the other K half's fp32 partial for these columns in shared
 // memory, laid out [column / 4][128 rows][4].
@@ -242,7 +264,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         const uint64_t o2 = fmul2(a2, gelu_erf2(g2));
         packed[j / 2] = pack_bf16(lo2(o2), hi2(o2));
       }
-      if (kLean || p.probe_noepi != 2) st_row64(p.d + (long long)row * p.ldd + ocol, packed, v8);
+      if (kLean || p.probe_noepi != 2) st_row64(p.d + d_row_off(p, row) + ocol, packed, v8);
       else if (packed[0] == 0x7fc07fc0u) p.d[row] = __float2bfloat16(0.f);   // keep the math live
     }
     return;
@@ -254,6 +276,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
   float st_sum = 0.f, st_sq = 0.f;            // LayerNorm partials of the stored (bf16) row
   float sh_k = 0.f, sh_s1 = 0.f, sh_s2 = 0.f;   // stats_out: sums shifted by the segment's first value
   if (has_res) ld_row64(res_row, rn, v8);
+  const long long drow = d_row_off(p, row);
   const int nch = c_count / 32;
 #pragma unroll 1
   for (int cc = 0; cc < nch; ++cc) {
@@ -335,7 +358,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     uint32_t w[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) w[q] = pack_bf16(lo2(v2[q]), hi2(v2[q]));
-    if (kLean || p.probe_noepi != 2) st_row64(p.d + (long long)row * p.ldd + col, w, v8);
+    if (kLean || p.probe_noepi != 2) st_row64(p.d + drow + col, w, v8);
     else if (w[0] == 0x7fc07fc0u) p.d[row] = __float2bfloat16(0.f);          // keep the math live
     if constexpr (EPI == kEpiStats) {
       if ((c * 32) % kStatW == 0) sh_k = unpack_bf16(w[0]).x;
@@ -695,7 +718,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           y0 = rem / p.out_w;
           x0 = rem - y0 * p.out_w;
         }
-        const int nb = n0 + (int)rank * (kSubN / 2);
+        const int nb = n0 + (int)rank * (kSubN / 2) + (p.mode == HP_A_UPCONV ? bt * p.N : 0);
         for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -709,8 +732,15 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           } else {
             const int tap = kb / p.cin_blocks;
             const int cb = kb - tap * p.cin_blocks;
-            const int dy = tap / 3, dx = tap - dy * 3;
-            if (p.mode == HP_A_CONV3X3) {
+            int dy, dx;
+            if (p.mode == HP_A_UPCONV) {           // 2x2 taps shifted by the output phase
+              dy = (tap >> 1) + (bt >> 1);
+              dx = (tap & 1) + (bt & 1);
+            } else {
+              dy = tap / 3;
+              dx = tap - dy * 3;
+            }
+            if (p.mode != HP_A_CONV3X3_S2) {
               tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, x0 + dx - 1, y0 + dy - 1, img);
             } else {
               tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, 2 * x0 + dx - 1, 2 * y0 + dy - 1, img);
@@ -786,18 +816,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc_fence_after();
       const uint32_t t_acc = tmem_base + acc * BN;
       if constexpr (EP != kEpRuntime) {            // one epilogue flavour compiled in
-        GemmParams q = p;                          // batched: this tile's image
-        if (p.batch > 1) {
-          q.d += (long long)bt * p.d_bs;
-          if (q.res) q.res += (long long)bt * p.r_bs;
-          if (q.colscale) q.colscale += (long long)bt * p.cs_bs;
-        }
+        GemmParams q = p;                          // batched: this tile's image (or phase)
+        if (p.batch > 1) batch_offsets(q, bt);
         epilogue_tile<BN, EP, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
       } else if (p.batch > 1) {
         GemmParams q = p;
-        q.d += (long long)bt * p.d_bs;
-        if (q.res) q.res += (long long)bt * p.r_bs;
-        if (q.colscale) q.colscale += (long long)bt * p.cs_bs;
+        batch_offsets(q, bt);
         epilogue_tile<BN, kEpiPlain, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       } else if (fold) {
         epilogue_tile<BN, kEpiFold, AM>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
@@ -1209,8 +1233,9 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   if ((d->K % 8) || (d->ldb % 8)) return HP_ERR_UNSUPPORTED;   // 16-byte TMA strides
   if ((reinterpret_cast<uintptr_t>(d->a) | reinterpret_cast<uintptr_t>(d->b)) & 15) return HP_ERR_UNSUPPORTED;
   num_sms();
-  const int bn = d->block_n ? d->block_n
-                            : pick_bn(d->M * (d->batch > 1 ? d->batch : 1), d->N, d->K, d->act, d->batch, d->a_mode);
+  const bool upconv = d->a_mode == HP_A_UPCONV;
+  const int nbatch = upconv ? 4 : (d->batch > 1 ? d->batch : 1);
+  const int bn = d->block_n ? d->block_n : pick_bn(d->M * nbatch, d->N, d->K, d->act, nbatch, d->a_mode);
   if (bn == 0 || d->N % bn) return HP_ERR_UNSUPPORTED;
   if (d->act == HP_ACT_GEGLU && (bn % 64)) return HP_ERR_UNSUPPORTED;
   const int64_t n_out = d->act == HP_ACT_GEGLU ? d->N / 2 : d->N;
@@ -1230,7 +1255,10 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   p.colscale = d->colscale;
   if (d->colscale && (reinterpret_cast<uintptr_t>(d->colscale) & 15)) return HP_ERR_UNSUPPORTED;
   p.alpha = d->alpha == 0.0f ? 1.0f : d->alpha;
-  p.batch = d->batch > 1 ? d->batch : 1;
+  p.batch = nbatch;
+  if (upconv && (d->batch > 1 || d->residual || d->colscale || d->bias2 || d->ln_y || d->stats_out ||
+                 d->ln_stats || d->act == HP_ACT_GEGLU || d->M <= BM || !pair_enabled()))
+    return HP_ERR_UNSUPPORTED;
   p.ln_mode = d->ln_y != nullptr;
   p.ln_g = d->ln_gamma; p.ln_b = d->ln_beta; p.ln_eps = d->ln_eps;
   p.ln_y = static_cast<__nv_bfloat16*>(d->ln_y); p.ldy = d->ldy;
@@ -1239,7 +1267,7 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
     return HP_ERR_UNSUPPORTED;
   p.vec256 = ((d->ldd % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->d) & 31) == 0) &&
              (!d->residual || (((d->ldr % 16) == 0) && ((reinterpret_cast<uintptr_t>(d->residual) & 31) == 0))) &&
-             (p.batch <= 1 || (((d->d_bstride | d->r_bstride) % 16) == 0));
+             (p.batch <= 1 || upconv || (((d->d_bstride | d->r_bstride) % 16) == 0));
   // development probes, read once: HP_GEMM_PROBE_NOEPI=1 skips the plain epilogue, =2 only
   // its stores (isolates the main loop); HP_GEMM_RASTER_N=1 walks N tiles fastest
   static const int probe = [] {
@@ -1263,7 +1291,15 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
       return HP_ERR_UNSUPPORTED;
   }
   p.a_bs = d->a_bstride; p.d_bs = d->d_bstride; p.r_bs = d->r_bstride; p.cs_bs = d->cs_bstride;
-  if (p.batch > 1 && d->a_mode != HP_A_PLAIN) return HP_ERR_UNSUPPORTED;
+  if (upconv) {      // output phases (py, px) of the 2x grid: see HP_A_UPCONV
+    p.ldd = 2 * d->ldd;
+    p.row_w = d->img_w;
+    p.ld_hi = 4LL * d->img_w * d->ldd;
+    p.d_bs = 2LL * d->img_w * d->ldd;
+    p.d_bs2 = d->ldd;
+    p.a_bs = p.r_bs = p.cs_bs = 0;
+  }
+  if (p.batch > 1 && d->a_mode != HP_A_PLAIN && !upconv) return HP_ERR_UNSUPPORTED;
   if (p.batch > 1 && ((p.a_bs | p.d_bs | p.r_bs) % 8 || p.cs_bs % 4)) return HP_ERR_UNSUPPORTED;
   p.num_m_tiles = (int)((d->M + BM - 1) / BM);
   p.num_n_tiles = (int)(d->N / bn);
@@ -1284,10 +1320,10 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
       const uint32_t box[2] = {BK, BM};
       if (!make_map(&ta, d->a, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;
     }
-  } else if (d->a_mode == HP_A_CONV3X3 || d->a_mode == HP_A_CONV3X3_S2) {
+  } else if (d->a_mode == HP_A_CONV3X3 || d->a_mode == HP_A_CONV3X3_S2 || upconv) {
     const int s = d->a_mode == HP_A_CONV3X3_S2 ? 2 : 1;
     const int c = d->img_c;
-    if (c % BK || d->K != 9LL * c) return HP_ERR_SHAPE;
+    if (c % BK || d->K != (upconv ? 4LL : 9LL) * c) return HP_ERR_SHAPE;
     p.out_h = d->img_h / s;
     p.out_w = d->img_w / s;
     if ((int64_t)d->img_n * p.out_h * p.out_w != d->M) return HP_ERR_SHAPE;
@@ -1295,7 +1331,7 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
     p.box_h = BM / p.box_w;
     if (BM % p.box_w || p.out_w % p.box_w || p.out_h % p.box_h) return HP_ERR_UNSUPPORTED;
     p.cin_blocks = c / BK;
-    p.num_kb = 9 * p.cin_blocks;
+    p.num_kb = (upconv ? 4 : 9) * p.cin_blocks;
     const uint64_t dims[4] = {(uint64_t)c, (uint64_t)d->img_w, (uint64_t)d->img_h, (uint64_t)d->img_n};
     const uint64_t str[3] = {(uint64_t)c * 2, (uint64_t)d->img_w * c * 2, (uint64_t)d->img_h * d->img_w * c * 2};
     const uint32_t box[4] = {BK, (uint32_t)(p.box_w * s), (uint32_t)(p.box_h * s), 1};
@@ -1307,7 +1343,7 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   // CTA pairs for every GEMM with more than one 128-row block (not the cluster-LN mode)
   const bool pair = pair_enabled() && !p.ln_mode && d->M > BM;
   {
-    const uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)d->N};
+    const uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)d->N * (upconv ? 4 : 1)};   // upconv: 4 phases
     const uint64_t str[1] = {(uint64_t)d->ldb * 2};
     const uint32_t box[2] = {BK, (uint32_t)(pair ? (bn > 256 ? bn / 4 : bn / 2) : bn)};
     if (!make_map(&tb, d->b, 2, dims, str, box, nullptr)) return HP_ERR_CUDA;

@@ -28,7 +28,7 @@ def check(rc, what):
 
 _VP, _I32, _I64, _F32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
 
-HP_A_PLAIN, HP_A_CONV3X3, HP_A_CONV3X3_S2 = 0, 1, 2
+HP_A_PLAIN, HP_A_CONV3X3, HP_A_CONV3X3_S2, HP_A_UPCONV = 0, 1, 2, 3
 ACT_NONE, ACT_GELU, ACT_SILU, ACT_GEGLU = 0, 1, 2, 3
 
 
@@ -274,6 +274,55 @@ def silu(x, out=None):
     lib = N.load()
     out = torch.empty_like(x) if out is None else out
     check(lib.hp_silu(_p(x), _p(out), x.numel(), _s()), "hp_silu")
+    return out
+
+
+# sub-pixel decomposition of nearest-2x upsample + 3x3 conv: for output phase p (row or
+# column parity) the 2x2 taps t = 0, 1 read input offsets p - 1 + t, and collect the 3x3
+# taps k that land on the same input pixel
+_UP_TAPS = {0: ((0,), (1, 2)), 1: ((0, 1), (2,))}
+
+
+def upconv_weights(w3):
+    """3x3 conv weights [co, 3, 3, ci] (any float dtype) -> the HP_A_UPCONV operand
+    [4 * co, 4 * ci] bf16: phase-major (py, px), then tap (ty, tx), channel-minor."""
+    w3 = w3.float()
+    co, _, _, ci = w3.shape
+    ph = []
+    for py in (0, 1):
+        for px in (0, 1):
+            taps = []
+            for ty in (0, 1):
+                for tx in (0, 1):
+                    t = torch.zeros(co, ci, device=w3.device)
+                    for ky in _UP_TAPS[py][ty]:
+                        for kx in _UP_TAPS[px][tx]:
+                            t = t + w3[:, ky, kx, :]
+                    taps.append(t)
+            ph.append(torch.stack(taps, dim=1).reshape(co, 4 * ci))
+    return torch.cat(ph, dim=0).to(torch.bfloat16).contiguous()
+
+
+def upsample_conv(x, n, h, w, c, w4, bias=None, out=None):
+    """conv3x3(nearest_upsample_2x(x)) in one tensor-core launch (HP_A_UPCONV):
+    x [n*h*w, c] NHWC low-res, w4 = upconv_weights(...) -> [n*2h*2w, co]."""
+    lib = N.load()
+    _bf16(x, "A")
+    _bf16(w4, "W")
+    co = w4.shape[0] // 4
+    if w4.shape[1] != 4 * c:
+        raise ShapeError(f"upconv weight K={w4.shape[1]} != 4*{c}")
+    if out is None:
+        out = torch.empty((n * 4 * h * w, co), dtype=torch.bfloat16, device=x.device)
+    d = HpGemmDesc()
+    d.a, d.lda, d.a_mode = _p(x), c, HP_A_UPCONV
+    d.img_n, d.img_h, d.img_w, d.img_c = n, h, w, c
+    d.b, d.ldb = _p(w4), w4.stride(0)
+    d.d, d.ldd = _p(out), out.stride(0)
+    d.M, d.N, d.K = n * h * w, co, 4 * c
+    d.bias = _p(bias)
+    d.alpha = 1.0
+    check(lib.hp_gemm(C.byref(d), _s()), f"hp_gemm upconv n={n} {h}x{w} {c}->{co}")
     return out
 
 

@@ -62,6 +62,21 @@ class _Conv:
         return K.gemm(x, self.w, bias=self.b, conv=(n, h, w, self.ci, stride), **kw)
 
 
+class _UpConv(_Conv):
+    """Upsampler: nearest 2x then 3x3 conv, as one sub-pixel launch (HP_A_UPCONV:
+    16 instead of 36 taps of MMA work per output pixel; no upsampled tensor)."""
+
+    def __init__(self, W, name, dev="cuda"):
+        super().__init__(W, name, dev)
+        self.w4 = K.upconv_weights(W[name + ".weight"].to(dev).permute(0, 2, 3, 1))
+
+    def up(self, x, n, h, w):
+        """x: [n*h*w, ci] low-res -> [n*2h*2w, co]"""
+        if n * h * w > 128:                    # CTA-pair kernel (M > 128 rows)
+            return K.upsample_conv(x, n, h, w, self.ci, self.w4, self.b)
+        return self(K.upsample2x(x, n, h, w, self.ci), n, 2 * h, 2 * w)
+
+
 class _Norm:
     def __init__(self, W, name, dev="cuda"):
         self.g = _f32(W[name + ".weight"].to(dev))
@@ -187,7 +202,7 @@ class UNet:
             res = [_ResBlock(W, f"up_blocks.{u}.resnets.{j}", s.temb_dim, dev) for j in range(s.layers_per_block + 1)]
             att = [(_Transformer(W, f"up_blocks.{u}.attentions.{j}", co, s.transformer_depth[lvl], s.head_dim, dev)
                     if s.transformer_depth[lvl] else None) for j in range(s.layers_per_block + 1)]
-            us = _Conv(W, f"up_blocks.{u}.upsamplers.0.conv", dev) if u < len(ch) - 1 else None
+            us = _UpConv(W, f"up_blocks.{u}.upsamplers.0.conv", dev) if u < len(ch) - 1 else None
             self.up.append((res, att, us))
         self.norm_out = _Norm(W, "conv_norm_out", dev)
         wo = W["conv_out.weight"].to(dev)                                  # [4, 320, 3, 3]
@@ -286,9 +301,8 @@ class UNet:
                 if a is not None:
                     h = a(h, n, hh * ww, g, st, self.ctx_len, key, rs)
             if us is not None:
-                h = K.upsample2x(h, n, hh, ww, h.shape[1])
+                h = us.up(h, n, hh, ww)
                 hh, ww = hh * 2, ww * 2
-                h = us(h, n, hh, ww)
         y = K.group_norm(h, n, hh * ww, s.block_out[0], self.norm_out.g, self.norm_out.b, groups=g, silu=True, stats=st)
         e64 = K.gemm(y, self.conv_out_w, bias=self.conv_out_b, conv=(n, hh, ww, s.block_out[0], 1))
         eps = K.copy_cols(e64, s.out_channels)
@@ -353,6 +367,6 @@ def unet_flops(spec: UNetSpec, n: int) -> float:
                 fl += tr(hw, co, s.transformer_depth[lvl])
         if u < len(ch) - 1:
             hw *= 4
-            fl += conv(hw, co, co)
+            fl += conv(hw, co, co) * 4 / 9        # upsampler: sub-pixel, 4 of the 9 taps (HP_A_UPCONV)
     fl += 2.0 * n * H * H * ch[0] * s.out_channels * 9
     return fl

@@ -8,7 +8,8 @@ restatement ``oracle/vae_ref.py`` of the same architecture and weights.
 Layout and kernels are the U-Net's: NHWC bf16 activations, 3x3 convolutions as
 tensor-core implicit GEMMs (the 4 latent channels and the 3 pixel channels are
 zero-padded to 64 by ``copy_cols``), GroupNorm(+SiLU) single-launch kernels,
-nearest 2x upsampling. The mid-block attention is one head of width 512 over
+nearest-2x upsampling fused with the following 3x3 conv (four sub-pixel 2x2
+convs in one launch, ``kernels.upsample_conv``). The mid-block attention is one head of width 512 over
 all (h*w) latent positions; it runs as Q K^T (GEMM, bf16 scores) -> row
 softmax -> P V (GEMM against V^T, which a GEMM produces directly as
 W_v . x^T; the V bias folds into the output projection because softmax rows
@@ -122,7 +123,10 @@ class VAEDecoder:
         self.up = []
         for u in range(len(rev)):
             res = [_Resnet(W, f"decoder.up_blocks.{u}.resnets.{j}", dev) for j in range(s.layers_per_block + 1)]
-            us = _Conv(W, f"decoder.up_blocks.{u}.upsamplers.0.conv", dev) if u < len(rev) - 1 else None
+            us = None
+            if u < len(rev) - 1:     # nearest-2x + 3x3 conv as one sub-pixel launch (HP_A_UPCONV)
+                name = f"decoder.up_blocks.{u}.upsamplers.0.conv"
+                us = (_Conv(W, name, dev), K.upconv_weights(W[name + ".weight"].to(dev).permute(0, 2, 3, 1)))
             self.up.append((res, us))
         self.norm_out = _Norm(W, "decoder.conv_norm_out", dev)
         self.conv_out = _Conv(W, "decoder.conv_out", dev, cout_pad=self.PAD)
@@ -145,9 +149,12 @@ class VAEDecoder:
             for r in res:
                 x = r(x, n, h, w, g, st)
             if us is not None:
-                x = K.upsample2x(x, n, h, w, x.shape[1])
+                conv, w4 = us
+                if n * h * w > 128:                    # CTA-pair kernel (M > 128 rows)
+                    x = K.upsample_conv(x, n, h, w, conv.ci, w4, conv.b)
+                else:
+                    x = conv(K.upsample2x(x, n, h, w, x.shape[1]), n, 2 * h, 2 * w)
                 h, w = 2 * h, 2 * w
-                x = us(x, n, h, w)
         y = K.group_norm(x, n, h * w, x.shape[1], self.norm_out.g, self.norm_out.b, groups=g, eps=1e-6, silu=True,
                          stats=st)
         img = K.copy_cols(self.conv_out(y, n, h, w), s.out_channels)
@@ -181,6 +188,6 @@ def vae_decoder_flops(spec: VAESpec, n: int) -> float:
         prev = co
         if u < len(rev) - 1:
             px *= 4
-            fl += conv(px, co, co)
+            fl += conv(px, co, co) * 4 / 9                               # sub-pixel upsampler (HP_A_UPCONV)
     fl += conv(px, rev[-1], spec.out_channels)
     return n * fl

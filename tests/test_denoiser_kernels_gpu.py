@@ -267,3 +267,18 @@ def test_gemm_rows_batch_invariant(N, Kd, stats):
     if stats:
         assert r2.parts == r1.parts and r2.part_n == r1.part_n
         assert torch.equal(r2.buf[:2 * 1024 * r1.parts], r1.buf[:2 * 1024 * r1.parts])
+
+
+@pytest.mark.parametrize("n,h,w,c,co", [(2, 32, 32, 1280, 1280), (2, 64, 64, 640, 640), (1, 16, 16, 64, 128),
+                                        (1, 8, 32, 128, 320)])
+def test_upsample_conv_subpixel(n, h, w, c, co):
+    """nearest-2x upsample + 3x3 conv as four sub-pixel 2x2 convs in one launch
+    (HP_A_UPCONV) vs torch fp32 on the same bf16 input and weights."""
+    torch.manual_seed(n * h + c)
+    x = rnd(n * h * w, c)
+    w3 = torch.randn(co, 3, 3, c, device="cuda") * (9 * c) ** -0.5
+    bias = torch.randn(co, device="cuda")
+    out = K.upsample_conv(x, n, h, w, c, K.upconv_weights(w3), bias)
+    xi = x.float().view(n, h, w, c).permute(0, 3, 1, 2)
+    ref = F.conv2d(F.interpolate(xi, scale_factor=2, mode="nearest"), w3.permute(0, 3, 1, 2), bias, padding=1)
+    close(out.view(n, 2 * h, 2 * w, co), ref.permute(0, 2, 3, 1))
