@@ -48,7 +48,7 @@ STEPS_T = 50
 def _forward_traffic():
     """DRAM bytes of one forward from the committed ncu launch list (profiles/):
     dram__bytes_read.sum + dram__bytes_write.sum summed over the forward's kernels."""
-    path = os.path.join(ROOT, "profiles", "r01", "forward_r1g_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r01", "forward_r1i_traffic.json")
     try:
         with open(path) as fh:
             t = json.load(fh)
