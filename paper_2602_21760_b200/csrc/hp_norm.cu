@@ -13,10 +13,16 @@
 #include <math.h>
 #include "hybridpar_b200_denoiser.h"
 #include "hp_common.cuh"
+#include "hp_tc.cuh"
 
 namespace {
 
 using bf16 = __nv_bfloat16;
+using hptc::fence_barrier_init;
+using hptc::mbar_arrive_expect_tx;
+using hptc::mbar_init;
+using hptc::mbar_wait;
+using hptc::smem_u32;
 
 __device__ __forceinline__ void load8(const bf16* p, float* v) {
   uint4 u = *reinterpret_cast<const uint4*>(p);
@@ -63,13 +69,14 @@ constexpr int kMaxC = 2560;
 
 // GroupNorm partial sums of one (image n, pixel split) block: fixed-order
 // reduction (no float atomics): deterministic, batch-invariant
-__device__ __forceinline__ void gn_stats_block(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2,
-                                               int c2, int64_t hw, int groups, int splits,
-                                               float* __restrict__ part, int n, int split, float* s_sum,
-                                               float* s_sq, float* p_sum, float* p_sq) {
+// ch1 / ch2: the chunk's first pixel row of each input (global memory or a shared-memory
+// copy with the same row strides c1 / c2); npx pixels. Same arithmetic order either way.
+__device__ __forceinline__ void gn_stats_block(const bf16* ch1, int c1, const bf16* ch2, int c2, int64_t npx,
+                                               int groups, int splits, float* __restrict__ part, int n, int split,
+                                               float* s_sum, float* s_sq, float* p_sum, float* p_sq) {
   const int C = c1 + c2;
   const int V = C / 8;
-  const int64_t p_begin = hw * split / splits, p_end = hw * (split + 1) / splits;
+  const int64_t p_begin = 0, p_end = npx;
   for (int j0 = 0; j0 < V; j0 += kGnThreads) {
     const int vecs = min(V - j0, kGnThreads);
     const int rows = kGnThreads / vecs;
@@ -78,7 +85,7 @@ __device__ __forceinline__ void gn_stats_block(const bf16* __restrict__ x1, int 
     float sum[8] = {0}, sq[8] = {0};
     if (r < rows) {
       const int ch = j * 8;
-      const bf16* src = ch < c1 ? x1 + (int64_t)n * hw * c1 + ch : x2 + (int64_t)n * hw * c2 + (ch - c1);
+      const bf16* src = ch < c1 ? ch1 + ch : ch2 + (ch - c1);
       const int64_t st = ch < c1 ? c1 : c2;
       int64_t p = p_begin + r;
       // four 16-byte loads in flight per thread (the loop is latency-bound otherwise)
@@ -145,18 +152,23 @@ gn_stats_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
   pdl_trigger();
   __shared__ float s_sum[kMaxC], s_sq[kMaxC];
   __shared__ float p_sum[kGnThreads * 8], p_sq[kGnThreads * 8];
-  gn_stats_block(x1, c1, x2, c2, hw, groups, splits, part, blockIdx.y, blockIdx.x, s_sum, s_sq, p_sum, p_sq);
+  const int n = blockIdx.y, split = blockIdx.x;
+  const int64_t p0 = hw * split / splits, p1 = hw * (split + 1) / splits;
+  gn_stats_block(x1 + ((int64_t)n * hw + p0) * c1, c1, x2 ? x2 + ((int64_t)n * hw + p0) * c2 : nullptr, c2, p1 - p0,
+                 groups, splits, part, n, split, s_sum, s_sq, p_sum, p_sq);
 }
 
 // GroupNorm pass 2 for image n: fold the per-split partials (fixed order), then
 // y = x * sa[c] + sb[c] (+ SiLU) over pixels p_first + r, stepping p_mul * rows
-__device__ __forceinline__ void gn_apply_block(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2,
-                                               int c2, int64_t hw, int groups, int splits,
-                                               const float* __restrict__ part, float eps,
+// xa / xb: image n's first pixel row of each input (or a shared-memory chunk copy
+// whose row 0 is pixel `src_p0`); y: the output image base. Pixels p_first + r,
+// stepping p_mul * rows, up to p_end (image pixel indices).
+__device__ __forceinline__ void gn_apply_block(const bf16* xa, int c1, const bf16* xb, int c2, int64_t hw, int groups,
+                                               int splits, const float* __restrict__ part, float eps,
                                                const float* __restrict__ gamma, const float* __restrict__ beta,
-                                               int do_silu, bf16* __restrict__ y, int n, int64_t p_first,
-                                               int64_t p_mul, int64_t p_end, float* s_mean, float* s_rstd,
-                                               double* s_pa, double* s_pb, float* sa, float* sb) {
+                                               int do_silu, bf16* __restrict__ yo, int n, int64_t src_p0,
+                                               int64_t p_first, int64_t p_mul, int64_t p_end, float* s_mean,
+                                               float* s_rstd, double* s_pa, double* s_pb, float* sa, float* sb) {
   const int C = c1 + c2;
   const int V = C / 8;
   const int cg = C / groups;
@@ -208,9 +220,6 @@ __device__ __forceinline__ void gn_apply_block(const bf16* __restrict__ x1, int 
   const int vc = V < kGnThreads ? V : kGnThreads;
   const int rows = kGnThreads / vc;
   const int r = threadIdx.x / vc;
-  const bf16* xa = x1 + (int64_t)n * hw * c1;
-  const bf16* xb = x2 ? x2 + (int64_t)n * hw * c2 : nullptr;
-  bf16* yo = y + (int64_t)n * hw * C;
   if (r >= rows) return;
   for (int j = threadIdx.x % vc; j < V; j += vc) {
     const int ch = j * 8;
@@ -225,7 +234,7 @@ __device__ __forceinline__ void gn_apply_block(const bf16* __restrict__ x1, int 
     for (; p + 3 * step < p_end; p += 4 * step) {         // four loads in flight
       uint4 u[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(src + (p + k * step) * sstride);
+      for (int k = 0; k < 4; ++k) u[k] = *reinterpret_cast<const uint4*>(src + (p - src_p0 + k * step) * sstride);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[k]);
@@ -245,7 +254,7 @@ __device__ __forceinline__ void gn_apply_block(const bf16* __restrict__ x1, int 
     }
     for (; p < p_end; p += step) {
       float v[8];
-      load8(src + p * sstride, v);
+      load8(src + (p - src_p0) * sstride, v);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const float o = fmaf(v[k], av[k], bv[k]);
@@ -266,7 +275,9 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
   __shared__ float s_mean[64], s_rstd[64];
   __shared__ double s_pa[kGnThreads], s_pb[kGnThreads];
   __shared__ __align__(16) float sa[kMaxC], sb[kMaxC];
-  gn_apply_block(x1, c1, x2, c2, hw, groups, splits, part, eps, gamma, beta, do_silu, y, blockIdx.y,
+  const int n = blockIdx.y;
+  gn_apply_block(x1 + (int64_t)n * hw * c1, c1, x2 ? x2 + (int64_t)n * hw * c2 : nullptr, c2, hw, groups, splits,
+                 part, eps, gamma, beta, do_silu, y + (int64_t)n * hw * (c1 + c2), n, 0,
                  (int64_t)blockIdx.x * (kGnThreads / min((c1 + c2) / 8, kGnThreads)), gridDim.x, hw, s_mean, s_rstd,
                  s_pa, s_pb, sa, sb);
 }
@@ -275,6 +286,19 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
 // sense-reversing barrier (every CTA of the grid is resident: the launcher checks
 // occupancy), fold the partials and normalise the pixels they just reduced (an
 // L2 hit). Same partition and fold as the two-kernel path: bit-identical output.
+// largest pixel chunk of a split, bytes, rounded to 128 (the staged variant's scratch follows it)
+__host__ __device__ __forceinline__ size_t gn_chunk_bytes(int64_t hw, int splits, int C) {
+  return ((size_t)((hw + splits - 1) / splits) * C * 2 + 127) & ~(size_t)127;
+}
+__host__ __device__ __forceinline__ size_t gn_smem_bytes(int64_t hw, int splits, int C) {
+  return gn_chunk_bytes(hw, splits, C) + (size_t)(2 * C + 2 * kGnThreads * 8) * sizeof(float);
+}
+// 1-D bulk async copy global -> this CTA's shared memory, completion on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void image_barrier(unsigned* cnt, unsigned* gen, unsigned expected) {
   const unsigned g = *reinterpret_cast<volatile unsigned*>(gen);
   __threadfence();
@@ -288,24 +312,67 @@ __device__ __forceinline__ void image_barrier(unsigned* cnt, unsigned* gen, unsi
   __threadfence();
 }
 
+// SMEM: the CTA first copies its pixel chunk of each input into shared memory with
+// bulk async copies (all of it in flight at once), reduces it from there and
+// normalises it from there (no second global read).
+template <bool SMEM>
 __global__ void __launch_bounds__(kGnThreads)
 gn_fused_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
                 int groups, int splits, float* __restrict__ part, float eps, const float* __restrict__ gamma,
                 const float* __restrict__ beta, int do_silu, bf16* __restrict__ y, unsigned* __restrict__ bar) {
+  extern __shared__ __align__(128) uint8_t gn_chunk[];
+  __shared__ uint64_t ld_bar;
   pdl_wait();
   pdl_trigger();
-  __shared__ __align__(16) float sm[2 * kMaxC + 2 * kGnThreads * 8];
   const int n = blockIdx.y, split = blockIdx.x;
-  gn_stats_block(x1, c1, x2, c2, hw, groups, splits, part, n, split, sm, sm + kMaxC, sm + 2 * kMaxC,
-                 sm + 2 * kMaxC + kGnThreads * 8);
+  const int64_t p_begin = hw * split / splits, p_end = hw * (split + 1) / splits;
+  const int64_t npx = p_end - p_begin;
+  // reduction scratch: [cmax] sums, [cmax] squares, [kGnThreads * 8] x 2 thread partials
+  // (reused by the apply phase); sized by C behind the chunk when it is staged
+  float* sm;
+  int cmax;
+  if constexpr (SMEM) {
+    cmax = c1 + c2;
+    sm = reinterpret_cast<float*>(gn_chunk + gn_chunk_bytes(hw, splits, c1 + c2));
+  } else {
+    __shared__ __align__(16) float sm_static[2 * kMaxC + 2 * kGnThreads * 8];
+    cmax = kMaxC;
+    sm = sm_static;
+  }
+  const bf16* g1 = x1 + ((int64_t)n * hw + p_begin) * c1;
+  const bf16* g2 = x2 ? x2 + ((int64_t)n * hw + p_begin) * c2 : nullptr;
+  const bf16* ch1 = g1;
+  const bf16* ch2 = g2;
+  if constexpr (SMEM) {
+    bf16* d1 = reinterpret_cast<bf16*>(gn_chunk);
+    bf16* d2 = d1 + npx * c1;
+    if (threadIdx.x == 0) {
+      mbar_init(&ld_bar, 1);
+      fence_barrier_init();
+      const uint32_t b1 = (uint32_t)(npx * c1 * 2), b2 = g2 ? (uint32_t)(npx * c2 * 2) : 0u;
+      mbar_arrive_expect_tx(&ld_bar, b1 + b2);
+      constexpr uint32_t kPiece = 16384;
+      for (uint32_t o = 0; o < b1; o += kPiece)
+        bulk_g2s(reinterpret_cast<uint8_t*>(d1) + o, reinterpret_cast<const uint8_t*>(g1) + o, min(kPiece, b1 - o),
+                 &ld_bar);
+      for (uint32_t o = 0; o < b2; o += kPiece)
+        bulk_g2s(reinterpret_cast<uint8_t*>(d2) + o, reinterpret_cast<const uint8_t*>(g2) + o, min(kPiece, b2 - o),
+                 &ld_bar);
+    }
+    __syncthreads();
+    mbar_wait(&ld_bar, 0);
+    ch1 = d1;
+    ch2 = g2 ? d2 : nullptr;
+  }
+  gn_stats_block(ch1, c1, ch2, c2, npx, groups, splits, part, n, split, sm, sm + cmax, sm + 2 * cmax,
+                 sm + 2 * cmax + kGnThreads * 8);
   __syncthreads();
   if (threadIdx.x == 0) image_barrier(bar + 2 * n, bar + 2 * n + 1, (unsigned)splits);
   __syncthreads();
-  const int64_t p_begin = hw * split / splits, p_end = hw * (split + 1) / splits;
-  double* dp = reinterpret_cast<double*>(sm + 2 * kMaxC);              // [2][kGnThreads] doubles
-  float* s_mean = sm + 2 * kMaxC + 4 * kGnThreads;
-  gn_apply_block(x1, c1, x2, c2, hw, groups, splits, part, eps, gamma, beta, do_silu, y, n, p_begin, 1, p_end,
-                 s_mean, s_mean + 64, dp, dp + kGnThreads, sm, sm + kMaxC);
+  double* dp = reinterpret_cast<double*>(sm + 2 * cmax);               // [2][kGnThreads] doubles
+  float* s_mean = sm + 2 * cmax + 4 * kGnThreads;
+  gn_apply_block(ch1, c1, ch2, c2, hw, groups, splits, part, eps, gamma, beta, do_silu, y + (int64_t)n * hw * (c1 + c2),
+                 n, p_begin, p_begin, 1, p_end, s_mean, s_mean + 64, dp, dp + kGnThreads, sm, sm + cmax);
 }
 
 // ---------------------------------------------------------------------------
@@ -774,25 +841,41 @@ inline int ok() { return cudaGetLastError() == cudaSuccess ? HP_OK : HP_ERR_CUDA
 constexpr int kGnMaxImages = 64;
 unsigned* g_gn_bar = nullptr;
 
-bool gn_fused_ok(int ctas, cudaStream_t st) {
-  static int capacity = -1;
+constexpr size_t kGnSmemMax = 112 * 1024;   // staged chunk + scratch limit: two CTAs per SM
+constexpr size_t kGnSmemMin = 32 * 1024;    // smaller chunks: direct loads are faster
+
+// 0: two-kernel path; 1: single launch reading global memory; 2: single launch with the
+// chunk staged in shared memory (`smem` bytes)
+int gn_fused_mode(int ctas, size_t smem, cudaStream_t st) {
   static bool disabled = getenv("HP_GN_FUSED") && getenv("HP_GN_FUSED")[0] == '0';
-  if (disabled) return false;
+  static bool no_smem = getenv("HP_GN_SMEM") && getenv("HP_GN_SMEM")[0] == '0';
+  if (disabled) return 0;
   if (!g_gn_bar) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
-    if (cudaMalloc(&g_gn_bar, 2 * kGnMaxImages * sizeof(unsigned)) != cudaSuccess) { g_gn_bar = nullptr; return false; }
-    if (cudaMemset(g_gn_bar, 0, 2 * kGnMaxImages * sizeof(unsigned)) != cudaSuccess) return false;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return 0;
+    if (cudaMalloc(&g_gn_bar, 2 * kGnMaxImages * sizeof(unsigned)) != cudaSuccess) { g_gn_bar = nullptr; return 0; }
+    if (cudaMemset(g_gn_bar, 0, 2 * kGnMaxImages * sizeof(unsigned)) != cudaSuccess) return 0;
   }
-  if (capacity < 0) {
-    int per_sm = 0, dev = 0, sms = 0;
+  static int sms = 0;
+  static bool attr = false;
+  if (!sms) {
+    int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gn_fused_kernel, kGnThreads, 0) != cudaSuccess)
-      per_sm = 0;
-    capacity = per_sm * sms;
+    attr = cudaFuncSetAttribute(gn_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kGnSmemMax) == cudaSuccess;
   }
-  return ctas <= capacity;    // every CTA resident: the in-kernel barrier cannot deadlock
+  // every CTA resident (occupancy-checked): the in-kernel barrier cannot deadlock
+  int per_sm = 0;
+  if (!no_smem && attr && smem <= kGnSmemMax &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gn_fused_kernel<true>, kGnThreads, smem) ==
+          cudaSuccess &&
+      ctas <= per_sm * sms)
+    return 2;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gn_fused_kernel<false>, kGnThreads, 0) == cudaSuccess &&
+      ctas <= per_sm * sms)
+    return 1;
+  return 0;
 }
 
 }  // namespace
@@ -810,9 +893,18 @@ int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_
   // the pixel partition depends on hw only (never on the batch size n), so one
   // image's statistics are bit-identical whatever else is in the batch
   int splits = hw < 128 ? (int)hw : 128;
-  if (n <= kGnMaxImages && gn_fused_ok(n * splits, st)) {
-    hp_launch_pdl(gn_fused_kernel, dim3(splits, n), dim3(kGnThreads), 0, st, static_cast<const bf16*>(x1), c1,
-                  static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups, splits, stats, eps, gamma, beta, do_silu,
+  // stage the chunk in shared memory when it is large enough for the bulk copies to pay
+  static const size_t smem_min = [] {        // development probe: HP_GN_SMEM_MIN=<bytes>
+    const char* e = getenv("HP_GN_SMEM_MIN");
+    return e ? (size_t)atol(e) : kGnSmemMin;
+  }();
+  const bool stage = gn_chunk_bytes(hw, splits, C) >= smem_min;
+  const size_t smem = gn_smem_bytes(hw, splits, C);
+  const int mode = n <= kGnMaxImages ? gn_fused_mode(n * splits, stage ? smem : kGnSmemMax + 1, st) : 0;
+  if (mode) {
+    const auto kern = mode == 2 ? gn_fused_kernel<true> : gn_fused_kernel<false>;
+    hp_launch_pdl(kern, dim3(splits, n), dim3(kGnThreads), mode == 2 ? smem : 0, st, static_cast<const bf16*>(x1),
+                  c1, static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups, splits, stats, eps, gamma, beta, do_silu,
                   static_cast<bf16*>(y), g_gn_bar);
     if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
     return ok();
