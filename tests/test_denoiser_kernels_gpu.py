@@ -116,7 +116,10 @@ def test_attention_fused_qkv_columns():
 
 
 @pytest.mark.parametrize("n,hw,c,c2,silu", [(2, 4096, 320, 0, True), (2, 1024, 1280, 640, False),
-                                            (1, 256, 960, 0, True)])
+                                            (1, 256, 960, 0, True),
+                                            # >= 32 KB pixel chunks: staged in shared memory
+                                            (2, 16384, 320, 0, True), (2, 4096, 640, 640, True),
+                                            (2, 1024, 1280, 1280, False)])
 def test_group_norm(n, hw, c, c2, silu):
     x = rnd(n * hw, c, s=2.0) + 0.5
     x2 = rnd(n * hw, c2) if c2 else None
@@ -130,12 +133,14 @@ def test_group_norm(n, hw, c, c2, silu):
     close(out, ref)
 
 
-def test_group_norm_batch_invariant():
-    x = rnd(2 * 1024, 640)
-    g, b = torch.ones(640, device="cuda"), torch.zeros(640, device="cuda")
-    both = K.group_norm(x, 2, 1024, 640, g, b)
-    one = K.group_norm(x[1024:].contiguous(), 1, 1024, 640, g, b)
-    assert torch.equal(both[1024:], one)
+@pytest.mark.parametrize("hw,c", [(1024, 640), (16384, 320)])
+def test_group_norm_batch_invariant(hw, c):
+    """Image 1's output does not depend on image 0 (also on the shared-memory staged path)."""
+    x = rnd(2 * hw, c)
+    g, b = torch.ones(c, device="cuda"), torch.zeros(c, device="cuda")
+    both = K.group_norm(x, 2, hw, c, g, b)
+    one = K.group_norm(x[hw:].contiguous(), 1, hw, c, g, b)
+    assert torch.equal(both[hw:], one)
 
 
 @pytest.mark.parametrize("c", [640, 1280, 1536])
