@@ -33,10 +33,12 @@ def main():
     src, tag = sys.argv[1], sys.argv[2]
     launches = load(src)
     starts = [i for i, d in enumerate(launches) if "timestep_emb" in d["name"]]
-    seg = launches[starts[-1]:]
+    # the last complete denoising step (forward + sampler) when the capture holds two or
+    # more (a launch-count cap may cut the last one short), else the last forward
+    seg = launches[starts[-2]:starts[-1]] if len(starts) >= 2 and "--last" not in sys.argv else launches[starts[-1]:]
     short = lambda n: n.split("(")[0].replace("void ", "").replace("<unnamed>::", "")  # noqa: E731
     with open(tag + "_launches.csv", "w") as fh:
-        fh.write(f"# last forward of {src}: {len(seg)} launches\n")
+        fh.write(f"# one denoising step of {src}: {len(seg)} launches\n")
         fh.write("kernel,grid,duration_ns,dram_read_bytes,dram_write_bytes\n")
         for d in seg:
             fh.write(f"\"{short(d['name'])}\",\"{d['grid']}\",{d.get('gpu__time_duration.sum', 0):.0f},"
