@@ -18,7 +18,10 @@ from ..errors import check as _check
 # number of our kernel launches issued through these wrappers (the engine and
 # bench read it around graph capture to report launches per forward)
 LAUNCHES = 0
-_KERNELS_PER_CALL = {"hp_group_norm": 2}
+# wrappers whose C entry issues more than one kernel (hp_group_norm is one launch on its
+# single-launch path, which every denoiser shape takes; two only for batches too large
+# for all statistics CTAs to be resident)
+_KERNELS_PER_CALL: dict = {}
 
 
 def check(rc, what):
