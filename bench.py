@@ -263,6 +263,55 @@ def forward_roofline(den, spec, reps=20):
     return t, unet_flops(spec, 2)
 
 
+def top_kernel_rooflines(bf16_peak, reps=20):
+    """The step's two dominant kernels (profiles/r01/bench_r1j_summary.txt: split-KV
+    self-attention 19%, GEGLU GEMM 17%) at their SDXL shapes, each timed live with CUDA
+    events around a CUDA graph of `reps` back-to-back launches on the launching stream
+    (inputs L2-resident between launches: a per-kernel ceiling, not the in-step rate)."""
+    import torch
+    from paper_2602_21760_b200.denoiser import kernels as K
+
+    def graph_us(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(reps):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps * 1e3
+
+    out = []
+    for S, H, n in ((4096, 10, 10), (1024, 20, 60)):       # level 1 / level 2 self-attention, launches per step
+        q = torch.randn(2 * S, H * 64, device="cuda").bfloat16()
+        kv = torch.randn(2 * S, 2 * H * 64, device="cuda").bfloat16()
+        o = torch.empty_like(q)
+        us = graph_us(lambda: K.attention(q, kv, kv, o, batch=2, heads=H, sq=S, skv=S, scale=0.125,
+                                          q_col0=0, k_col0=0, v_col0=H * 64))
+        fl = 4.0 * 2 * H * S * S * 64
+        # the softmax bound: one exp2 per score, 5/8 of them on MUFU (16 / clk / SM at 1965 MHz)
+        mufu_us = 2.0 * H * S * S * 5 / 8 / (16 * 148 * 1.965e9) * 1e6
+        out.append({"kernel": f"attn_splitkv S={S} H={H} B=2 (x{n} per step)", "flops_per_launch": fl,
+                    "us": us, "achieved": fl / us / 1e6, "frac": fl / us / 1e6 / bf16_peak,
+                    "mufu_bound_us": mufu_us, "frac_of_mufu_bound": mufu_us / us})
+    M, N, Kd = 2048, 10240, 1280                                # level-2 GEGLU (x60 per step)
+    a = torch.randn(M, Kd, device="cuda").bfloat16()
+    w = (torch.randn(N, Kd, device="cuda") * Kd ** -0.5).bfloat16()
+    y = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+    us = graph_us(lambda: K.gemm(a, w, out=y, act=K.ACT_GEGLU))
+    fl = 2.0 * M * N * Kd
+    out.append({"kernel": f"gemm_pair GEGLU {M}x{N}x{Kd} (x60 per step)", "flops_per_launch": fl, "us": us,
+                "achieved": fl / us / 1e6, "frac": fl / us / 1e6 / bf16_peak})
+    return out
+
+
 def time_replicas(args, spec, ws, rank, local):
     """Every GPU generates its own images with the serial (CFG-batched) plan."""
     import torch
@@ -396,6 +445,7 @@ def main():
     launches_fwd = (den.g_both.launches if mode != "pairs"
                     else max(den.g_cond.launches, getattr(getattr(den, "g_uncond", None), "launches", 0)))
     samp = sampler_roofline(hbm_peak) if rank == 0 else {}
+    top = top_kernel_rooflines(bf16_burst) if rank == 0 else []
 
     if rank != 0:
         if ws > 1:
@@ -431,7 +481,8 @@ def main():
                      "achieved_isolated_forward": achieved_fwd,
                      "peak": bf16_sus, "unit": "TFLOP/s", "frac": achieved / bf16_sus,
                      "peak_kind": f"{peak_src} sustained", "frac_of_burst": achieved / bf16_burst,
-                     "flops_per_launch": fwd_flops, "forward_ms": fwd_s * 1e3, **_forward_traffic()},
+                     "flops_per_launch": fwd_flops, "forward_ms": fwd_s * 1e3, **_forward_traffic(),
+                     "top_kernels": top, "top_kernels_peak": f"{peak_src} burst bf16 {bf16_burst}"},
         "sampler_roofline": {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_src,
                              "sizes": list(samp.values())},
         "clocks": clocks.summary(),
