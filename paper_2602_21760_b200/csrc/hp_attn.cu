@@ -104,6 +104,23 @@ __device__ __forceinline__ void tmem_ld_x32_at(uint32_t taddr, uint32_t* r, cons
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+      :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+         "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+// D (TMEM) += A (TMEM: lane = row, K packed two bf16 per column) . B (smem descriptor)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t desc_b, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      :: "r"(tmem_d), "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate) : "memory");
+}
 
 // SINGLE: every key fits one 128-key block (cross-attention, skv <= 128). Then no
 // rescale exists, O_q reuses S_q's TMEM columns once the softmax has consumed S_q,
@@ -392,8 +409,8 @@ attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
   uint8_t* sQ = smem;                                        // 1 tile
   uint8_t* sK = sQ + kTileBytes;                             // [stream][stage]
   uint8_t* sV = sK + 2 * kStSplit * kTileBytes;              // [stream][stage]
-  uint8_t* sP = sV + 2 * kStSplit * kTileBytes;              // [stream]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
+  // P_q lives in TMEM columns [384 + 64 q, 448 + 64 q) (bf16 pairs), read by a TS-MMA
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kStSplit * kTileBytes);
   uint64_t* q_full = bars;
   uint64_t* kv_full = q_full + 1;                            // [stream][stage]
   uint64_t* kv_empty = kv_full + 2 * kStSplit;
@@ -456,9 +473,8 @@ attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         const uint8_t* v = v_at(q, i % kStSplit);
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k) {
-          const uint64_t da = sdesc_sw128_kmajor(sP + q * kPBytes + (k >> 2) * (kBQ * 128)) + 2 * (k & 3);
           const uint64_t dv = sdesc_sw128_mnmajor(v + k * 2048, 8192);
-          umma_bf16(tmem + 256 + q * kD, da, dv, kIdescO, (i > 0 || k > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + 256 + q * kD, tmem + 384 + q * 64 + 8 * k, dv, kIdescO, (i > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&o_done[q]);
         umma_commit(&kv_empty[q * kStSplit + i % kStSplit]);
@@ -491,7 +507,7 @@ attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t t_s = tmem + lane_base + q * kBK;
     const uint32_t t_o = tmem + lane_base + 256 + q * kD;
-    uint8_t* pbase = sP + q * kPBytes;
+    const uint32_t t_p = tmem + lane_base + 384 + q * 64;
     float m_run = -INFINITY, l_run = 0.f;
     const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
     const int n = nj[q];
@@ -557,16 +573,10 @@ attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
           sum2 = fadd2(sum2, e2);
           packed[e / 2] = pack_bf16(lo2(e2), hi2(e2));
         }
-        uint8_t* atom = pbase + (c >> 1) * (kBQ * 128) + row * 128;
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          const int chunk = ((c & 1) * 4 + qq) ^ (row & 7);
-          *reinterpret_cast<uint4*>(atom + chunk * 16) =
-              make_uint4(packed[4 * qq], packed[4 * qq + 1], packed[4 * qq + 2], packed[4 * qq + 3]);
-        }
+        tmem_st_32x32b_x16(t_p + c * 16, packed);
       }
       l_run += lo2(sum2) + hi2(sum2);
-      fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[q]);
@@ -714,7 +724,7 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   const int sms = num_sms_attn();
   const int tail = pair_ctas % sms;
   if (splitkv_enabled() && tail != 0 && tail * 2 < sms) {
-    constexpr size_t smem = 1024 + (size_t)kTileBytes * (1 + 4 * kStSplit) + 2 * kPBytes + 256 + 4 * kBQ * 4;
+    constexpr size_t smem = 1024 + (size_t)kTileBytes * (1 + 4 * kStSplit) + 256 + 4 * kBQ * 4;
     static bool attr_s = false;
     if (!attr_s) {
       if (cudaFuncSetAttribute(attn_splitkv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
