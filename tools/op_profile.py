@@ -2,7 +2,7 @@
 call, eager forward, warm). Prints per-shape achieved TFLOP/s / GB/s and the
 time share, to pick the next kernel to optimise.
 
-    python tools/op_profile.py [tiny]
+    python tools/op_profile.py [tiny|sd3]
 """
 import collections
 import sys
@@ -55,16 +55,29 @@ def gn_key(x, n, hw, c, *a, **kw):
     return (f"groupnorm n={n} hw={hw} c={c}", 2 * 2.0 * n * hw * c)
 
 
+def ljoint_key(*a, **kw):
+    return ("layer_norm_joint", 0.0)
+
+
 def main():
-    spec = Wm.TINY if "tiny" in sys.argv else Wm.SDXL
-    den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=50, use_graph=False)
+    sd3 = "sd3" in sys.argv
+    if sd3:
+        spec = Wm.SD3
+        den = pipelines.build_sd3_denoiser(spec, n_prompts=1, steps=28, use_graph=False)
+    else:
+        spec = Wm.TINY if "tiny" in sys.argv else Wm.SDXL
+        den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=50, use_graph=False)
     K.gemm = wrap("gemm", K.gemm, gemm_key)
     K.attention = wrap("attn", K.attention, attn_key)
     K.layer_norm = wrap("ln", K.layer_norm, ln_key)
     K.group_norm = wrap("gn", K.group_norm, gn_key)
+    if hasattr(K, "layer_norm_joint"):
+        K.layer_norm_joint = wrap("lnj", K.layer_norm_joint, ljoint_key)
+    import paper_2602_21760_b200.denoiser.mmdit as D
     import paper_2602_21760_b200.denoiser.unet as U
     U.K = K
-    x = torch.randn(1, spec.latent_hw * spec.latent_hw * 4, device="cuda")
+    D.K = K
+    x = torch.randn(1, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
     den.load_input(x)
     for _ in range(2):
         RECS.clear()
