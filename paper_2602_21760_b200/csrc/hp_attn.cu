@@ -20,7 +20,8 @@
 //   S_kv <= 128        single-block kernel, 2 CTAs/SM (cross-attention)
 //   short last wave    split-KV kernel: one query tile per CTA, its key range cut
 //                      in two halves processed by the two warpgroups and merged
-//                      (fixed split point: batch-invariant)
+//                      (fixed split point: batch-invariant); there P goes to TMEM
+//                      (bf16 pairs) and the PV MMA reads it from there (TS-MMA)
 //   otherwise          the two-tile kernel above
 // (Measured and dropped: P kept in TMEM as the A operand of a TS-MMA with the
 // whole S row in 200 registers: 180 us vs 169 us at S=4096; 64-key blocks with

@@ -2,21 +2,31 @@
 //
 //   D[M, N] = epilogue( alpha * A[M, K] . B[N, K]^T )
 //
-// A is either a plain row-major activation matrix or, for 3x3 convolutions,
-// an NHWC activation read as an implicit GEMM: the K loop walks 9 taps x
-// (Cin/64) channel blocks and each A tile is one 4-D TMA box of the input
-// shifted by the tap offset (TMA zero-fills the padding halo; stride-2
-// convolutions use TMA element strides). B is the K-major weight [N, K]
-// (conv weights stored [Cout][3][3][Cin]). No im2col buffer exists.
+// A is a plain row-major activation matrix or an NHWC activation read as an
+// implicit GEMM: 3x3 convolutions walk 9 taps x (Cin/64) channel blocks, each A
+// tile one 4-D TMA box of the input shifted by the tap (TMA zero-fills the
+// halo; stride 2 via TMA element strides); HP_A_UPCONV runs nearest-2x +
+// 3x3 conv as four sub-pixel 2x2 convs (one per output phase, as batch
+// entries). B is the K-major weight [N, K] (conv weights [Cout][taps][Cin]).
+// No im2col buffer exists.
 //
+// Kernels:
+//   gemm_kernel        one CTA per 128-row tile (M <= 128, and the cluster-LN mode)
+//   gemm_pair_kernel   CTA pair (cta_group::2): 256-row tiles, each CTA loads its A
+//                      rows and half of B; widths 64..320 (320 = two N=160 MMAs)
+//   gemm_splitk_kernel two CTA pairs of a 4-CTA cluster split K of one 256x320 tile
+//                      and exchange accumulator halves through DSMEM
 // Roles (256 threads, 1 CTA/SM, persistent over output tiles):
-//   warp 0      TMA producer   (smem ring of STAGES {A 128x64, B BNx64} tiles, SW128)
-//   warp 1      MMA issuer     (tcgen05.mma M=128, N=BN, K=16; fp32 accumulators in TMEM)
-//   warp 2      TMEM allocator (2 x BN columns: accumulator double buffer)
+//   warp 0      TMA producer   (smem ring of STAGES {A 128x64, B x64} tiles, SW128)
+//   warp 1      MMA issuer     (tcgen05.mma; fp32 accumulators in TMEM)
+//   warp 2      TMEM allocator (up to 4 accumulator buffers)
 //   warps 4..7  epilogue       (tcgen05.ld 32x32b -> bias / per-image bias / residual /
-//                               GELU / SiLU / GEGLU -> bf16 stores)
-// The epilogue of tile i overlaps the MMAs of tile i+1 through the TMEM
-// double buffer; TMA runs STAGES k-blocks ahead of the tensor core.
+//                               GELU / SiLU / GEGLU / column gate / LayerNorm fold or
+//                               statistics -> 256-bit bf16 stores)
+// The epilogue of tile i overlaps the MMAs of tile i+1 through the TMEM buffers;
+// TMA runs STAGES k-blocks ahead of the tensor core. Activation and epilogue
+// flavour are template parameters (each runtime branch in the unrolled epilogue
+// costs the common case).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>

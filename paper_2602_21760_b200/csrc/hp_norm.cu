@@ -3,7 +3,10 @@
 // GroupNorm(+SiLU) is two passes (per-image partial statistics over pixel
 // chunks, then a normalise pass that folds the partials in fixed order), so
 // it is deterministic and batch-invariant: image b's statistics never depend
-// on the other images in the batch. LayerNorm is one warp per row with an
+// on the other images in the batch. Normally one launch: an image's statistics
+// CTAs meet at an in-kernel barrier (all resident: occupancy-checked), each CTA
+// having staged its pixel chunk in shared memory with bulk async copies when the
+// chunk is >= 32 KB. LayerNorm is one warp per row with an
 // exact two-pass mean/variance from registers and optional adaLN modulation.
 // Everything else is a 16-byte-vectorised streaming kernel.
 #include <cuda_runtime.h>
