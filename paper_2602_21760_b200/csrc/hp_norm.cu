@@ -6,7 +6,7 @@
 // on the other images in the batch. Normally one launch: an image's statistics
 // CTAs meet at an in-kernel barrier (all resident: occupancy-checked), each CTA
 // having staged its pixel chunk in shared memory with bulk async copies when the
-// chunk is >= 32 KB. LayerNorm is one warp per row with an
+// chunk is >= 16 KB. LayerNorm is one warp per row with an
 // exact two-pass mean/variance from registers and optional adaLN modulation.
 // Everything else is a 16-byte-vectorised streaming kernel.
 #include <cuda_runtime.h>
@@ -845,7 +845,7 @@ constexpr int kGnMaxImages = 64;
 unsigned* g_gn_bar = nullptr;
 
 constexpr size_t kGnSmemMax = 112 * 1024;   // staged chunk + scratch limit: two CTAs per SM
-constexpr size_t kGnSmemMin = 32 * 1024;    // smaller chunks: direct loads are faster
+constexpr size_t kGnSmemMin = 16 * 1024;    // smaller chunks: direct loads are faster
 
 // 0: two-kernel path; 1: single launch reading global memory; 2: single launch with the
 // chunk staged in shared memory (`smem` bytes)
