@@ -27,6 +27,11 @@ CASES = {
     "serial": dict(variant="serial"),
     "hybrid_cap": dict(variant="hybrid", switch=dict(L=4, g_slope=1e-12, tau_cap=8, k=5)),
     "hybrid_k0": dict(variant="hybrid", switch=dict(L=4, g_slope=1e-12, tau_cap=8, k=0)),
+    # natural slope detection on the network's own M_t: fires at s=5 (G=2.2e-3 in [0, 4e-3))
+    "hybrid_natural": dict(variant="hybrid", switch=dict(L=4, g_slope=4e-3, tau_cap=8, k=5)),
+    # SURVEY 8(d) config-1 parameters: the detector runs every step from s=5 and must NOT
+    # fire (G is negative or >= 4e-4 at s=5..7), the cap forces tau1=8
+    "hybrid_survey": dict(variant="hybrid", switch=dict(L=4, g_slope=4e-4, tau_cap=8, k=5)),
 }
 T, GUIDANCE, SEED, PROMPTS = 20, 5.0, 3, 1
 

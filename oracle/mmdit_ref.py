@@ -22,9 +22,13 @@ def _sinus(t, dim, max_period=10000.0):
 
 
 class MMDiTRef:
-    def __init__(self, spec, W: dict):
+    """``dtype=torch.bfloat16``: the same network as a stock-torch bf16 model (the
+    yardstick for the error bf16 itself costs)."""
+
+    def __init__(self, spec, W: dict, dtype=torch.float32):
         self.s = spec
-        self.W = {k: v.float() for k, v in W.items()}
+        self.dt = dtype
+        self.W = {k: v.to(dtype) for k, v in W.items()}
 
     def _lin(self, x, name):
         return F.linear(x, self.W[name + ".weight"], self.W.get(name + ".bias"))
@@ -35,14 +39,14 @@ class MMDiTRef:
         n, Hl, Wl, C = x_nhwc.shape
         P, H = s.patch, s.hidden
         gh, gw = Hl // P, Wl // P
-        tok = x_nhwc.view(n, gh, P, gw, P, C).permute(0, 1, 3, 2, 4, 5).reshape(n, gh * gw, P * P * C)
+        tok = x_nhwc.to(self.dt).view(n, gh, P, gw, P, C).permute(0, 1, 3, 2, 4, 5).reshape(n, gh * gw, P * P * C)
         off = (s.pos_max - gh) // 2
         pos = W["pos_embed.pos"].view(s.pos_max, s.pos_max, H)[off:off + gh, off:off + gw].reshape(gh * gw, H)
         xi = self._lin(tok, "pos_embed.proj") + pos
-        xc = self._lin(context.float(), "context_embedder")
-        te = F.silu(self._lin(_sinus(t, s.freq_dim), "time_text_embed.timestep_embedder.linear_1"))
+        xc = self._lin(context.to(self.dt), "context_embedder")
+        te = F.silu(self._lin(_sinus(t, s.freq_dim).to(self.dt), "time_text_embed.timestep_embedder.linear_1"))
         te = self._lin(te, "time_text_embed.timestep_embedder.linear_2")
-        pe = F.silu(self._lin(pooled.float(), "time_text_embed.text_embedder.linear_1"))
+        pe = F.silu(self._lin(pooled.to(self.dt), "time_text_embed.text_embedder.linear_1"))
         c = te + self._lin(pe, "time_text_embed.text_embedder.linear_2")
         sc = F.silu(c)
         heads = s.heads
@@ -77,4 +81,4 @@ class MMDiTRef:
         scale, shift = self._lin(sc, "norm_out.linear").chunk(2, dim=1)
         y = F.layer_norm(xi, (H,), eps=1e-6) * (1 + scale[:, None]) + shift[:, None]
         o = self._lin(y, "proj_out")
-        return o.view(n, gh, gw, P, P, C).permute(0, 1, 3, 2, 4, 5).reshape(n, Hl, Wl, C)
+        return o.float().view(n, gh, gw, P, P, C).permute(0, 1, 3, 2, 4, 5).reshape(n, Hl, Wl, C)

@@ -26,9 +26,14 @@ def _sinus(t, dim, max_period=10000.0):
 
 
 class UNetRef:
-    def __init__(self, spec, W: dict):
+    """``dtype=torch.bfloat16`` gives the same network as a stock-torch bf16 model
+    (cuBLAS/cuDNN bf16 with fp32 accumulation): the yardstick for how much error
+    bf16 itself costs, against which our kernels' error is judged."""
+
+    def __init__(self, spec, W: dict, dtype=torch.float32):
         self.s = spec
-        self.W = {k: v.float() for k, v in W.items()}
+        self.dt = dtype
+        self.W = {k: v.to(dtype) for k, v in W.items()}
 
     def _lin(self, x, name, bias=True):
         b = self.W.get(name + ".bias") if bias else None
@@ -79,14 +84,15 @@ class UNetRef:
         """x [B, C, H, W] fp32, t [B] timesteps, context [B, L, D], pooled [B, P] -> eps NCHW."""
         s = self.s
         B = x_nchw.shape[0]
-        temb = self._lin(F.silu(self._lin(_sinus(t, s.block_out[0]), "time_embedding.linear_1")),
+        x_nchw = x_nchw.to(self.dt)
+        temb = self._lin(F.silu(self._lin(_sinus(t, s.block_out[0]).to(self.dt), "time_embedding.linear_1")),
                          "time_embedding.linear_2")
         size = 8.0 * s.latent_hw
         ids = torch.tensor([size, size, 0.0, 0.0, size, size], device=x_nchw.device).repeat(B, 1).reshape(-1)
         tid = _sinus(ids, s.time_id_dim).reshape(B, -1)
-        a = torch.cat([pooled.float(), tid], dim=1)
+        a = torch.cat([pooled.float(), tid], dim=1).to(self.dt)
         emb = temb + self._lin(F.silu(self._lin(a, "add_embedding.linear_1")), "add_embedding.linear_2")
-        ctx = context.float()
+        ctx = context.to(self.dt)
         h = self._conv(x_nchw, "conv_in")
         skips = [h]
         ch = s.block_out
@@ -113,7 +119,7 @@ class UNetRef:
                 h = F.interpolate(h, scale_factor=2.0, mode="nearest")
                 h = self._conv(h, f"up_blocks.{u}.upsamplers.0.conv")
         h = F.silu(self._gn(h, "conv_norm_out"))
-        return self._conv(h, "conv_out")
+        return self._conv(h, "conv_out").float()
 
 
 def net_timestep(t: int, T: int) -> float:

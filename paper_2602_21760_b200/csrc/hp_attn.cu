@@ -128,19 +128,13 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 // and one K/V stage suffices: 256 TMEM columns and 97 KB of smem, so two CTAs
 // share an SM and one's latency chain (TMA -> MMA -> softmax -> PV -> store)
 // overlaps the other's.
-//
-// SOLO: one query tile per CTA (4 softmax warps + TMA + MMA warp, 256 TMEM
-// columns, 2 K/V stages, 112 KB smem), two CTAs per SM. Twice the units of the
-// two-tile CTA, so the last partial wave of a 160- or 320-unit grid on 148 SMs
-// is half as long, and a lone CTA in that wave runs its softmax without a
-// co-resident tile competing for MUFU/FMA.
-constexpr int kModePair = 0, kModeSingle = 1, kModeSolo = 2;
+constexpr int kModePair = 0, kModeSingle = 1;
 template <int MODE> struct AttnCfg {
   static constexpr bool kSingle = MODE == kModeSingle;
-  static constexpr int kNq = MODE == kModeSolo ? 1 : 2;
+  static constexpr int kNq = 2;
   static constexpr int kThr = 32 * (4 * kNq + 2);
   static constexpr int kMinBlocks = MODE == kModePair ? 1 : 2;
-  static constexpr int kSt = kSingle ? 1 : (MODE == kModeSolo ? 2 : kStages);
+  static constexpr int kSt = kSingle ? 1 : kStages;
   static constexpr uint32_t kCols = MODE == kModePair ? kTmemCols : 256;
   static constexpr size_t kSmem = kSingle ? kTileBytes * 5 + 256
                                           : (size_t)kTileBytes * (kNq + 2 * kSt) + kNq * kPBytes + 256;
@@ -157,10 +151,6 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
   constexpr uint32_t kCols = Cfg::kCols;
   constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  if constexpr (MODE == kModeSolo) {
-    // the launch requests no alignment slack (two CTAs must fit an SM)
-    if (smem_u32(smem_raw) & 1023) __trap();
-  }
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                                  // NQ tiles
   uint8_t* sK = sQ + NQ * kTileBytes;
@@ -686,15 +676,6 @@ bool splitkv_enabled() {
   return on == 1;
 }
 
-bool solo_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("HP_ATTN_SOLO");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
-}
-
 }  // namespace
 
 extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
@@ -738,11 +719,6 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
     dim3 g1((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
     const auto kern = (d->skv % kBK) ? attn_splitkv_kernel<true> : attn_splitkv_kernel<false>;
     return hp_launch_pdl(kern, g1, dim3(kThreads), smem, st, tq, tk, tv, p) == cudaSuccess ? HP_OK : HP_ERR_CUDA;
-  }
-  if (solo_enabled() && tail != 0 && tail * 2 < sms) {
-    dim3 g1((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
-    return mask ? launch_attn<kModeSolo, true>(g1, st, tq, tk, tv, p, 0)
-                : launch_attn<kModeSolo, false>(g1, st, tq, tk, tv, p, 0);
   }
   return mask ? launch_attn<kModePair, true>(grid, st, tq, tk, tv, p, 1024)
               : launch_attn<kModePair, false>(grid, st, tq, tk, tv, p, 1024);

@@ -88,8 +88,23 @@ def test_conv3x3_implicit_gemm(n, h, w, c, co, stride):
     close(out.view(n, h // stride, w // stride, co), ref.permute(0, 2, 3, 1))
 
 
-@pytest.mark.parametrize("B,H,sq,skv", [(1, 1, 128, 128), (2, 3, 256, 256), (2, 2, 333, 333),
-                                        (2, 4, 256, 77), (1, 2, 1024, 1024), (2, 1, 130, 500)])
+# dispatch (csrc/hp_attn.cu hp_attention): one key block -> single-block CTAs;
+# else two-query-tile CTAs ("pair") unless that grid leaves a short last wave
+# (tail*2 < 148 SMs) -> split-KV CTAs. Each path with and without the
+# partial-key-block mask (S_kv % 128 != 0):
+ATTN_SHAPES = [
+    (1, 1, 128, 128), (2, 4, 256, 77),                    # single block
+    (2, 3, 256, 256), (1, 2, 1024, 1024),                 # split-KV, unmasked
+    (2, 2, 333, 333), (2, 1, 130, 500),                   # split-KV, masked
+    (2, 10, 4096, 4096), (2, 20, 1024, 1024),             # split-KV at the SDXL-1024 shapes (B=2)
+    (1, 37, 1024, 1024), (1, 20, 1024, 1024),             # pair, unmasked (grid 148: no tail / tail 80)
+    (2, 24, 4429, 4429),                                  # pair, masked: SD3-1024 joint attention
+    (1, 24, 4429, 4429),                                  # SD3 at B=1 (one branch per GPU)
+    (1, 2, 16384, 16384),                                 # SDXL-2048 level-1 sequence length
+]
+
+
+@pytest.mark.parametrize("B,H,sq,skv", ATTN_SHAPES)
 def test_attention(B, H, sq, skv):
     torch.manual_seed(sq + skv)
     q = rnd(B * sq, H * 64)
@@ -117,7 +132,7 @@ def test_attention_fused_qkv_columns():
 
 @pytest.mark.parametrize("n,hw,c,c2,silu", [(2, 4096, 320, 0, True), (2, 1024, 1280, 640, False),
                                             (1, 256, 960, 0, True),
-                                            # >= 32 KB pixel chunks: staged in shared memory
+                                            # >= 16 KB pixel chunks: staged in shared memory
                                             (2, 16384, 320, 0, True), (2, 4096, 640, 640, True),
                                             (2, 1024, 1280, 1280, False)])
 def test_group_norm(n, hw, c, c2, silu):

@@ -3,10 +3,15 @@ drop-in engine, against the fp32 torch reference network and against the
 REFERENCE ENGINE run with the same network at its seam (golden fixtures from
 oracle/gen_golden_unet.py, BASELINE config 1).
 
-Tolerances (stated, bf16 compute / fp32 latent): one forward: max-abs <= 5e-2
-of max|eps_ref| and mean-abs <= 1e-2 of mean|eps_ref|; 20-step x0 vs the
-reference engine: max-abs <= 5e-2, mean-abs <= 1e-2 (latents are O(1)).
-Schedules (tau1, tau2, stage labels, series keys) must be identical.
+Tolerances (stated, bf16 compute / fp32 latent): one forward: max-abs <= 3e-2
+of max|eps_ref| and mean-abs <= 2e-2 of mean|eps_ref| (the full-shape
+forwards in test_fullshape_gpu.py are also held to the stock-torch bf16
+yardstick); 20-step x0 vs the
+reference engine: max-abs <= 1e-2 (north_star's bf16 bound), mean-abs <= 2e-3
+(latents are O(1)). Schedules (tau1, tau2, stage labels, series keys) must be
+identical, including a case where the slope detector fires naturally on the
+network's M_t (``hybrid_natural``) and one where it runs and must not fire
+(``hybrid_survey``); the slope margin at every decision step is printed.
 """
 import json
 import os
@@ -21,6 +26,10 @@ from paper_2602_21760_b200.denoiser.unet import UNet
 from paper_2602_21760_b200.denoiser.weights import TINY, init_weights, synthetic_conditioning, unet_param_specs
 
 pytestmark = pytest.mark.gpu
+
+# measured on B200: config-1 x0 max-abs 5.2e-3, mean-abs
+# 1.0e-3, M_t rel 6e-3 vs the reference engine's fp32 run; bounds with ~2x headroom
+X0_MAX, X0_MEAN = 1e-2, 2e-3
 
 
 @pytest.fixture(scope="module")
@@ -48,8 +57,10 @@ def test_forward_matches_fp32_reference(tiny):
     eps = net.forward(x.bfloat16(), t, key="k").float()
     ref = _ref_net(W)(x.permute(0, 3, 1, 2), t, ctx, pooled).permute(0, 2, 3, 1)
     err = (eps - ref).abs()
-    assert err.max().item() <= 5e-2 * ref.abs().max().item()
-    assert err.mean().item() <= 1e-2 * ref.abs().mean().item()
+    print(f"PARITY tiny forward: max_abs={err.max().item():.4g} of max|ref| {ref.abs().max().item():.4g}, "
+          f"mean_abs={err.mean().item():.4g} of mean|ref| {ref.abs().mean().item():.4g}")
+    assert err.max().item() <= 3e-2 * ref.abs().max().item()
+    assert err.mean().item() <= 2e-2 * ref.abs().mean().item()
 
 
 def test_batch_invariance_bitwise(tiny):
@@ -73,7 +84,19 @@ def golden(golden_dir):
     return meta, np.load(os.path.join(golden_dir, "unet_tiny.npz"))
 
 
-@pytest.mark.parametrize("case", ["serial", "hybrid_cap", "hybrid_k0"])
+def _slope_margins(series, sw):
+    """Per measured step s >= L+1 (up to tau1): G = (M_t - M_{t+L}) / L (monitor.py:121-132)
+    and its distance to the firing interval [0, g_slope) edges."""
+    m = dict(series)
+    out = []
+    for t in sorted(m, reverse=True):
+        if t + sw["L"] in m:
+            G = (m[t] - m[t + sw["L"]]) / sw["L"]
+            out.append((t, G, min(abs(G), abs(sw["g_slope"] - G))))
+    return out
+
+
+@pytest.mark.parametrize("case", ["serial", "hybrid_cap", "hybrid_k0", "hybrid_natural", "hybrid_survey"])
 def test_engine_matches_reference_engine_with_seam(tiny, golden, case):
     W, cond = tiny
     meta, arrays = golden
@@ -85,19 +108,33 @@ def test_engine_matches_reference_engine_with_seam(tiny, golden, case):
         from dataclasses import replace
         plan = replace(plan, switch=hp.SwitchConfig(**c["switch"]))
     res = hp.run_plan(plan)
+    # the switch schedule is bit-exact: tau1, tau2, stage labels via the series keys
     assert (res.tau1, res.tau2) == (c["tau1"], c["tau2"])
     assert [t for t, _ in res.series] == [t for t, _ in c["series"]]
     ref = arrays[case]
     err = np.abs(res.x0 - ref)
-    assert err.max() <= 5e-2, err.max()
-    assert err.mean() <= 1e-2, err.mean()
-    np.testing.assert_allclose([m for _, m in res.series], [m for _, m in c["series"]], rtol=2e-2)
-    # the switch schedule from the GPU-measured series equals the reference controller's
+    m_rel = np.abs(np.array([m for _, m in res.series]) / np.array([m for _, m in c["series"]]) - 1.0)
+    print(f"PARITY config1 {case}: x0 max_abs={err.max():.4g} mean_abs={err.mean():.4g} "
+          f"M_t max_rel={m_rel.max():.3g}")
+    assert err.max() <= X0_MAX, err.max()
+    assert err.mean() <= X0_MEAN, err.mean()
+    assert m_rel.max() <= 1.5e-2
     if "switch" in c:
-        st, labels = hp.replay_series([(t, m) for t, m in res.series], hp.SwitchConfig(**c["switch"])) \
-            if c["switch"]["k"] == 0 else (None, None)
-        if st is not None:
+        sw = c["switch"]
+        # the reference controller replayed on the GPU-measured series fires at the same step
+        if sw["k"] == 0 or res.tau1 is not None:
+            st, _ = hp.replay_series([(t, m) for t, m in res.series if t >= meta["T"] - res.tau1 + 1],
+                                     hp.SwitchConfig(**sw))
             assert st.tau1 == res.tau1
+        margins = _slope_margins(res.series, sw)
+        gpu_G = {t: G for t, G, _ in margins}
+        ref_G = {t: G for t, G, _ in _slope_margins(c["series"], sw)}
+        for t, G, marg in margins:
+            if meta["T"] - t + 1 <= res.tau1:
+                print(f"  s={meta['T'] - t + 1} G_gpu={G:.6g} G_ref={ref_G[t]:.6g} "
+                      f"|dG|={abs(G - ref_G[t]):.3g} margin_to_edges={marg:.3g}")
+                # the decision is robust: the bf16-vs-fp32 slope error is far inside the margin
+                assert abs(G - ref_G[t]) < 0.25 * marg
 
 
 def test_serial_fcp_k0_bit_identical_on_gpu(tiny):
