@@ -82,23 +82,43 @@ def initial_latents(weights, means, variances, cond_rows, seed, ab_T):
     return np.sqrt(ab_T) * x0 + np.sqrt(1.0 - ab_T) * e
 
 
-def run_exact(den, x, T, w, abar, sig):
+def _update(x, e, t, T, abar, sig, update):
+    """ddim_step (schedules.py:152-168) or fm_euler_step (schedules.py:171-182)
+    at t_cont = t/T, dt = 1/T (the engine's FM parameterisation)."""
+    if update == "euler":
+        return smp.euler(x, e, 1.0 / T)
+    return smp.ddim(x, e, t, abar, sig)
+
+
+def run_exact(den, x, T, w, abar, sig, update="ddim"):
     """Serial / full condition partitioning (engine.py:195-251): every step exact."""
     series = []
     for t in range(T, 0, -1):
         ec, eu = den.branches(x, t)
         series.append((t, smp.rel_mae(ec, eu)))
-        x = smp.ddim(x, smp.cfg(ec, eu, w), t, abar, sig)
+        x = _update(x, smp.cfg(ec, eu, w), t, T, abar, sig, update)
     return x, series
 
 
-def run_staged(den, x, T, w, abar, sig, L, g, tau_cap, k, fractions):
-    """_run_staged (engine.py:264-304): warm-up, pipelined window, reconnect."""
+def run_staged(den, x, T, w, abar, sig, L, g, tau_cap, k, fractions, update="ddim",
+               pipeline="reference_blend"):
+    """_run_staged (engine.py:264-304): warm-up, pipelined window, reconnect.
+
+    ``update="euler"``: the same loop with fm_euler_step (schedules.py:171-182) in
+    place of ddim_step -- BASELINE config 3's flow-matching staged loop, which the
+    reference engine (DDIM-only, engine.py:31) composes from its public pieces.
+    ``pipeline="stage_split"``: the window runs the network split into
+    len(fractions) stages (``den`` is an ``oracle.stage_ref.StagedNet``), stage j
+    on the boundary state stage j-1 produced at the previous step, filled from
+    the conditional forward of the last measured step (paper_2602_21760_b200/
+    stages.py states the convention); ``reference_blend`` is engine.py:254-261."""
     n = len(fractions)
     state = {"steps": 0, "tau1": None, "tau2": None}
     series: dict = {}
     history: list = []
     labels = []
+    prev = None
+    bstate = None
     for s in range(1, T + 1):
         t = T - s + 1
         history = [x] + history[:n - 1]
@@ -106,18 +126,24 @@ def run_staged(den, x, T, w, abar, sig, L, g, tau_cap, k, fractions):
             ec, eu = den.branches(x, t)
             series[t] = smp.rel_mae(ec, eu)
             label = ctl.step(state, series, t, L, g, tau_cap, k)
-            x = smp.ddim(x, smp.cfg(ec, eu, w), t, abar, sig)
+            x = _update(x, smp.cfg(ec, eu, w), t, T, abar, sig, update)
         else:
             label = ctl.step(state, series, t, L, g, tau_cap, k)
-            if label == ctl.PAR:
+            if label == ctl.PAR and pipeline == "stage_split":
+                if prev != ctl.PAR:
+                    bstate = den.recorded()                      # fill from the last exact forward
+                est, bstate = den.window_step(x, bstate, t)
+                x = _update(x, est, t, T, abar, sig, update)
+            elif label == ctl.PAR:
                 est = np.zeros_like(history[0])                   # _pipelined_estimate :254-261
                 for d, f in enumerate(fractions):
                     est += f * den.conditional(history[min(d, len(history) - 1)], t)
-                x = smp.ddim(x, est, t, abar, sig)
+                x = _update(x, est, t, T, abar, sig, update)
             else:
                 ec, eu = den.branches(x, t)
                 series[t] = smp.rel_mae(ec, eu)
-                x = smp.ddim(x, smp.cfg(ec, eu, w), t, abar, sig)
+                x = _update(x, smp.cfg(ec, eu, w), t, T, abar, sig, update)
         labels.append(label)
+        prev = label
     ser = sorted(series.items(), key=lambda kv: -kv[0])
     return x, ser, state["tau1"], state["tau2"], labels

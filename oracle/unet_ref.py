@@ -80,46 +80,96 @@ class UNetRef:
         h = self._lin(h, name + ".proj_out")
         return h.reshape(B, H, Wd, C).permute(0, 3, 1, 2) + x
 
-    def __call__(self, x_nchw, t, context, pooled):
-        """x [B, C, H, W] fp32, t [B] timesteps, context [B, L, D], pooled [B, P] -> eps NCHW."""
+    def _emb(self, t, pooled, B, device):
         s = self.s
-        B = x_nchw.shape[0]
-        x_nchw = x_nchw.to(self.dt)
         temb = self._lin(F.silu(self._lin(_sinus(t, s.block_out[0]).to(self.dt), "time_embedding.linear_1")),
                          "time_embedding.linear_2")
         size = 8.0 * s.latent_hw
-        ids = torch.tensor([size, size, 0.0, 0.0, size, size], device=x_nchw.device).repeat(B, 1).reshape(-1)
+        ids = torch.tensor([size, size, 0.0, 0.0, size, size], device=device).repeat(B, 1).reshape(-1)
         tid = _sinus(ids, s.time_id_dim).reshape(B, -1)
         a = torch.cat([pooled.float(), tid], dim=1).to(self.dt)
-        emb = temb + self._lin(F.silu(self._lin(a, "add_embedding.linear_1")), "add_embedding.linear_2")
+        return temb + self._lin(F.silu(self._lin(a, "add_embedding.linear_1")), "add_embedding.linear_2")
+
+    def run_units(self, state, t, context, pooled, a, b):
+        """Units [a, b) of ``ref_units(spec)`` on a boundary state: ``{"x": NCHW
+        latent}`` before unit 0, ``{"eps": NCHW}`` after the last, else ``{"h":
+        NCHW activation, "skips": [pushed skips]}`` (the stage-split pipeline's
+        unit of hand-off; every stage embeds the current step's t)."""
+        s = self.s
+        units = ref_units(s)
+        if a == 0:
+            x = state["x"].to(self.dt)
+            h, skips = None, []
+        else:
+            h, skips = state["h"], list(state["skips"])
+        B = (x if a == 0 else h).shape[0]
+        emb = self._emb(t, pooled, B, (x if a == 0 else h).device)
         ctx = context.to(self.dt)
-        h = self._conv(x_nchw, "conv_in")
-        skips = [h]
-        ch = s.block_out
-        for lvl in range(len(ch)):
-            for j in range(s.layers_per_block):
-                h = self._res(h, f"down_blocks.{lvl}.resnets.{j}", emb)
-                if s.transformer_depth[lvl]:
-                    h = self._transformer(h, ctx, f"down_blocks.{lvl}.attentions.{j}", s.transformer_depth[lvl])
+        depth = {"down": s.transformer_depth, "up": s.transformer_depth[::-1]}
+        for u in units[a:b]:
+            kind = u[0]
+            if kind == "conv_in":
+                h = self._conv(x, "conv_in")
                 skips.append(h)
-            if lvl < len(ch) - 1:
-                h = self._conv(h, f"down_blocks.{lvl}.downsamplers.0.conv", stride=2)
+            elif kind == "res":
+                _, where, lvl, j, push = u
+                name = f"mid_block.resnets.{j}" if where == "mid" else f"{where}_blocks.{lvl}.resnets.{j}"
+                if where == "up":
+                    h = torch.cat([h, skips.pop()], dim=1)
+                h = self._res(h, name, emb)
+                if push:
+                    skips.append(h)
+            elif kind == "attn":
+                _, where, lvl, j, push = u
+                if where == "mid":
+                    h = self._transformer(h, ctx, "mid_block.attentions.0", s.mid_depth)
+                else:
+                    h = self._transformer(h, ctx, f"{where}_blocks.{lvl}.attentions.{j}", depth[where][lvl])
+                if push:
+                    skips.append(h)
+            elif kind == "ds":
+                h = self._conv(h, f"down_blocks.{u[1]}.downsamplers.0.conv", stride=2)
                 skips.append(h)
-        h = self._res(h, "mid_block.resnets.0", emb)
-        h = self._transformer(h, ctx, "mid_block.attentions.0", s.mid_depth)
-        h = self._res(h, "mid_block.resnets.1", emb)
-        for u in range(len(ch)):
-            lvl = len(ch) - 1 - u
-            for j in range(s.layers_per_block + 1):
-                h = torch.cat([h, skips.pop()], dim=1)
-                h = self._res(h, f"up_blocks.{u}.resnets.{j}", emb)
-                if s.transformer_depth[lvl]:
-                    h = self._transformer(h, ctx, f"up_blocks.{u}.attentions.{j}", s.transformer_depth[lvl])
-            if u < len(ch) - 1:
+            elif kind == "us":
                 h = F.interpolate(h, scale_factor=2.0, mode="nearest")
-                h = self._conv(h, f"up_blocks.{u}.upsamplers.0.conv")
-        h = F.silu(self._gn(h, "conv_norm_out"))
-        return self._conv(h, "conv_out").float()
+                h = self._conv(h, f"up_blocks.{u[1]}.upsamplers.0.conv")
+            elif kind == "out":
+                h = F.silu(self._gn(h, "conv_norm_out"))
+                return {"eps": self._conv(h, "conv_out").float()}
+        return {"h": h, "skips": skips}
+
+    def __call__(self, x_nchw, t, context, pooled):
+        """x [B, C, H, W] fp32, t [B] timesteps, context [B, L, D], pooled [B, P] -> eps NCHW."""
+        return self.run_units({"x": x_nchw}, t, context, pooled, 0, len(ref_units(self.s)))["eps"]
+
+
+def ref_units(s) -> list:
+    """The forward's units in execution order (diffusers UNet2DConditionModel
+    order): conv_in; per down level (resnet[, transformer]) x layers, then the
+    downsampler; mid resnet, transformer, resnet; per up level (resnet[,
+    transformer]) x (layers + 1), then the upsampler; norm_out + conv_out.
+    ``push``: the unit's output is pushed as a skip."""
+    ch = s.block_out
+    out = [("conv_in",)]
+    for lvl in range(len(ch)):
+        d = s.transformer_depth[lvl]
+        for j in range(s.layers_per_block):
+            out.append(("res", "down", lvl, j, not d))
+            if d:
+                out.append(("attn", "down", lvl, j, True))
+        if lvl < len(ch) - 1:
+            out.append(("ds", lvl))
+    out += [("res", "mid", 0, 0, False), ("attn", "mid", 0, 0, False), ("res", "mid", 0, 1, False)]
+    for u in range(len(ch)):
+        d = s.transformer_depth[len(ch) - 1 - u]
+        for j in range(s.layers_per_block + 1):
+            out.append(("res", "up", u, j, False))
+            if d:
+                out.append(("attn", "up", u, j, False))
+        if u < len(ch) - 1:
+            out.append(("us", u))
+    out.append(("out",))
+    return out
 
 
 def net_timestep(t: int, T: int) -> float:

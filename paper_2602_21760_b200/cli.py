@@ -66,6 +66,8 @@ def _plan(cfg, args, **kw):
         plan = replace(plan, denoiser=den)
     if getattr(args, "clock", None):
         plan = replace(plan, clock=args.clock)
+    if getattr(args, "pipeline_numerics", None):
+        plan = replace(plan, pipeline_numerics=args.pipeline_numerics)
     return plan
 
 
@@ -222,7 +224,9 @@ def _parser() -> argparse.ArgumentParser:
     common = dict(config=dict(help="experiment JSON; defaults apply if omitted"),
                   denoiser=dict(choices=["gmm", "tiny", "sdxl", "tiny-dit", "sd3"], default="gmm",
                                 help="branch evaluator at the seam"),
-                  clock=dict(choices=["model", "device"], default=None, help="trace clock"))
+                  clock=dict(choices=["model", "device"], default=None, help="trace clock"),
+                  **{"pipeline-numerics": dict(choices=["reference_blend", "stage_split"], default=None,
+                                               help="window numerics (stage_split needs a network denoiser)")})
     specs = {
         "simulate": (simulate, "run one plan and write metrics + trace",
                      [("--variant", dict(choices=[v.value for v in PlanVariant])), ("--seed", dict(type=int)),

@@ -19,6 +19,7 @@ from __future__ import annotations
 import torch
 
 from .. import _native as N
+from ..stages import Boundary, stage_bounds, state_rows
 from . import kernels as K
 
 
@@ -97,6 +98,8 @@ class NetDenoiser:
         self.g_both = _Graphed(both, self.x_both, self.t_both, use_graph)
         self.g_cond = _Graphed(cond, self.x_cond, self.t_cond, use_graph)
         self._slot = half.view(self.B, self.numel)
+        self.use_graph = use_graph
+        self.cuts = None
 
     def input_slot(self):
         """bf16 [B, N] buffer the sampler kernel writes the next latent into."""
@@ -132,3 +135,83 @@ class NetDenoiser:
         self.x_unc.view(self.B, self.numel).copy_(x.to(torch.bfloat16).view(self.B, self.numel))
         self._set_t(self.t_unc, t)
         return self.g_uncond.run().reshape(self.B, self.numel)
+
+    # ---- stage-split pipeline window (stages.py) -------------------------------------
+    def enable_stage_split(self, cuts) -> None:
+        """Split the network at unit indices ``cuts`` (network order). The CFG
+        forward is re-captured so it keeps the boundary states at the cuts (its
+        conditional rows fill the window's first step); one graph per stage runs
+        the conditional rows of that stage on static boundary buffers."""
+        cuts = tuple(int(c) for c in cuts)
+        if cuts == self.cuts:
+            return
+        net, B = self.net, self.B
+        U = len(net.units)
+        self.cuts = cuts
+        self.bounds = stage_bounds(cuts, U)
+        self._rec = None
+
+        def both(x, t):
+            x[B:].copy_(x[:B])
+            rec = {c: None for c in cuts}
+            out = net.run_units({"x": x}, t, "both", 0, U, record=rec)["eps"]
+            self._rec = rec
+            return out
+        self.g_both = _Graphed(both, self.x_both, self.t_both, self.use_graph)
+        self.g_both.run()                                    # capture; defines the recorded states
+        # boundary j (input of stage j >= 1) holds the conditional rows [B, 2B)
+        self.bnd = [None] + [Boundary(state_rows(self._rec[c], B, 2 * B), self.dev) for c in cuts]
+        self.x_stage = torch.zeros((B,) + self.shape, dtype=torch.bfloat16, device=self.dev)
+        self.t_stage = torch.zeros(B, dtype=torch.float32, device=self.dev)
+        self.g_stage = [None] * len(self.bounds)
+
+    @property
+    def n_stages(self) -> int:
+        return len(self.bounds)
+
+    def _stage_fn(self, j):
+        a, b = self.bounds[j]
+        last = j == len(self.bounds) - 1
+
+        def fn(_x, t):
+            st = {"x": self.x_stage} if j == 0 else self.bnd[j].state()
+            out = self.net.run_units(st, t, "cond", a, b)
+            if last:
+                return out["eps"]
+            self.bnd[j + 1].load(out)                        # hand-off buffer (one message)
+            return self.bnd[j + 1].buf
+        return fn
+
+    def stage_run(self, j: int, t: int):
+        """Run network stage j at timestep t on its static input (``stage_input``);
+        the last stage returns eps [B, N] bf16, the others fill ``bnd[j+1]``."""
+        if self.g_stage[j] is None:
+            self.g_stage[j] = _Graphed(self._stage_fn(j), None, self.t_stage, self.use_graph)
+        self._set_t(self.t_stage, t)
+        out = self.g_stage[j].run()
+        return out.reshape(self.B, self.numel) if j == len(self.bounds) - 1 else out
+
+    def stage_input(self, j: int):
+        """The static input buffer of stage j: the bf16 latent for j = 0, else the
+        contiguous boundary buffer (what an upstream rank pushes into)."""
+        return self.x_stage if j == 0 else self.bnd[j].buf
+
+    def load_stage_x(self, x) -> None:
+        self.x_stage.view(self.B, self.numel).copy_(x.to(torch.bfloat16).view(self.B, self.numel))
+
+    def window_fill(self) -> None:
+        """Boundary states of the last CFG forward's conditional rows -> stage inputs."""
+        for j, c in enumerate(self.cuts, start=1):
+            self.bnd[j].load(state_rows(self._rec[c], self.B, 2 * self.B))
+
+    def window_step(self, x, t):
+        """One pipelined step on one device: every stage on its stale input, last
+        stage first so each stage reads its input before the upstream stage
+        overwrites it. Returns the unguided eps estimate [B, N]."""
+        self.load_stage_x(x)
+        eps = None
+        for j in reversed(range(len(self.bounds))):
+            out = self.stage_run(j, t)
+            if j == len(self.bounds) - 1:
+                eps = out
+        return eps

@@ -90,27 +90,64 @@ class MMDiT:
         p = K.linear_small(_f32(pooled.to(self.dev)), self.p1w, self.p1b, act_out=K.ACT_SILU)
         self.pemb[key] = K.linear_small(p, self.p2w, self.p2b)
 
-    def forward(self, x: torch.Tensor, t: torch.Tensor, key="default") -> torch.Tensor:
+    @property
+    def units(self):
+        """Forward units (stage-split granularity): patch + context embedding, the
+        joint blocks, the output head."""
+        return [("embed",)] + [("block", d) for d in range(self.spec.depth)] + [("out",)]
+
+    @property
+    def unit_flops(self):
+        return [f for _, f in mmdit_units(self.spec)]
+
+    def run_units(self, state: dict, t: torch.Tensor, key: str, a: int, b: int, record=None) -> dict:
+        """Units [a, b) on a boundary state: ``{"x": latent}`` before unit 0,
+        ``{"eps": velocity}`` after the last, else ``{"X": joint token buffer
+        [n, Ti + L, H], "hw": (Hl, Wl)}``. The conditioning vector is recomputed
+        from the current step's t in every stage. ``record``: {unit index: None}
+        filled with a COPY of the token buffer entering each listed unit (the
+        blocks update it in place)."""
         s = self.spec
         H, P = s.hidden, s.patch
-        n, Hl, Wl, C = x.shape
-        Ti = (Hl // P) * (Wl // P)
         L = s.ctx_len
-        T = Ti + L
         heads = s.heads
-        X = torch.empty((n, T, H), dtype=torch.bfloat16, device=x.device)
-        tok = K.patchify(x, n, Hl, Wl, C, P).view(n, Ti, P * P * C)
-        K.gemm(tok, self.patch_w, bias=self.patch_b, residual=self.pos, out=X[:, :Ti])
-        X[:, Ti:].copy_(self.ctx_cache[key])
+        if a == 0:
+            x = state["x"]
+            n, Hl, Wl, C = x.shape
+        else:
+            X = state["X"]
+            n = X.shape[0]
+            Hl, Wl = state["hw"]
+            C = s.in_channels
+        Ti = (Hl // P) * (Wl // P)
+        T = Ti + L
+        dev = self.dev
         te = K.timestep_embedding(t, s.freq_dim)
         te = K.linear_small(te, self.t1w, self.t1b, act_out=K.ACT_SILU)
         c = K.linear_small(te, self.t2w, self.t2b) + self.pemb[key]
-        qkv = torch.empty((n, T, 3 * H), dtype=torch.bfloat16, device=x.device)
-        att = torch.empty((n, T, H), dtype=torch.bfloat16, device=x.device)
-        hid_i = torch.empty((n, Ti, s.mlp_ratio * H), dtype=torch.bfloat16, device=x.device)
-        hid_c = torch.empty((n, L, s.mlp_ratio * H), dtype=torch.bfloat16, device=x.device)
+        qkv = torch.empty((n, T, 3 * H), dtype=torch.bfloat16, device=dev)
+        att = torch.empty((n, T, H), dtype=torch.bfloat16, device=dev)
+        hid_i = torch.empty((n, Ti, s.mlp_ratio * H), dtype=torch.bfloat16, device=dev)
+        hid_c = torch.empty((n, L, s.mlp_ratio * H), dtype=torch.bfloat16, device=dev)
         scale = 1.0 / math.sqrt(H // heads)
-        for blk in self.blocks:
+        units = self.units
+        for i in range(a, b):
+            u = units[i]
+            if record is not None and i in record:
+                record[i] = {"X": X.clone(), "hw": (Hl, Wl)}
+            if u[0] == "embed":
+                X = torch.empty((n, T, H), dtype=torch.bfloat16, device=dev)
+                tok = K.patchify(x, n, Hl, Wl, C, P).view(n, Ti, P * P * C)
+                K.gemm(tok, self.patch_w, bias=self.patch_b, residual=self.pos, out=X[:, :Ti])
+                X[:, Ti:].copy_(self.ctx_cache[key])
+                continue
+            if u[0] == "out":
+                nf = K.linear_small(c, self.nout_w, self.nout_b, act_in=K.ACT_SILU)     # [n, 2H]: scale, shift
+                Y = K.layer_norm_joint(X, H, T, Ti, nf[:, H:2 * H], nf[:, 0:H], nf[:, H:2 * H], nf[:, 0:H], 2 * H)
+                o = K.gemm(Y[:, :Ti], self.out_w, bias=self.out_b)                       # [n, Ti, P*P*C]
+                v = K.patchify(o, n, Hl, Wl, C, P, inverse=True)
+                return {"eps": v.view(n, Hl, Wl, C)}
+            blk = self.blocks[u[1]]
             last = blk["last"]
             mod = K.linear_small(c, blk["mod_w"], blk["mod_b"], act_in=K.ACT_SILU)   # [n, 12H] (8H last)
             ldm = mod.shape[1]
@@ -145,11 +182,25 @@ class MMDiT:
                 K.gemm(Y[:, Ti:], blk["m1_c_w"], bias=blk["m1_c_b"], act=K.ACT_GELU, out=hid_c)
                 K.gemm(hid_c, blk["m2_c_w"], bias=blk["m2_c_b"], residual=X[:, Ti:], colscale=mc[:, 5 * H:6 * H],
                        out=X[:, Ti:])
-        nf = K.linear_small(c, self.nout_w, self.nout_b, act_in=K.ACT_SILU)        # [n, 2H]: scale, shift
-        Y = K.layer_norm_joint(X, H, T, Ti, nf[:, H:2 * H], nf[:, 0:H], nf[:, H:2 * H], nf[:, 0:H], 2 * H)
-        o = K.gemm(Y[:, :Ti], self.out_w, bias=self.out_b)                          # [n, Ti, P*P*C]
-        v = K.patchify(o, n, Hl, Wl, C, P, inverse=True)
-        return v.view(n, Hl, Wl, C)
+        return {"X": X, "hw": (Hl, Wl)}
+
+    def forward(self, x: torch.Tensor, t: torch.Tensor, key="default") -> torch.Tensor:
+        return self.run_units({"x": x}, t, key, 0, len(self.units))["eps"]
+
+
+def mmdit_units(spec: MMDiTSpec) -> list:
+    """(unit, FLOPs for one image) in forward order; sums to ``mmdit_flops(spec, 1)``."""
+    s = spec
+    H = s.hidden
+    Ti = (s.latent_hw // s.patch) ** 2
+    T = Ti + s.ctx_len
+    out = [(("embed",), 2.0 * Ti * (s.patch ** 2 * s.in_channels) * H)]
+    for d in range(s.depth):
+        rows_out = Ti if d == s.depth - 1 else T
+        f = 2.0 * T * H * 3 * H + 4.0 * T * T * H + 2.0 * rows_out * H * H + 2 * 2.0 * rows_out * H * s.mlp_ratio * H
+        out.append((("block", d), f))
+    out.append((("out",), 2.0 * Ti * H * s.patch ** 2 * s.in_channels))
+    return out
 
 
 def build_mmdit(spec: MMDiTSpec, seed: int = 0, device="cuda", weights: dict | None = None) -> MMDiT:

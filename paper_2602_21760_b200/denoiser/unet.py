@@ -228,6 +228,10 @@ class UNet:
         self.tproj_slot = {id(r): (off, r.c1.co) for r, off in zip(blocks, offs)}
         for r in blocks:
             r.tproj = None
+        spec_units = unet_units(s)
+        self.units = [u for u, _, _ in spec_units]
+        self.unit_flops = [f for _, f, _ in spec_units]
+        self._levels = [lv for _, _, lv in spec_units]
 
     def _row_stats(self, floats: int) -> "K.RowStats":
         rs = getattr(self, "_rs", None)
@@ -260,53 +264,160 @@ class UNet:
         a = K.linear_small(add_in, self.a1.w, self.a1.b, act_out=K.ACT_SILU)
         self.aug[key] = K.linear_small(a, self.a2.w, self.a2.b)
 
-    def forward(self, x: torch.Tensor, t: torch.Tensor, key="default") -> torch.Tensor:
-        """x: [n, H, W, in_ch] bf16 NHWC; t: [n] fp32 timesteps -> eps [n, H, W, out_ch] bf16."""
+    def _prologue(self, t: torch.Tensor, key: str) -> torch.Tensor:
+        """Per-step embeddings: every ResBlock's time-embedding bias for timestep t
+        (one batched GEMV over all blocks) -> [n, sum(co)] fp32."""
         s = self.spec
-        n, H, Wd = x.shape[0], x.shape[1], x.shape[2]
-        st, g = self.stats, s.groups
-        rs = self._row_stats(2 * n * H * Wd * max(c // 4 ** l for l, c in enumerate(s.block_out)) // 64)
         te = K.timestep_embedding(t, s.block_out[0])
         te = K.linear_small(te, self.t1.w, self.t1.b, act_out=K.ACT_SILU)
         temb = K.linear_small(te, self.t2.w, self.t2.b)
         temb = temb + self.aug[key]                    # tiny [n, 1280] add
-        tb_all = K.linear_small(temb, self.tproj_w, self.tproj_b, act_in=K.ACT_SILU)   # [n, sum(co)]
+        return K.linear_small(temb, self.tproj_w, self.tproj_b, act_in=K.ACT_SILU)
+
+    def run_units(self, state: dict, t: torch.Tensor, key: str, a: int, b: int, record=None) -> dict:
+        """Execute units [a, b) of the forward (``unet_units`` order) on a boundary
+        state and return the boundary state after unit b-1.
+
+        A boundary state is ``{"x": latent}`` before unit 0, ``{"eps": eps}``
+        after the last unit, else ``{"h": activation [n*hh*ww, c], "skips":
+        [pushed, not yet popped skip tensors], "hw": (hh, ww), "n": n}``. The
+        per-step time embedding is recomputed from t (stage-split pipelining runs
+        every stage at the current step's t, SPEC.md:390 / PAPER.md:45).
+
+        ``record``: {unit index: None} filled with the boundary state entering
+        each listed unit (tensor references: no unit writes a tensor it did
+        not create, so they stay valid until the next forward)."""
+        s = self.spec
+        st, g = self.stats, s.groups
+        units = self.units
+        if a == 0:
+            x = state["x"]
+            n, H, Wd = x.shape[0], x.shape[1], x.shape[2]
+            h, skips, (hh, ww) = None, [], (H, Wd)
+        else:
+            n, h, skips, (hh, ww) = state["n"], state["h"], list(state["skips"]), state["hw"]
+        full_hw = hh * (2 ** self._levels[a]) if a else hh       # latent side length
+        rs = self._row_stats(2 * n * full_hw * full_hw * max(c // 4 ** l for l, c in enumerate(s.block_out)) // 64)
+        tb_all = self._prologue(t, key) if any(u[0] in ("res",) for u in units[a:b]) else None
 
         def tb(r):
             off, co = self.tproj_slot[id(r)]
             return tb_all[:, off:off + co]             # row stride sum(co): GEMM bias2_ld
-        xp = K.copy_cols(x.view(n * H * Wd, s.in_channels), self.cin_pad)
-        h = K.gemm(xp, self.conv_in_w, bias=self.conv_in_b, conv=(n, H, Wd, self.cin_pad, 1))
-        skips = [h]
-        hh, ww = H, Wd
-        for res, att, ds in self.down:
-            for r, a in zip(res, att):
-                h = r(h, n, hh, ww, tb(r), g, st)
-                if a is not None:
-                    h = a(h, n, hh * ww, g, st, self.ctx_len, key, rs)
+        for i in range(a, b):
+            u = units[i]
+            kind = u[0]
+            if record is not None and i in record:
+                record[i] = {"h": h, "skips": list(skips), "hw": (hh, ww), "n": n}
+            if kind == "conv_in":
+                xp = K.copy_cols(x.view(n * hh * ww, s.in_channels), self.cin_pad)
+                h = K.gemm(xp, self.conv_in_w, bias=self.conv_in_b, conv=(n, hh, ww, self.cin_pad, 1))
                 skips.append(h)
-            if ds is not None:
-                h = ds(h, n, hh, ww, stride=2)
+            elif kind == "res":
+                _, where, lvl, j, push = u
+                r = self._res_of(where, lvl, j)
+                if where == "up":
+                    sk = skips.pop()
+                    h = K.concat_channels(h, h.shape[1], sk, sk.shape[1], n * hh * ww)
+                h = r(h, n, hh, ww, tb(r), g, st)
+                if push:
+                    skips.append(h)
+            elif kind == "attn":
+                _, where, lvl, j, push = u
+                h = self._attn_of(where, lvl, j)(h, n, hh * ww, g, st, self.ctx_len, key, rs)
+                if push:
+                    skips.append(h)
+            elif kind == "ds":
+                h = self.down[u[1]][2](h, n, hh, ww, stride=2)
                 hh, ww = hh // 2, ww // 2
                 skips.append(h)
-        r0, tr, r1 = self.mid
-        h = r0(h, n, hh, ww, tb(r0), g, st)
-        h = tr(h, n, hh * ww, g, st, self.ctx_len, key, rs)
-        h = r1(h, n, hh, ww, tb(r1), g, st)
-        for res, att, us in self.up:
-            for r, a in zip(res, att):
-                sk = skips.pop()
-                cat = K.concat_channels(h, h.shape[1], sk, sk.shape[1], n * hh * ww)
-                h = r(cat, n, hh, ww, tb(r), g, st)
-                if a is not None:
-                    h = a(h, n, hh * ww, g, st, self.ctx_len, key, rs)
-            if us is not None:
-                h = us.up(h, n, hh, ww)
+            elif kind == "us":
+                h = self.up[u[1]][2].up(h, n, hh, ww)
                 hh, ww = hh * 2, ww * 2
-        y = K.group_norm(h, n, hh * ww, s.block_out[0], self.norm_out.g, self.norm_out.b, groups=g, silu=True, stats=st)
-        e64 = K.gemm(y, self.conv_out_w, bias=self.conv_out_b, conv=(n, hh, ww, s.block_out[0], 1))
-        eps = K.copy_cols(e64, s.out_channels)
-        return eps.view(n, hh, ww, s.out_channels)
+            elif kind == "out":
+                y = K.group_norm(h, n, hh * ww, s.block_out[0], self.norm_out.g, self.norm_out.b, groups=g,
+                                 silu=True, stats=st)
+                e64 = K.gemm(y, self.conv_out_w, bias=self.conv_out_b, conv=(n, hh, ww, s.block_out[0], 1))
+                eps = K.copy_cols(e64, s.out_channels)
+                return {"eps": eps.view(n, hh, ww, s.out_channels)}
+        return {"h": h, "skips": skips, "hw": (hh, ww), "n": n}
+
+    def _res_of(self, where, lvl, j):
+        if where == "mid":
+            return self.mid[0] if j == 0 else self.mid[2]
+        return (self.down if where == "down" else self.up)[lvl][0][j]
+
+    def _attn_of(self, where, lvl, j):
+        if where == "mid":
+            return self.mid[1]
+        return (self.down if where == "down" else self.up)[lvl][1][j]
+
+    def forward(self, x: torch.Tensor, t: torch.Tensor, key="default") -> torch.Tensor:
+        """x: [n, H, W, in_ch] bf16 NHWC; t: [n] fp32 timesteps -> eps [n, H, W, out_ch] bf16."""
+        return self.run_units({"x": x}, t, key, 0, len(self.units))["eps"]
+
+
+def unet_units(spec: UNetSpec) -> list:
+    """The U-Net forward as a list of units, the granularity at which it can be
+    cut into pipeline stages, with each unit's FLOPs for ONE image (same
+    counting as ``unet_flops``) and the resolution level of its input.
+
+    Units: ("conv_in",), ("res", where, lvl, j, push), ("attn", where, lvl, j,
+    push), ("ds", lvl), ("us", u), ("out",); ``push`` = the unit ends a
+    (res[, attn]) group whose output is pushed as a skip."""
+    s = spec
+    ch = s.block_out
+    H = s.latent_hw
+    L = s.context_len
+    out = []
+
+    def conv(hw, ci, co, k=3):
+        return 2.0 * hw * ci * co * k * k
+
+    def res(hw, ci, co):
+        f = conv(hw, ci, co) + conv(hw, co, co)
+        if ci != co:
+            f += conv(hw, ci, co, 1)
+        return f
+
+    def tr(hw, c, depth):
+        f = 2 * 2.0 * hw * c * c
+        per = (2.0 * hw * c * 3 * c + 2.0 * hw * c * c + 4.0 * hw * hw * c + 2.0 * hw * c * c * 2
+               + 4.0 * hw * L * c + 2.0 * hw * c * 8 * c + 2.0 * hw * 4 * c * c)
+        return f + depth * per
+
+    out.append((("conv_in",), 2.0 * H * H * s.in_channels * ch[0] * 9, 0))
+    hw, lv, prev = H * H, 0, ch[0]
+    for lvl, co in enumerate(ch):
+        d = s.transformer_depth[lvl]
+        for j in range(s.layers_per_block):
+            out.append((("res", "down", lvl, j, not d), res(hw, prev if j == 0 else co, co), lv))
+            if d:
+                out.append((("attn", "down", lvl, j, True), tr(hw, co, d), lv))
+        prev = co
+        if lvl < len(ch) - 1:
+            out.append((("ds", lvl), conv(hw // 4, co, co), lv))
+            hw //= 4
+            lv += 1
+    out.append((("res", "mid", 0, 0, False), res(hw, ch[-1], ch[-1]), lv))
+    out.append((("attn", "mid", 0, 0, False), tr(hw, ch[-1], s.mid_depth), lv))
+    out.append((("res", "mid", 0, 1, False), res(hw, ch[-1], ch[-1]), lv))
+    skips = unet_skip_channels(s)
+    prev = ch[-1]
+    for u in range(len(ch)):
+        lvl = len(ch) - 1 - u
+        co = ch[lvl]
+        d = s.transformer_depth[lvl]
+        for j in range(s.layers_per_block + 1):
+            out.append((("res", "up", u, j, False), res(hw, prev + skips.pop(), co), lv))
+            prev = co
+            if d:
+                out.append((("attn", "up", u, j, False), tr(hw, co, d), lv))
+        if u < len(ch) - 1:
+            out.append((("us", u), conv(hw * 4, co, co) * 4 / 9, lv))
+            hw *= 4
+            lv -= 1
+    out.append((("out",), 2.0 * H * H * ch[0] * s.out_channels * 9, 0))
+    return out
 
 
 def build_unet(spec: UNetSpec, seed: int = 0, device="cuda", weights: dict | None = None) -> UNet:

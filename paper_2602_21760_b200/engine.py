@@ -19,7 +19,9 @@ Drop-in for the reference engine (engine.py:35-396): same ``PlanVariant``,
 Numeric contract (engine.py:1-20): measured steps are exact guided steps, so
 serial, full condition partitioning and an empty-window hybrid produce the
 same latents bit for bit; pipelined steps use the segment-blended conditional
-estimate of engine.py:254-261 (``pipeline_numerics="reference_blend"``).
+estimate of engine.py:254-261 (``pipeline_numerics="reference_blend"``), or
+the network split into stages fed with previous-step boundary states
+(``"stage_split"``, stages.py; north_star iii).
 """
 from __future__ import annotations
 
@@ -49,6 +51,7 @@ class PlanVariant(enum.Enum):
 STAGED = (PlanVariant.HYBRID, PlanVariant.BATCH_LEVEL, PlanVariant.LAYER_WISE)
 CLOCKS = ("model", "device")
 SAMPLERS = ("ddim", "euler")
+PIPELINE_NUMERICS = ("reference_blend", "stage_split")
 
 
 @dataclass(frozen=True)
@@ -90,8 +93,12 @@ class ExecutionPlan:
             raise PlanError(f"clock must be one of {CLOCKS}, got {self.clock!r}")
         if self.sampler not in SAMPLERS:
             raise PlanError(f"sampler must be one of {SAMPLERS}, got {self.sampler!r}")
-        if self.pipeline_numerics not in ("reference_blend",):
+        if self.pipeline_numerics not in PIPELINE_NUMERICS:
             raise PlanError(f"unknown pipeline_numerics {self.pipeline_numerics!r}")
+        if (self.pipeline_numerics == "stage_split" and self.variant in STAGED
+                and not hasattr(self.denoiser, "enable_stage_split")):
+            raise PlanError("pipeline_numerics='stage_split' needs a layered network denoiser "
+                            "(the analytic GMM has no stages)")
         nd = len(self.devices)
         v = self.variant
         if v is PlanVariant.SERIAL:
@@ -248,6 +255,11 @@ class _StepRunner:
         else:
             self.coef = {t: StepCoefficients.ddim(plan.schedule, t) for t in range(1, T + 1)}
         self.update = N.HP_UPDATE_EULER if plan.sampler == "euler" else N.HP_UPDATE_DDIM
+        self.split = plan.pipeline_numerics == "stage_split" and plan.variant in STAGED
+        if self.split:
+            from .stages import network_fractions, stage_cuts
+            fr = plan.segment_fractions or (0.5, 0.5)
+            self.den.enable_stage_split(stage_cuts(self.den.net.unit_flops, network_fractions(fr)))
 
     def reset(self):
         """Fresh controller + mirror for another run on the same runner."""
@@ -303,6 +315,14 @@ class _StepRunner:
                 acc = torch.empty(e.shape, dtype=x.dtype, device=x.device)
             K.blend_accumulate(acc, e, f, first=(d == 0))
         return self._advance(x, xb, acc, None, t, N.HP_CTRL_NONE)
+
+    def pipelined_split(self, x, xb, t, fill):
+        """Stage-split window step on one device (stages.py): every stage on its
+        previous-step input, then an unguided update."""
+        if fill:
+            self.den.window_fill()
+        eps = self.den.window_step(x, t)
+        return self._advance(x, xb, eps, None, t, N.HP_CTRL_NONE)
 
     def poll(self, t):
         mr = self.mirror.wait_step(t)
@@ -476,8 +496,12 @@ def _run_staged(plan: ExecutionPlan, fractions, x_init=None, to_host=True) -> Ru
         else:
             update_controller(host, no_series, t, sw)
             if host.stage is Stage.PARALLELISM:
-                x, xb = st.pipelined(history, fractions, t)
-                clock.pipelined_step(s, fill=prev is not Stage.PARALLELISM)
+                fill = prev is not Stage.PARALLELISM
+                if st.split:
+                    x, xb = st.pipelined_split(x, xb, t, fill)
+                else:
+                    x, xb = st.pipelined(history, fractions, t)
+                clock.pipelined_step(s, fill=fill)
             else:
                 x, xb = st.measured(x, xb, t, N.HP_CTRL_RECORD)
                 clock.measured_step(s, host.stage.value)

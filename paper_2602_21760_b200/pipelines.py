@@ -101,25 +101,25 @@ def build_sd3_denoiser(spec, n_prompts=1, steps=28, seed=0, use_graph=True, weig
 
 
 def sd3_plan(spec, *, variant="serial", steps=28, n_prompts=1, seed=0, guidance=5.0, denoiser=None,
-             switch_key="sd3", **kw) -> ExecutionPlan:
+             switch_key="sd3", switch=None, **kw) -> ExecutionPlan:
     """SD3-shaped MMDiT, flow-matching Euler (x_1 = x0 + e straight path, engine
     ``sampler="euler"``), CFG; BASELINE configs 3 and 5."""
     if denoiser is None:
         denoiser = build_sd3_denoiser(spec, n_prompts=n_prompts, steps=steps)
     numel = spec.latent_hw * spec.latent_hw * spec.in_channels
     return make_plan(variant=variant, denoiser=denoiser, schedule=sd3_schedule(steps), numel=numel,
-                     n_prompts=n_prompts, seed=seed, guidance=guidance, switch=SWITCH[switch_key],
+                     n_prompts=n_prompts, seed=seed, guidance=guidance, switch=switch or SWITCH[switch_key],
                      sampler="euler", **kw)
 
 
 def sdxl_plan(spec, *, variant="serial", steps=50, n_prompts=1, seed=0, guidance=5.0,
-              denoiser=None, switch_key=None, **kw) -> ExecutionPlan:
+              denoiser=None, switch_key=None, switch=None, **kw) -> ExecutionPlan:
     if denoiser is None:
         denoiser = build_sdxl_denoiser(spec, n_prompts=n_prompts, steps=steps)
     numel = spec.latent_hw * spec.latent_hw * spec.in_channels
     key = switch_key or ("tiny" if spec.name == "tiny" else "sdxl")
     return make_plan(variant=variant, denoiser=denoiser, schedule=sdxl_schedule(steps), numel=numel,
-                     n_prompts=n_prompts, seed=seed, guidance=guidance, switch=SWITCH[key], **kw)
+                     n_prompts=n_prompts, seed=seed, guidance=guidance, switch=switch or SWITCH[key], **kw)
 
 
 def build_sdxl_vae(spec=None, seed: int = 0, weights=None):
