@@ -180,6 +180,14 @@ int hp_signal(uint32_t* flag, uint32_t value, void* stream);
 int hp_flag_wait(const volatile uint32_t* flag, uint32_t value,
                  int32_t* status, uint64_t timeout_ns, void* stream);
 
+/* HOST-side wait: poll *flag (device memory, local or peer-mapped) with small
+ * D2H reads on a private non-blocking stream until *flag >= value; the value
+ * read is stored in *observed (may be NULL). No kernel waits, so ranks that
+ * share one GPU (tests) cannot stall each other's contexts; also used by
+ * passive ranks to learn the window's first step. HP_ERR_TIMEOUT after
+ * timeout_ns (0 = never). */
+int hp_flag_poll(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* observed);
+
 /* K3: copy nbytes from src (local) to dst (peer-mapped or local) with 16-byte
  * vector stores, then release-signal *flag = value (flag may be NULL).
  * engine.py:322-337 activation hand-off. */

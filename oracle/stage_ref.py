@@ -60,23 +60,32 @@ class StagedNet:
             return self.net.run_units(state, self._t(t, B), ctx, pooled, a, b)
 
     # ---- loop protocol -------------------------------------------------------------
-    def branches(self, x, t):
-        """Exact CFG branches; the conditional forward runs stage by stage so its
-        boundary states at the cuts are kept (the window's fill)."""
+    def cond(self, x, t):
+        """The conditional branch, run stage by stage so its boundary states at
+        the cuts are kept (the window's fill)."""
         B = x.shape[0]
-        xn = self._to_net(x)
-        st = {"x": xn}
+        st = {"x": self._to_net(x)}
         rec = []
         for j in range(len(self.edges) - 1):
             st = self._run(st, t, B, True, self.edges[j], self.edges[j + 1])
             if j < len(self.edges) - 2:
                 rec.append(st)
         self._rec = rec
-        ec = self._from_net(st["eps"])
+        return self._from_net(st["eps"])
+
+    def uncond(self, x, t):
+        B = x.shape[0]
         with torch.no_grad():
             ctx, pooled = self._ctx(B, False)
-            eu = self._from_net(self.net(xn, self._t(t, B), ctx, pooled))
-        return ec, eu
+            return self._from_net(self.net(self._to_net(x), self._t(t, B), ctx, pooled))
+
+    def branches(self, x, t):
+        """Exact CFG branches (eps_c, eps_u); records the conditional boundary states."""
+        return self.cond(x, t), self.uncond(x, t)
+
+    def stage(self, j, inp, t, B):
+        """Network stage j on its input (``{"x": net-layout latent}`` for j = 0)."""
+        return self._run(inp, t, B, True, self.edges[j], self.edges[j + 1])
 
     def conditional(self, x, t):
         B = x.shape[0]

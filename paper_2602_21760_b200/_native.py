@@ -87,6 +87,7 @@ SIGNATURES = {
     "hp_enable_peer": (C.c_int, [_I32]),
     "hp_signal": (C.c_int, [_VP, _U32, _VP]),
     "hp_flag_wait": (C.c_int, [_VP, _U32, _VP, C.c_uint64, _VP]),
+    "hp_flag_poll": (C.c_int, [_VP, _U32, C.c_uint64, C.POINTER(C.c_uint32)]),
     "hp_stage_send": (C.c_int, [_VP, _VP, _I64, _VP, _U32, _VP]),
     "hp_stage_broadcast": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int32, _VP, _I64, _U32, _VP]),
     "hp_alloc": (C.c_int, [_I64, C.POINTER(C.c_void_p)]),

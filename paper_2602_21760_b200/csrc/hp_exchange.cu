@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
+#include <chrono>
+#include <thread>
 #include "hybridpar_b200.h"
 #include "hp_common.cuh"
 
@@ -116,6 +118,36 @@ int hp_flag_wait(const volatile uint32_t* flag, uint32_t value, int32_t* status,
   if (!flag) return HP_ERR_PARAMETER;
   wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, value, status, timeout_ns);
   return cudaGetLastError() == cudaSuccess ? HP_OK : HP_ERR_CUDA;
+}
+
+int hp_flag_poll(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, uint32_t* observed) {
+  if (!flag) return HP_ERR_PARAMETER;
+  static thread_local cudaStream_t st = nullptr;
+  static thread_local int st_dev = -1;
+  static thread_local uint32_t* host = nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return HP_ERR_CUDA;
+  if (!st || st_dev != dev) {
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return HP_ERR_CUDA;
+    if (!host && cudaMallocHost(&host, sizeof(uint32_t)) != cudaSuccess) return HP_ERR_CUDA;
+    st_dev = dev;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    if (cudaMemcpyAsync(host, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      return HP_ERR_CUDA;
+    const uint32_t v = *reinterpret_cast<volatile uint32_t*>(host);
+    if (v >= value) {
+      if (observed) *observed = v;
+      return HP_OK;
+    }
+    if (timeout_ns) {
+      const auto ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0);
+      if ((uint64_t)ns.count() > timeout_ns) return HP_ERR_TIMEOUT;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(5));
+  }
 }
 
 int hp_stage_send(void* dst, const void* src, int64_t nbytes, uint32_t* flag, uint32_t value,

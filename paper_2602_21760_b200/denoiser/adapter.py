@@ -116,12 +116,14 @@ class NetDenoiser:
         if x_bf16 is None or x_bf16.data_ptr() != self._slot.data_ptr():
             self.load_input(x)
         self._set_t(self.t_both, t)
+        self._last = "both"
         out = self.g_both.run().reshape(2 * self.B, self.numel)
         return out[self.B:], out[: self.B]            # eps_c, eps_u
 
     def conditional(self, x, t, x_bf16=None):
         self.x_cond.view(self.B, self.numel).copy_(x.to(torch.bfloat16).view(self.B, self.numel))
         self._set_t(self.t_cond, t)
+        self._last = "cond"
         return self.g_cond.run().reshape(self.B, self.numel)
 
     def unconditional(self, x, t, x_bf16=None):
@@ -149,18 +151,27 @@ class NetDenoiser:
         U = len(net.units)
         self.cuts = cuts
         self.bounds = stage_bounds(cuts, U)
-        self._rec = None
+        self._rec = {}
 
         def both(x, t):
             x[B:].copy_(x[:B])
             rec = {c: None for c in cuts}
             out = net.run_units({"x": x}, t, "both", 0, U, record=rec)["eps"]
-            self._rec = rec
+            self._rec["both"] = rec
+            return out
+
+        def cond(x, t):
+            rec = {c: None for c in cuts}
+            out = net.run_units({"x": x}, t, "cond", 0, U, record=rec)["eps"]
+            self._rec["cond"] = rec
             return out
         self.g_both = _Graphed(both, self.x_both, self.t_both, self.use_graph)
+        self.g_cond = _Graphed(cond, self.x_cond, self.t_cond, self.use_graph)
         self.g_both.run()                                    # capture; defines the recorded states
-        # boundary j (input of stage j >= 1) holds the conditional rows [B, 2B)
-        self.bnd = [None] + [Boundary(state_rows(self._rec[c], B, 2 * B), self.dev) for c in cuts]
+        self.g_cond.run()
+        self._last = "both"
+        # boundary j (input of stage j >= 1): the conditional rows of a forward
+        self.bnd = [None] + [Boundary(state_rows(self._rec["cond"][c], 0, B), self.dev) for c in cuts]
         self.x_stage = torch.zeros((B,) + self.shape, dtype=torch.bfloat16, device=self.dev)
         self.t_stage = torch.zeros(B, dtype=torch.float32, device=self.dev)
         self.g_stage = [None] * len(self.bounds)
@@ -200,18 +211,28 @@ class NetDenoiser:
         self.x_stage.view(self.B, self.numel).copy_(x.to(torch.bfloat16).view(self.B, self.numel))
 
     def window_fill(self) -> None:
-        """Boundary states of the last CFG forward's conditional rows -> stage inputs."""
+        """Boundary states of the conditional rows of the last exact forward (the
+        CFG batch on one device, or the conditional-only forward of dev0 in a
+        condition-partitioned pair) -> stage inputs."""
+        lo = self.B if self._last == "both" else 0
         for j, c in enumerate(self.cuts, start=1):
-            self.bnd[j].load(state_rows(self._rec[c], self.B, 2 * self.B))
+            self.bnd[j].load(state_rows(self._rec[self._last][c], lo, lo + self.B))
 
-    def window_step(self, x, t):
+    def window_step(self, x, t, steps_left=None):
         """One pipelined step on one device: every stage on its stale input, last
         stage first so each stage reads its input before the upstream stage
-        overwrites it. Returns the unguided eps estimate [B, N]."""
-        self.load_stage_x(x)
+        overwrites it. ``steps_left`` (window steps after this one): stage j is
+        skipped when its output could no longer reach the last stage (the
+        pipeline's drain; numerically irrelevant). Returns the unguided eps
+        estimate [B, N]."""
+        n = len(self.bounds)
         eps = None
-        for j in reversed(range(len(self.bounds))):
+        for j in reversed(range(n)):
+            if steps_left is not None and j < n - 1 and steps_left < n - 1 - j:
+                continue
+            if j == 0:
+                self.load_stage_x(x)
             out = self.stage_run(j, t)
-            if j == len(self.bounds) - 1:
+            if j == n - 1:
                 eps = out
         return eps

@@ -316,12 +316,12 @@ class _StepRunner:
             K.blend_accumulate(acc, e, f, first=(d == 0))
         return self._advance(x, xb, acc, None, t, N.HP_CTRL_NONE)
 
-    def pipelined_split(self, x, xb, t, fill):
+    def pipelined_split(self, x, xb, t, fill, steps_left=None):
         """Stage-split window step on one device (stages.py): every stage on its
         previous-step input, then an unguided update."""
         if fill:
             self.den.window_fill()
-        eps = self.den.window_step(x, t)
+        eps = self.den.window_step(x, t, steps_left)
         return self._advance(x, xb, eps, None, t, N.HP_CTRL_NONE)
 
     def poll(self, t):
@@ -498,7 +498,7 @@ def _run_staged(plan: ExecutionPlan, fractions, x_init=None, to_host=True) -> Ru
             if host.stage is Stage.PARALLELISM:
                 fill = prev is not Stage.PARALLELISM
                 if st.split:
-                    x, xb = st.pipelined_split(x, xb, t, fill)
+                    x, xb = st.pipelined_split(x, xb, t, fill, host.tau2 - s)
                 else:
                     x, xb = st.pipelined(history, fractions, t)
                 clock.pipelined_step(s, fill=fill)

@@ -1,15 +1,16 @@
 """GPU (one device, three processes): the group exchange mechanics for real.
 
-Each rank exports its receive buffers and flag words by CUDA IPC
-(`hp_alloc` + `hp_ipc_get_handle`), opens the others' (`hp_ipc_open`), and
-pushes a known branch output into every other rank's slot with ONE
-`hp_stage_broadcast` (vector stores through the mapped pointers + system-scope
-release of the message number into each destination's flag). Rank 2 (a passive
-layer-wise rank) also acknowledges to ranks 0 and 1. After a host barrier each
-rank checks payloads, flags and acks, then runs the fused sampler kernel with
-the in-kernel flag wait on ALREADY released flags (so no kernel ever waits on
+Each rank exports its receive slots and flag words by CUDA IPC
+(`hp_alloc` + `hp_ipc_get_handle`, ``parallel.LinkBuffers``), opens the
+others' (`hp_ipc_open`), and pushes a known branch output as message 1 of its
+link to every other rank (`hp_stage_broadcast`: vector stores through the
+mapped pointer + system-scope release of the link's message count into the
+destination's flag). Rank 2 also acknowledges message 1 to ranks 0 and 1.
+After a host barrier each rank checks payloads, flags (read from the host with
+`hp_flag_poll`) and acks, then runs the fused sampler kernel with the
+in-kernel flag wait on ALREADY released flags (so no kernel ever waits on
 another process's kernel — the rule for sharing one GPU) and remote operands
-read from its receive buffer, against torch.
+read from its receive slots, against torch.
 """
 import os
 import socket
@@ -38,19 +39,19 @@ def _worker(rank, port, q):
     torch.cuda.set_device(0)
     try:
         from paper_2602_21760_b200 import _kernels as K, _native as N
-        from paper_2602_21760_b200.parallel import GroupBuffers, _Raw
+        from paper_2602_21760_b200.parallel import LinkBuffers, _Raw
         lib = N.load()
         n = 65536 + 40
-        buf = GroupBuffers(n, 2, None, rank, WORLD)
+        buf = LinkBuffers(n * 2, None, rank, WORLD)
         mine = _payload(rank, n)
-        s = 7
+        s = 1                                   # message 1 on every link
         others = [r for r in range(WORLD) if r != rank]
         dsts = (C.c_void_p * len(others))(*[buf.peer_slot(r, s) for r in others])
         flags = (C.c_void_p * len(others))(*[buf.peer_data_flag(r) for r in others])
         rc = lib.hp_stage_broadcast(dsts, flags, len(others), C.c_void_p(mine.data_ptr()), n * 2, s,
                                     C.c_void_p(N.stream_ptr()))
         assert rc == 0, rc
-        if rank == 2:       # passive rank: acknowledge message s to the branch ranks
+        if rank == 2:       # rank 2 consumed message 1 of ranks 0 and 1: acknowledge
             acks = (C.c_void_p * 2)(buf.peer_ack_flag(0), buf.peer_ack_flag(1))
             rc = lib.hp_stage_broadcast((C.c_void_p * 2)(0, 0), acks, 2, None, 0, s, C.c_void_p(N.stream_ptr()))
             assert rc == 0, rc
@@ -66,8 +67,11 @@ def _worker(rank, port, q):
         fl = torch.zeros(16, dtype=torch.int32, device="cuda")
         assert lib.hp_stage_send(C.c_void_p(fl.data_ptr()), C.c_void_p(buf.flags), 64, None, 0, st) == 0
         fl = fl.tolist()
+        got = C.c_uint32()
         ok_flag = all(fl[src] == s for src in others) and fl[rank] == 0
-        ok_ack = fl[WORLD + 2] == s if rank < 2 else True
+        ok_flag &= all(lib.hp_flag_poll(C.c_void_p(buf.data_flag(src)), s, 1_000_000_000, C.byref(got)) == 0
+                       and got.value == s for src in others)
+        ok_ack = buf.ack_flag(2) and fl[WORLD + 2] == s if rank < 2 else True
         # fused sampler: remote operands straight from this rank's receive buffer
         x = torch.randn(n, device="cuda")
         out = torch.empty_like(x)
