@@ -1,31 +1,28 @@
 // hp_attn.cu — K5: fused multi-head attention (head_dim 64) on tcgen05.
 //
-// One CTA = two 128-query tiles of one (head, batch); 320 threads:
-//   warps 0-3   softmax for query tile 0 (thread i owns query row i)
-//   warps 4-7   softmax for query tile 1
-//   warp 8      TMA: Q0, Q1 once, then K/V tiles of 128 keys (3-stage ring)
-//   warp 9      TMEM allocation + MMA issue:
-//                 S_q(j) = Q_q K(j)^T           -> TMEM S_q   (128 cols fp32)
-//                 O_q   += P_q(j) V(j)          -> TMEM O_q   (64 cols fp32, accumulated)
-//               issued S0(j), PV0(j-1), S1(j), PV1(j-1), so the tensor core
-//               works on one tile while the other tile's softmax runs.
-// Softmax (per row, fp32, log2 domain): one TMEM pass over S, block max, lazy
-// rescale of O in TMEM only when the running max grows by more than 2^8
-// (otherwise the stale max is kept: p <= 2^8, exact after the final 1/l), and
-// exp2 split between MUFU.EX2 and a degree-3 polynomial on the FMA pipe (P is
-// rounded to bf16 anyway). P goes to shared memory as the SW128 K-major A
-// operand of the PV MMA; V is consumed MN-major straight from its TMA tile.
-//
-// Launch variants (hp_attention picks one):
-//   S_kv <= 128        single-block kernel, 2 CTAs/SM (cross-attention)
-//   short last wave    split-KV kernel: one query tile per CTA, its key range cut
-//                      in two halves processed by the two warpgroups and merged
-//                      (fixed split point: batch-invariant); there P goes to TMEM
-//                      (bf16 pairs) and the PV MMA reads it from there (TS-MMA)
-//   otherwise          the two-tile kernel above
-// (Measured and dropped: P kept in TMEM as the A operand of a TS-MMA with the
-// whole S row in 200 registers: 180 us vs 169 us at S=4096; 64-key blocks with
-// double-buffered S: slower; 2 threads per score row: slower.)
+// Two kernels (hp_attention picks one):
+//   attn_single_kernel   S_kv <= 128 (cross-attention, causal text-encoder
+//                        attention): two query tiles per CTA, 2 CTAs/SM.
+//   attn_stream_kernel   everything else: two softmax "streams" per CTA, each
+//                        with its own score-MMA and PV-MMA issuing warp; the
+//                        128-score row is pulled into registers in one TMEM
+//                        load and S released at once, so S(i+1) = Q K(i+1)^T
+//                        runs on the tensor core while the softmax of block i
+//                        computes its exponentials. PAIR: stream = query tile
+//                        (two per CTA, shared K/V ring); SPLIT (when the PAIR
+//                        grid leaves a short last wave): one query tile, key
+//                        range halved between the streams (fixed split point:
+//                        batch-invariant), halves merged at the end.
+// Softmax (per row, fp32, log2 domain): block max, lazy rescale of O in TMEM only
+// when the running max grows by more than 2^8 (otherwise the stale max is kept:
+// p <= 2^8, exact after the final 1/l), exp2 split between MUFU.EX2 and a degree-3
+// polynomial on the FMA pipe (P is rounded to bf16 anyway); P is stored to TMEM as
+// bf16 pairs and read by a TS-MMA (O += P V, V MN-major straight from its TMA tile).
+// Round-2 measurements (tools/attn_ab.py, tools/micro/attn_trace.cu, profiles/r02):
+// S=4096 B=2 H=10: 151 -> 128 us; S=1024 B=2 H=20: 30 -> 27.5 us; SD3 S=4429 B=2
+// H=24: 420 -> 342 us. The period per 128-key block pair is ~2500 clk against
+// ~1240 clk of tensor work (PV at N=64 runs at 45 clk per K=16 step, not 32) and
+// ~1300 clk of MUFU: the softmax's issue/latency chain is the limit.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -42,10 +39,7 @@ using namespace hptc;
 namespace {
 
 constexpr int kBQ = 128, kBK = 128, kD = 64;
-constexpr int kStages = 3;
-constexpr int kThreads = 320;
 constexpr uint32_t kTileBytes = kBQ * kD * 2;        // 16 KB (Q, K or V tile)
-constexpr uint32_t kPBytes = kBQ * kBK * 2;          // 32 KB (two 64-key SW128 atoms)
 constexpr uint32_t kIdescS = idesc_bf16_f32(kBQ, kBK, 0);
 constexpr uint32_t kIdescO = idesc_bf16_f32(kBQ, kD, 1);  // B (= V) MN-major
 constexpr uint32_t kTmemCols = 512;
@@ -123,67 +117,51 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
       :: "r"(tmem_d), "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate) : "memory");
 }
 
-// SINGLE: every key fits one 128-key block (cross-attention, skv <= 128). Then no
-// rescale exists, O_q reuses S_q's TMEM columns once the softmax has consumed S_q,
-// and one K/V stage suffices: 256 TMEM columns and 97 KB of smem, so two CTAs
-// share an SM and one's latency chain (TMA -> MMA -> softmax -> PV -> store)
-// overlaps the other's.
-constexpr int kModePair = 0, kModeSingle = 1;
-template <int MODE> struct AttnCfg {
-  static constexpr bool kSingle = MODE == kModeSingle;
-  static constexpr int kNq = 2;
-  static constexpr int kThr = 32 * (4 * kNq + 2);
-  static constexpr int kMinBlocks = MODE == kModePair ? 1 : 2;
-  static constexpr int kSt = kSingle ? 1 : kStages;
-  static constexpr uint32_t kCols = MODE == kModePair ? kTmemCols : 256;
-  static constexpr size_t kSmem = kSingle ? kTileBytes * 5 + 256
-                                          : (size_t)kTileBytes * (kNq + 2 * kSt) + kNq * kPBytes + 256;
-};
+// Single-block kernel: every key fits one 128-key block (cross-attention, skv <=
+// 128, and the text encoders' causal attention). One CTA = two 128-query tiles;
+// 320 threads: warps 0-3 / 4-7 softmax of tile 0 / 1, warp 8 TMA, warp 9 MMA.
+// No rescale exists; O_q reuses S_q's TMEM columns once the softmax has consumed
+// S_q, P_0 overwrites Q_0|Q_1 and P_1 overwrites K|X after both score MMAs, so the
+// CTA needs 256 TMEM columns and 97 KB of smem and two CTAs share an SM (one's
+// TMA -> MMA -> softmax -> PV -> store chain overlaps the other's).
+constexpr int kSingleThreads = 320;
+constexpr uint32_t kSingleCols = 256;
+constexpr size_t kSingleSmem = (size_t)kTileBytes * 5 + 256;
 
-template <int MODE, bool MASK>     // MASK: some key block is partial (or causal)
-__global__ void __launch_bounds__(AttnCfg<MODE>::kThr, AttnCfg<MODE>::kMinBlocks)
-attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-            const __grid_constant__ CUtensorMap tmV, AttnParams p) {
-  using Cfg = AttnCfg<MODE>;
-  constexpr bool SINGLE = Cfg::kSingle;
-  constexpr int NQ = Cfg::kNq;
-  constexpr int kSt = Cfg::kSt;
-  constexpr uint32_t kCols = Cfg::kCols;
-  constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;
+template <bool MASK>     // MASK: the key block is partial (or causal)
+__global__ void __launch_bounds__(kSingleThreads, 2)
+attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, AttnParams p) {
+  constexpr int kTmaWarp = 8, kMmaWarp = 9;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                                  // NQ tiles
-  uint8_t* sK = sQ + NQ * kTileBytes;
-  uint8_t* sV = sK + kSt * kTileBytes;
-  uint8_t* sP = sV + kSt * kTileBytes;                // 2 tiles (one P buffer per query tile)
-  // SINGLE: P_0 overwrites Q_0|Q_1 and P_1 overwrites K|X once both S MMAs are done
-  // (80 KB in all instead of 128 KB), so two CTAs fit an SM
-  uint64_t* bars = reinterpret_cast<uint64_t*>(SINGLE ? sP + kTileBytes : sP + NQ * kPBytes);
+  uint8_t* sQ = smem;                       // 2 tiles
+  uint8_t* sK = sQ + 2 * kTileBytes;
+  uint8_t* sV = sK + kTileBytes;
+  uint8_t* sX = sV + kTileBytes;            // spare tile: second atom of P_1
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + kTileBytes);
   auto p_atom = [&](int q, int a) -> uint8_t* {       // 64-key SW128 atom a of P_q
-    if constexpr (SINGLE) return q == 0 ? sQ + a * kTileBytes : (a == 0 ? sK : sP);
-    return sP + q * kPBytes + a * (kBQ * 128);
+    return q == 0 ? sQ + a * kTileBytes : (a == 0 ? sK : sX);
   };
   uint64_t* q_full = bars;
   uint64_t* kv_full = q_full + 1;
-  uint64_t* kv_empty = kv_full + kSt;
-  uint64_t* s_full = kv_empty + kSt;       // [2] per query tile
+  uint64_t* s_full = kv_full + 1;          // [2] per query tile
   uint64_t* p_full = s_full + 2;           // [2]
   uint64_t* o_done = p_full + 2;           // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y, b = blockIdx.z;
-  const int q0 = blockIdx.x * NQ * kBQ;
-  const int J = SINGLE ? 1 : p.n_kv;
+  const int q0 = blockIdx.x * 2 * kBQ;
 
   if (warp == kTmaWarp && lane == 0) {
     prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < kSt; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    mbar_init(kv_full, 1);
     for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1); }
     fence_barrier_init();
   }
-  if (warp == kMmaWarp) tmem_alloc<kCols>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<kSingleCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -193,61 +171,36 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
 
   if (warp == kTmaWarp) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, NQ * kTileBytes);
+      mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) tma_load_3d(sQ + q * kTileBytes, &tmQ, q_full, p.q_col0 + h * kD, q0 + q * kBQ, b);
-      for (int j = 0; j < J; ++j) {
-        const int s = j % kSt;
-        mbar_wait(&kv_empty[s], ((j / kSt) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[s], 2 * kTileBytes);
-        tma_load_3d(sK + s * kTileBytes, &tmK, &kv_full[s], p.k_col0 + h * kD, j * kBK, b);
-        tma_load_3d(sV + s * kTileBytes, &tmV, &kv_full[s], p.v_col0 + h * kD, j * kBK, b);
-      }
+      for (int q = 0; q < 2; ++q) tma_load_3d(sQ + q * kTileBytes, &tmQ, q_full, p.q_col0 + h * kD, q0 + q * kBQ, b);
+      mbar_arrive_expect_tx(kv_full, 2 * kTileBytes);
+      tma_load_3d(sK, &tmK, kv_full, p.k_col0 + h * kD, 0, b);
+      tma_load_3d(sV, &tmV, kv_full, p.v_col0 + h * kD, 0, b);
     }
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
       mbar_wait(q_full, 0);
-      auto issue_s = [&](int q, int j) {
-        const int s = j % kSt;
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      const uint64_t dk = sdesc_sw128_kmajor(sK);
+      for (int q = 0; q < 2; ++q) {
         const uint64_t dq = sdesc_sw128_kmajor(sQ + q * kTileBytes);
-        const uint64_t dk = sdesc_sw128_kmajor(sK + s * kTileBytes);
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem + q * kBK, dq + 2 * k, dk + 2 * k, kIdescS, k > 0 ? 1u : 0u);
         umma_commit(&s_full[q]);
-      };
-      auto issue_pv = [&](int q, int j, bool wait) {
-        const int s = j % kSt;
-        if (wait) {
-          mbar_wait(&p_full[q], j & 1);
-          tc_fence_after();
-        }
-        const uint32_t d_o = tmem + (SINGLE ? q * kBK : NQ * kBK + q * kD);
+      }
+      for (int q = 0; q < 2; ++q) {
+        mbar_wait(&p_full[q], 0);
+        tc_fence_after();
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k) {
           const uint64_t da = sdesc_sw128_kmajor(p_atom(q, k >> 2)) + 2 * (k & 3);
-          const uint64_t dv = sdesc_sw128_mnmajor(sV + s * kTileBytes + k * 2048, 8192);
-          umma_bf16(d_o, da, dv, kIdescO, (j > 0 || k > 0) ? 1u : 0u);
+          const uint64_t dv = sdesc_sw128_mnmajor(sV + k * 2048, 8192);
+          umma_bf16(tmem + q * kBK, da, dv, kIdescO, k > 0 ? 1u : 0u);
         }
         umma_commit(&o_done[q]);
-      };
-      for (int j = 0; j < J; ++j) {
-        mbar_wait(&kv_full[j % kSt], (j / kSt) & 1);
-        tc_fence_after();
-        for (int q = 0; q < NQ; ++q) {
-          if (j > 0) {
-            // S_q(j) overwrites S_q(j-1): the softmax has consumed it once P_q(j-1) is out
-            mbar_wait(&p_full[q], (j - 1) & 1);
-            tc_fence_after();
-          }
-          issue_s(q, j);
-          if (j > 0) {
-            issue_pv(q, j - 1, false);      // P_q(j-1) was waited for above
-            if (q == NQ - 1) umma_commit(&kv_empty[(j - 1) % kSt]);
-          }
-        }
       }
-      for (int q = 0; q < NQ; ++q) issue_pv(q, J - 1, true);
-      umma_commit(&kv_empty[(J - 1) % kSt]);
     }
   } else {
     // ------------------------------ softmax ------------------------------
@@ -256,107 +209,77 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t t_s = tmem + lane_base + q * kBK;
-    const uint32_t t_o = tmem + lane_base + (SINGLE ? q * kBK : NQ * kBK + q * kD);
-    float m_run = -INFINITY, l_run = 0.f;
+    const uint32_t t_o = t_s;                 // O_q overwrites S_q
     const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
-    for (int j = 0; j < J; ++j) {
-      mbar_wait(&s_full[q], j & 1);
-      tc_fence_after();
-      // keys of this block this row may see: the sequence end and, when causal (single
-      // block), the row's own position
-      const int valid = p.causal ? min(min(kBK, p.skv - j * kBK), q0 + q * kBQ + row - j * kBK + 1)
-                                 : min(kBK, p.skv - j * kBK);
-      // pass 1: block row max straight from TMEM (32 columns at a time)
-      float mx = -INFINITY;
+    mbar_wait(&s_full[q], 0);
+    tc_fence_after();
+    // keys this row may see: the sequence end and, when causal, the row's own position
+    const int valid = p.causal ? min(min(kBK, p.skv), q0 + q * kBQ + row + 1) : min(kBK, p.skv);
+    // pass 1: row max straight from TMEM, 32 columns at a time (two CTAs share the
+    // SM's registers here, so the row is not held whole)
+    float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kBK / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_s + c * 32, r);
-        tmem_ld_wait();
-        if (MASK && valid < kBK) {
+    for (int c = 0; c < kBK / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(t_s + c * 32, r);
+      tmem_ld_wait();
+      if (MASK && valid < kBK) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
-        }
-#pragma unroll
-        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
       }
-      const float m_blk = mx * p.scale_log2;
-      // lazy rescale: move the reference max only when it grows by > 2^8
-      const bool grow = (j == 0) || (m_blk > m_run + kRescaleThreshold);
-      if (!SINGLE && j > 0) {
-        // PV(j-1) must be complete before O is rescaled or P is overwritten
-        mbar_wait(&o_done[q], (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, grow)) {
-          const float alpha = grow ? ex2f(m_run - fmaxf(m_run, m_blk)) : 1.0f;
-          uint32_t o[32];
 #pragma unroll
-          for (int c = 0; c < kD / 32; ++c) {
-            tmem_ld_32x32b_x32(t_o + c * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st_32x32b_x32(t_o + c * 32, o);
-          }
-          tmem_st_wait();
-          if (grow) l_run *= alpha;
-        }
-      }
-      if (grow) m_run = fmaxf(m_run, m_blk);
-      const uint64_t negm2 = pack2(-m_run, -m_run);
-      uint64_t sum2 = 0ull;
-      if constexpr (SINGLE) {
-        // P overwrites Q and K: both tiles' score MMAs must have finished reading them
-        // (the commit behind S_1 covers S_0 too)
-        if (q == 0) {
-          mbar_wait(&s_full[1], 0);
-          tc_fence_after();
-        }
-      }
-      // pass 2: P = 2^(s*scale - m) in packed fp32 pairs; 3 of 8 pairs on the FMA-pipe polynomial
-#pragma unroll
-      for (int c = 0; c < kBK / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_s + c * 32, r);
-        tmem_ld_wait();
-        if (MASK && valid < kBK) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
-        }
-        uint32_t packed[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const uint64_t x2 = ffma2(pack2u(r[i], r[i + 1]), scale2, negm2);
-          uint64_t e2;
-          const int pr = (i >> 1) & 7;
-          if (pr == 2 || pr == 5 || pr == 7) {
-            e2 = exp2_poly2(x2);
-          } else {
-            e2 = pack2(ex2f(lo2(x2)), ex2f(hi2(x2)));
-          }
-          sum2 = fadd2(sum2, e2);
-          packed[i / 2] = pack_bf16(lo2(e2), hi2(e2));
-        }
-        uint8_t* atom = p_atom(q, c >> 1) + row * 128;
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          const int chunk = ((c & 1) * 4 + qq) ^ (row & 7);
-          *reinterpret_cast<uint4*>(atom + chunk * 16) =
-              make_uint4(packed[4 * qq], packed[4 * qq + 1], packed[4 * qq + 2], packed[4 * qq + 3]);
-        }
-      }
-      l_run += lo2(sum2) + hi2(sum2);
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[q]);
+      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
     }
-    mbar_wait(&o_done[q], (J - 1) & 1);
+    const float m = mx * p.scale_log2;
+    const uint64_t negm2 = pack2(-m, -m);
+    // P overwrites Q and K: both tiles' score MMAs must have finished reading them
+    // (the commit behind S_1 covers S_0 too)
+    if (q == 0) {
+      mbar_wait(&s_full[1], 0);
+      tc_fence_after();
+    }
+    uint64_t sum2[4] = {0ull, 0ull, 0ull, 0ull};
+    // pass 2: P = 2^(s*scale - m) in packed fp32 pairs, 2 of 8 pairs on the FMA-pipe polynomial
+#pragma unroll
+    for (int c = 0; c < kBK / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(t_s + c * 32, r);
+      tmem_ld_wait();
+      if (MASK && valid < kBK) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
+      }
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const uint64_t x2 = ffma2(pack2u(r[i], r[i + 1]), scale2, negm2);
+        uint64_t e2;
+        const int pr = (i >> 1) & 7;
+        if (pr == 3 || pr == 7) e2 = exp2_poly2(x2);
+        else e2 = pack2(ex2f(lo2(x2)), ex2f(hi2(x2)));
+        sum2[(i >> 1) & 3] = fadd2(sum2[(i >> 1) & 3], e2);
+        packed[i / 2] = pack_bf16(lo2(e2), hi2(e2));
+      }
+      uint8_t* atom = p_atom(q, c >> 1) + row * 128;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        const int chunk = ((c & 1) * 4 + qq) ^ (row & 7);
+        *reinterpret_cast<uint4*>(atom + chunk * 16) =
+            make_uint4(packed[4 * qq], packed[4 * qq + 1], packed[4 * qq + 2], packed[4 * qq + 3]);
+      }
+    }
+    const uint64_t s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
+    const float l = lo2(s01) + hi2(s01);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&p_full[q]);
+    mbar_wait(&o_done[q], 0);
     tc_fence_after();
     const int qrow = q0 + q * kBQ + row;
-    const float inv = 1.0f / l_run;
+    const float inv = 1.0f / l;
     uint32_t o[32];
 #pragma unroll
     for (int c = 0; c < kD / 32; ++c) {
@@ -378,51 +301,91 @@ attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == kMmaWarp) tmem_dealloc<kCols>(tmem);
+  if (warp == kMmaWarp) tmem_dealloc<kSingleCols>(tmem);
 }
 
 // ---------------------------------------------------------------------------
-// Split-KV CTA: ONE query tile, its key range cut in two halves that the two
-// softmax warpgroups ("streams") process concurrently against their own K/V rings,
-// S / P buffers and O accumulators; the halves are merged in the CTA at the end
-// (m = max(m0, m1), O = sum_h 2^(m_h - m) O_h, l likewise). Units are query tiles,
-// twice as many as two-tile CTAs, so the last partial wave on 148 SMs is half as
-// long. The split point depends on S_kv only: an image's rows are computed
-// identically whatever else is in the batch.
-constexpr int kStSplit = 2;
+// Streaming kernel (round 2): two independent softmax "streams" per CTA, each with
+// its OWN MMA-issue warp, and the score tile released as soon as the softmax has
+// pulled it into registers, so S(i+1) = Q K(i+1)^T runs on the tensor core while
+// the softmax of block i is still computing exponentials. (The round-1 kernels
+// re-read S from TMEM in a second pass, so S(i+1) could only start after P(i) was
+// out: ncu showed the softmax warps parked on the score barrier 1/3 of the time.)
+//   PAIR  (SPLIT=false): stream q = query tile q of the CTA (256 queries), K/V
+//          ring shared by both streams (a slot is released by both PV commits).
+//   SPLIT (SPLIT=true):  one query tile, key range cut in two halves (fixed split
+//          point: batch-invariant), one K/V ring per stream, halves merged at the end.
+// 512 threads: warps 0-3 / 4-7 softmax of stream 0 / 1 (thread = query row),
+// warp 8 TMA (warp 9 the second K/V producer in SPLIT), warps 10 / 11 issue the
+// score MMAs of stream 0 / 1, warps 12 / 13 the PV MMAs (tcgen05.mma holds its
+// issuing thread until the tensor pipe accepts it, and tcgen05.commit tracks the
+// issuing thread's MMAs: one issuer per (stream, kind) keeps S off PV's queue),
+// warps 14-15 idle. setmaxnreg moves registers from warpgroups 2-3 (48 each) to
+// the softmax warpgroups (208 each: the 128-score row stays in registers).
+// TMEM (512 cols): S_q [128 q, +128), O_q [256 + 64 q, +64), P_q [384 + 64 q, +64)
+// (P as bf16 pairs, the A operand of the TS-MMA O_q += P_q V).
+// Softmax per block: one TMEM load of the 128-score row, s_free arrive, a depth-10
+// FMNMX3 tree for the row max, exp2 (5/8 MUFU, 3/8 FMA polynomial) with four
+// partial sums, then the O rescale (lazy, > 2^8 only) once PV(i-1) is done, P
+// stored to TMEM, p_full arrive.
+constexpr int kStrThreads = 512;
+constexpr int kStrSplitStages = 3, kStrPairStages = 5;
+template <bool SPLIT> struct StrCfg {
+  static constexpr int kNq = SPLIT ? 1 : 2;                   // Q tiles in smem
+  static constexpr int kSlots = SPLIT ? 2 * kStrSplitStages : kStrPairStages;
+  static constexpr size_t kSmem = 1024 + (size_t)kTileBytes * (kNq + 2 * kSlots) + 256 + 4 * kBQ * 4;
+};
 
-template <bool MASK>             // MASK: S_kv is not a multiple of the 128-key block
-__global__ void __launch_bounds__(kThreads, 1)
-attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, AttnParams p) {
+#ifdef HP_ATTN_TRACE
+// event timeline of CTA (0,0,0) for tools/micro/attn_trace.cu: [stream][event][block]
+__device__ long long g_attn_trace[2][12][256];
+#define HP_TRACE(cond, q, ev, i) \
+  do { if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 256) \
+         g_attn_trace[q][ev][i] = clock64(); } while (0)
+#else
+#define HP_TRACE(cond, q, ev, i) do {} while (0)
+#endif
+template <bool SPLIT, bool MASK>   // MASK: S_kv is not a multiple of the 128-key block
+__global__ void __launch_bounds__(kStrThreads, 1)
+attn_stream_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, AttnParams p) {
+  using Cfg = StrCfg<SPLIT>;
+  constexpr int kSlots = Cfg::kSlots;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                                        // 1 tile
-  uint8_t* sK = sQ + kTileBytes;                             // [stream][stage]
-  uint8_t* sV = sK + 2 * kStSplit * kTileBytes;              // [stream][stage]
-  // P_q lives in TMEM columns [384 + 64 q, 448 + 64 q) (bf16 pairs), read by a TS-MMA
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + 2 * kStSplit * kTileBytes);
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + Cfg::kNq * kTileBytes;                    // [slot]
+  uint8_t* sV = sK + kSlots * kTileBytes;                      // [slot]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kSlots * kTileBytes);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = q_full + 1;                            // [stream][stage]
-  uint64_t* kv_empty = kv_full + 2 * kStSplit;
-  uint64_t* s_full = kv_empty + 2 * kStSplit;                // [stream]
-  uint64_t* p_full = s_full + 2;
+  uint64_t* kv_full = q_full + 1;                              // [kSlots]
+  uint64_t* kv_empty = kv_full + kSlots;                       // [kSlots]
+  uint64_t* s_full = kv_empty + kSlots;                        // [stream]
+  uint64_t* s_free = s_full + 2;
+  uint64_t* p_full = s_free + 2;
   uint64_t* o_done = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
   float* s_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // [stream][2][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y, b = blockIdx.z;
-  const int q0 = blockIdx.x * kBQ;
+  const int q0 = blockIdx.x * Cfg::kNq * kBQ;
   const int J = p.n_kv;
-  const int jh = (J + 1) / 2;
-  const int jb[2] = {0, jh}, nj[2] = {jh, J - jh};
+  const int jh = SPLIT ? (J + 1) / 2 : J;
+  // blocks of stream q: [jb(q), jb(q) + nj(q))
+  auto jb = [&](int q) { return SPLIT ? q * jh : 0; };
+  auto nj = [&](int q) { return SPLIT ? (q == 0 ? jh : J - jh) : J; };
+  // ring slot and phase of the i-th block of stream q
+  auto slot = [&](int q, int i) { return SPLIT ? q * kStrSplitStages + i % kStrSplitStages : i % kStrPairStages; };
+  auto phase = [&](int i) { return SPLIT ? (i / kStrSplitStages) & 1 : (i / kStrPairStages) & 1; };
 
   if (warp == 8 && lane == 0) {
     prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2 * kStSplit; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1); }
+    for (int s = 0; s < kSlots; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], SPLIT ? 2 : 4); }   // S and PV commits per stream
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1); mbar_init(&s_free[i], 4); mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc<kTmemCols>(tmem_slot);
@@ -433,65 +396,75 @@ attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
   pdl_wait();
   pdl_trigger();
 
-  auto k_at = [&](int q, int s) { return sK + (q * kStSplit + s) * kTileBytes; };
-  auto v_at = [&](int q, int s) { return sV + (q * kStSplit + s) * kTileBytes; };
-  if (warp == 8) {
+  if (warp >= 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
+  if (warp == 8 || (SPLIT && warp == 9)) {
+    // K/V producer(s): warp 8 feeds stream 0 (and, PAIR, the shared ring), warp 9
+    // stream 1 (SPLIT), so one stream's full ring never stalls the other's loads
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, kTileBytes);
-      tma_load_3d(sQ, &tmQ, q_full, p.q_col0 + h * kD, q0, b);
-      for (int i = 0; i < jh; ++i) {
-        for (int q = 0; q < 2; ++q) {
-          if (i >= nj[q]) continue;
-          const int s = i % kStSplit, bi = q * kStSplit + s, g = jb[q] + i;
-          mbar_wait(&kv_empty[bi], ((i / kStSplit) & 1) ^ 1);
-          mbar_arrive_expect_tx(&kv_full[bi], 2 * kTileBytes);
-          tma_load_3d(k_at(q, s), &tmK, &kv_full[bi], p.k_col0 + h * kD, g * kBK, b);
-          tma_load_3d(v_at(q, s), &tmV, &kv_full[bi], p.v_col0 + h * kD, g * kBK, b);
-        }
+      const int q = warp - 8;
+      if (q == 0) {
+        mbar_arrive_expect_tx(q_full, Cfg::kNq * kTileBytes);
+#pragma unroll
+        for (int t = 0; t < Cfg::kNq; ++t)
+          tma_load_3d(sQ + t * kTileBytes, &tmQ, q_full, p.q_col0 + h * kD, q0 + t * kBQ, b);
+      }
+      for (int i = 0; i < nj(q); ++i) {
+        const int s = slot(q, i), g = jb(q) + i;
+        mbar_wait_park(&kv_empty[s], phase(i) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[s], 2 * kTileBytes);
+        tma_load_3d(sK + s * kTileBytes, &tmK, &kv_full[s], p.k_col0 + h * kD, g * kBK, b);
+        tma_load_3d(sV + s * kTileBytes, &tmV, &kv_full[s], p.v_col0 + h * kD, g * kBK, b);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 10 || warp == 11) {
+    // S issuer of stream q: S(i) as soon as K(i) is in and the softmax holds S(i-1)
+    // in registers. tcgen05.mma holds the issuing thread until the tensor pipe takes
+    // the instruction, so S and PV get separate issuers: a queued PV never delays S.
+    const int q = warp - 10;
     if (lane == 0) {
-      mbar_wait(q_full, 0);
-      const uint64_t dq = sdesc_sw128_kmajor(sQ);
-      auto issue_s = [&](int q, int i) {
-        const uint64_t dk = sdesc_sw128_kmajor(k_at(q, i % kStSplit));
+      mbar_wait_park(q_full, 0);
+      const uint64_t dq = sdesc_sw128_kmajor(sQ + (SPLIT ? 0 : q * kTileBytes));
+      const uint32_t t_s = tmem + q * kBK;
+      const int n = nj(q);
+      for (int i = 0; i < n; ++i) {
+        mbar_wait_park(&kv_full[slot(q, i)], phase(i));
+        HP_TRACE(true, q, 0, i);
+        if (i > 0) mbar_wait_park(&s_free[q], (i - 1) & 1);
+        HP_TRACE(true, q, 1, i);
+        tc_fence_after();
+        const uint64_t dk = sdesc_sw128_kmajor(sK + slot(q, i) * kTileBytes);
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem + q * kBK, dq + 2 * k, dk + 2 * k, kIdescS, k > 0 ? 1u : 0u);
+        for (int k = 0; k < kD / 16; ++k) umma_bf16(t_s, dq + 2 * k, dk + 2 * k, kIdescS, k > 0 ? 1u : 0u);
         umma_commit(&s_full[q]);
-      };
-      auto issue_pv = [&](int q, int i) {
-        const uint8_t* v = v_at(q, i % kStSplit);
+        umma_commit(&kv_empty[slot(q, i)]);
+        HP_TRACE(true, q, 2, i);
+      }
+    }
+  } else if (warp == 12 || warp == 13) {
+    // PV issuer of stream q: O_q += P_q(i) V(i) once the softmax published P(i)
+    const int q = warp - 12;
+    if (lane == 0) {
+      const uint32_t t_o = tmem + 256 + q * kD, t_p = tmem + 384 + q * 64;
+      const int n = nj(q);
+      for (int i = 0; i < n; ++i) {
+        mbar_wait_park(&p_full[q], i & 1);
+        HP_TRACE(true, q, 3, i);
+        tc_fence_after();
+        const uint8_t* v = sV + slot(q, i) * kTileBytes;
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k) {
           const uint64_t dv = sdesc_sw128_mnmajor(v + k * 2048, 8192);
-          umma_bf16_ts(tmem + 256 + q * kD, tmem + 384 + q * 64 + 8 * k, dv, kIdescO, (i > 0 || k > 0) ? 1u : 0u);
+          umma_bf16_ts(t_o, t_p + 8 * k, dv, kIdescO, (i > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&o_done[q]);
-        umma_commit(&kv_empty[q * kStSplit + i % kStSplit]);
-      };
-      for (int i = 0; i < jh; ++i) {
-        for (int q = 0; q < 2; ++q) {
-          if (i >= nj[q]) continue;
-          const int bi = q * kStSplit + i % kStSplit;
-          mbar_wait(&kv_full[bi], (i / kStSplit) & 1);
-          tc_fence_after();
-          if (i > 0) {                       // S_q(i) overwrites S_q(i-1): P_q(i-1) is out
-            mbar_wait(&p_full[q], (i - 1) & 1);
-            tc_fence_after();
-          }
-          issue_s(q, i);
-          if (i > 0) issue_pv(q, i - 1);
-        }
-      }
-      for (int q = 0; q < 2; ++q) {
-        mbar_wait(&p_full[q], (nj[q] - 1) & 1);
-        tc_fence_after();
-        issue_pv(q, nj[q] - 1);
+        umma_commit(&kv_empty[slot(q, i)]);
       }
     }
+  }
   } else {
-    // ------------------------------ softmax: stream q over key blocks jb[q] .. ------------------------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+    // ------------------------------ softmax of stream q ------------------------------
     const int q = warp >> 2;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
@@ -501,32 +474,68 @@ attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     const uint32_t t_p = tmem + lane_base + 384 + q * 64;
     float m_run = -INFINITY, l_run = 0.f;
     const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
-    const int n = nj[q];
+    const int n = nj(q);
     for (int i = 0; i < n; ++i) {
-      mbar_wait(&s_full[q], i & 1);
+      HP_TRACE(quarter == 0 && lane == 0, q, 4, i);
+      mbar_wait_park(&s_full[q], i & 1);
+      HP_TRACE(quarter == 0 && lane == 0, q, 5, i);
       tc_fence_after();
-      const int valid = min(kBK, p.skv - (jb[q] + i) * kBK);
-      float mx = -INFINITY;
+      uint32_t r[128];
+      tmem_ld_x32_at(t_s + 0, r, 0);
+      tmem_ld_x32_at(t_s + 32, r, 32);
+      tmem_ld_x32_at(t_s + 64, r, 64);
+      tmem_ld_x32_at(t_s + 96, r, 96);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[q]);           // the MMA warp may overwrite S now
+      HP_TRACE(quarter == 0 && lane == 0, q, 6, i);
+      if (MASK) {
+        const int valid = min(kBK, p.skv - (jb(q) + i) * kBK);
+        if (valid < kBK) {
 #pragma unroll
-      for (int c = 0; c < kBK / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_s + c * 32, r);
-        tmem_ld_wait();
-        if (MASK && valid < kBK) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (c * 32 + e >= valid) r[e] = __float_as_uint(-INFINITY);
+          for (int e = 0; e < 128; ++e)
+            if (e >= valid) r[e] = __float_as_uint(-INFINITY);
         }
-#pragma unroll
-        for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(r[e]));
       }
-      const float m_blk = mx * p.scale_log2;
+      // row max: 8 independent chains (FMNMX3 pairs), then a small tree
+      float mx[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) mx[a] = __uint_as_float(r[a]);
+#pragma unroll
+      for (int e = 8; e < 128; e += 8) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) mx[a] = fmaxf(mx[a], __uint_as_float(r[e + a]));
+      }
+      const float m_blk = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * p.scale_log2;
+      // lazy rescale: move the reference max only when it grows by > 2^8
       const bool grow = (i == 0) || (m_blk > m_run + kRescaleThreshold);
+      const float m_new = grow ? fmaxf(m_run, m_blk) : m_run;
+      const float alpha = grow ? ex2f(m_run - m_new) : 1.0f;     // i == 0: 2^-inf = 0
+      const uint64_t negm2 = pack2(-m_new, -m_new);
+      uint64_t sum2[4] = {0ull, 0ull, 0ull, 0ull};
+      uint32_t packed[64];
+#pragma unroll
+      for (int e = 0; e < 128; e += 2) {
+        const uint64_t x2 = ffma2(pack2u(r[e], r[e + 1]), scale2, negm2);
+        uint64_t e2;
+        const int pr = (e >> 1) & 7;
+        if (pr == 3 || pr == 7) e2 = exp2_poly2(x2);   // 2 of 8 pairs on the FMA pipe
+        else e2 = pack2(ex2f(lo2(x2)), ex2f(hi2(x2)));
+        sum2[(e >> 1) & 3] = fadd2(sum2[(e >> 1) & 3], e2);
+        packed[e >> 1] = pack_bf16(lo2(e2), hi2(e2));
+      }
+      HP_TRACE(quarter == 0 && lane == 0, q, 7, i);
+      const uint64_t s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
+      l_run = l_run * alpha + (lo2(s01) + hi2(s01));
+      m_run = m_new;
       if (i > 0) {
-        mbar_wait(&o_done[q], (i - 1) & 1);
+        // PV(i-1) must be complete before O is rescaled or P is overwritten
+        mbar_wait_park(&o_done[q], (i - 1) & 1);
+        HP_TRACE(quarter == 0 && lane == 0, q, 8, i);
         tc_fence_after();
         if (__any_sync(0xffffffffu, grow)) {
-          const float alpha = grow ? ex2f(m_run - fmaxf(m_run, m_blk)) : 1.0f;
           uint32_t o[32];
 #pragma unroll
           for (int c = 0; c < kD / 32; ++c) {
@@ -536,72 +545,73 @@ attn_splitkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
             tmem_st_32x32b_x32(t_o + c * 32, o);
           }
-          tmem_st_wait();
-          if (grow) l_run *= alpha;
         }
       }
-      if (grow) m_run = fmaxf(m_run, m_blk);
-      const uint64_t negm2 = pack2(-m_run, -m_run);
-      uint64_t sum2 = 0ull;
 #pragma unroll
-      for (int c = 0; c < kBK / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_s + c * 32, r);
-        tmem_ld_wait();
-        if (MASK && valid < kBK) {
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (c * 32 + e >= valid) r[e] = __float_as_uint(-INFINITY);
-        }
-        uint32_t packed[16];
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const uint64_t x2 = ffma2(pack2u(r[e], r[e + 1]), scale2, negm2);
-          uint64_t e2;
-          const int pr = (e >> 1) & 7;
-          if (pr == 2 || pr == 5 || pr == 7) e2 = exp2_poly2(x2);
-          else e2 = pack2(ex2f(lo2(x2)), ex2f(hi2(x2)));
-          sum2 = fadd2(sum2, e2);
-          packed[e / 2] = pack_bf16(lo2(e2), hi2(e2));
-        }
-        tmem_st_32x32b_x16(t_p + c * 16, packed);
+        for (int e = 0; e < 16; ++e) pk[e] = packed[c * 16 + e];
+        tmem_st_32x32b_x16(t_p + c * 16, pk);
       }
-      l_run += lo2(sum2) + hi2(sum2);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[q]);
+      HP_TRACE(quarter == 0 && lane == 0, q, 9, i);
     }
-    mbar_wait(&o_done[q], (n - 1) & 1);
+    mbar_wait_park(&o_done[q], (n - 1) & 1);
     tc_fence_after();
-    // merge the two halves: both warpgroups reach every O column of their rows
-    s_ml[(q * 2 + 0) * kBQ + row] = m_run;
-    s_ml[(q * 2 + 1) * kBQ + row] = l_run;
-    tc_fence_before();
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    tc_fence_after();
-    const float m0 = s_ml[0 * kBQ + row], l0 = s_ml[1 * kBQ + row];
-    const float m1 = s_ml[2 * kBQ + row], l1 = s_ml[3 * kBQ + row];
-    const float m = fmaxf(m0, m1);
-    const float a0 = ex2f(m0 - m), a1 = ex2f(m1 - m);
-    const float inv = 1.0f / (a0 * l0 + a1 * l1);
-    const float w0 = a0 * inv, w1 = a1 * inv;
-    const int qrow = q0 + row;
-    // warpgroup q writes output columns [32q, 32q + 32)
-    uint32_t o0[32], o1[32];
-    tmem_ld_32x32b_x32(tmem + lane_base + 256 + q * 32, o0);
-    tmem_ld_32x32b_x32(tmem + lane_base + 256 + kD + q * 32, o1);
-    tmem_ld_wait();
-    if (qrow < p.sq) {
-      __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + q * 32;
+    if constexpr (!SPLIT) {
+      const int qrow = q0 + q * kBQ + row;
+      const float inv = 1.0f / l_run;
+      uint32_t o[32];
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        float v[8];
+      for (int c = 0; c < kD / 32; ++c) {
+        tmem_ld_32x32b_x32(t_o + c * 32, o);
+        tmem_ld_wait();
+        if (qrow < p.sq) {
+          __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + c * 32;
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          v[e] = fmaf(__uint_as_float(o0[8 * qq + e]), w0, __uint_as_float(o1[8 * qq + e]) * w1);
-        reinterpret_cast<uint4*>(dst)[qq] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
-                                                       pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+          for (int qq = 0; qq < 4; ++qq) {
+            uint4 u = make_uint4(pack_bf16(__uint_as_float(o[8 * qq]) * inv, __uint_as_float(o[8 * qq + 1]) * inv),
+                                 pack_bf16(__uint_as_float(o[8 * qq + 2]) * inv, __uint_as_float(o[8 * qq + 3]) * inv),
+                                 pack_bf16(__uint_as_float(o[8 * qq + 4]) * inv, __uint_as_float(o[8 * qq + 5]) * inv),
+                                 pack_bf16(__uint_as_float(o[8 * qq + 6]) * inv, __uint_as_float(o[8 * qq + 7]) * inv));
+            reinterpret_cast<uint4*>(dst)[qq] = u;
+          }
+        }
+      }
+    } else {
+      // merge the two halves: both warpgroups reach every O column of their rows
+      s_ml[(q * 2 + 0) * kBQ + row] = m_run;
+      s_ml[(q * 2 + 1) * kBQ + row] = l_run;
+      tc_fence_before();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      tc_fence_after();
+      const float m0 = s_ml[0 * kBQ + row], l0 = s_ml[1 * kBQ + row];
+      const float m1 = s_ml[2 * kBQ + row], l1 = s_ml[3 * kBQ + row];
+      const float m = fmaxf(m0, m1);
+      const float a0 = ex2f(m0 - m), a1 = ex2f(m1 - m);
+      const float inv = 1.0f / (a0 * l0 + a1 * l1);
+      const float w0 = a0 * inv, w1 = a1 * inv;
+      const int qrow = q0 + row;
+      // warpgroup q writes output columns [32q, 32q + 32)
+      uint32_t o0[32], o1[32];
+      tmem_ld_32x32b_x32(tmem + lane_base + 256 + q * 32, o0);
+      tmem_ld_32x32b_x32(tmem + lane_base + 256 + kD + q * 32, o1);
+      tmem_ld_wait();
+      if (qrow < p.sq) {
+        __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + q * 32;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            v[e] = fmaf(__uint_as_float(o0[8 * qq + e]), w0, __uint_as_float(o1[8 * qq + e]) * w1);
+          reinterpret_cast<uint4*>(dst)[qq] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                                                         pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+        }
       }
     }
   }
@@ -640,19 +650,17 @@ bool map3(CUtensorMap* m, const void* base, long long ld, int rows, int batch) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, bool MASK>
-int launch_attn(dim3 grid, cudaStream_t st, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                const AttnParams& p, size_t slack) {
-  const size_t smem = AttnCfg<MODE>::kSmem + slack;
+int launch_single(dim3 grid, cudaStream_t st, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                  const AttnParams& p) {
+  constexpr size_t smem = kSingleSmem + 1024;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(attn_kernel<MODE, MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(attn_single_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return HP_ERR_CUDA;
     attr = true;
   }
-  return hp_launch_pdl(attn_kernel<MODE, MASK>, grid, dim3(AttnCfg<MODE>::kThr), smem, st, tq, tk, tv, p) ==
-                 cudaSuccess
+  return hp_launch_pdl(attn_single_kernel<true>, grid, dim3(kSingleThreads), smem, st, tq, tk, tv, p) == cudaSuccess
              ? HP_OK : HP_ERR_CUDA;
 }
 
@@ -667,13 +675,29 @@ int num_sms_attn() {
   return n;
 }
 
-bool splitkv_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("HP_ATTN_SPLITKV");
-    on = (e && e[0] == '0') ? 0 : 1;
+// HP_ATTN_MODE: 0 auto, 1 two-tile, 2 split-KV (A/B switch)
+int attn_mode() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("HP_ATTN_MODE");
+    m = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
   }
-  return on == 1;
+  return m;
+}
+
+template <bool SPLIT, bool MASK>
+int launch_stream(dim3 grid, cudaStream_t st, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                  const AttnParams& p) {
+  constexpr size_t smem = StrCfg<SPLIT>::kSmem;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(attn_stream_kernel<SPLIT, MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return HP_ERR_CUDA;
+    attr = true;
+  }
+  return hp_launch_pdl(attn_stream_kernel<SPLIT, MASK>, grid, dim3(kStrThreads), smem, st, tq, tk, tv, p) ==
+                 cudaSuccess ? HP_OK : HP_ERR_CUDA;
 }
 
 }  // namespace
@@ -699,27 +723,17 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   p.n_kv = (d->skv + kBK - 1) / kBK;
   dim3 grid((d->sq + 2 * kBQ - 1) / (2 * kBQ), d->heads, d->batch);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p.n_kv == 1) return launch_attn<kModeSingle, true>(grid, st, tq, tk, tv, p, 1024);
+  if (p.n_kv == 1) return launch_single(grid, st, tq, tk, tv, p);
   const bool mask = (d->skv % kBK) != 0;
-  // one query tile per CTA when the two-tile grid would leave a short last wave
+  // one query tile per CTA (split-KV) when the two-tile grid would leave a short last wave
   const int pair_ctas = grid.x * grid.y * grid.z;
   const int sms = num_sms_attn();
   const int tail = pair_ctas % sms;
-  if (splitkv_enabled() && tail != 0 && tail * 2 < sms) {
-    constexpr size_t smem = 1024 + (size_t)kTileBytes * (1 + 4 * kStSplit) + 256 + 4 * kBQ * 4;
-    static bool attr_s = false;
-    if (!attr_s) {
-      if (cudaFuncSetAttribute(attn_splitkv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-              cudaSuccess ||
-          cudaFuncSetAttribute(attn_splitkv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-              cudaSuccess)
-        return HP_ERR_CUDA;
-      attr_s = true;
-    }
+  const int mode = attn_mode();
+  const bool split = mode == 2 || (mode == 0 && tail != 0 && tail * 2 < sms);
+  if (split) {
     dim3 g1((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
-    const auto kern = (d->skv % kBK) ? attn_splitkv_kernel<true> : attn_splitkv_kernel<false>;
-    return hp_launch_pdl(kern, g1, dim3(kThreads), smem, st, tq, tk, tv, p) == cudaSuccess ? HP_OK : HP_ERR_CUDA;
+    return mask ? launch_stream<true, true>(g1, st, tq, tk, tv, p) : launch_stream<true, false>(g1, st, tq, tk, tv, p);
   }
-  return mask ? launch_attn<kModePair, true>(grid, st, tq, tk, tv, p, 1024)
-              : launch_attn<kModePair, false>(grid, st, tq, tk, tv, p, 1024);
+  return mask ? launch_stream<false, true>(grid, st, tq, tk, tv, p) : launch_stream<false, false>(grid, st, tq, tk, tv, p);
 }
