@@ -9,16 +9,19 @@ drop-in ``run_plan`` API. At N=1 the plan is ``serial`` (both guidance
 branches on one GPU, batched); at N>1 each GPU pair runs one image with the
 hybrid plan (``--mode pairs``, the default: condition partitioning with the
 branch exchange fused into the sampler kernel over NVLink) or every GPU runs
-its own image (``--mode replicas``). If the pair path fails the line says so
-(``config.mode_note``) and reports replicas instead.
+its own image (``--mode replicas``). A failed run on any rank makes every rank
+agree and exit non-zero with an ``error`` line (no silent change of mode).
 
 Printed JSON (rank 0, one line): ``value`` = device-resident seconds per image
-for the whole job (inputs resident, no host copies); ``e2e`` = the same metric
-through ``run_plan`` with host x_T in and host x0 out each run; ``roofline``
-= the denoiser forward (tensor-bound) against MEASURED_PEAKS.json;
-``sampler_roofline`` = the fused exchange+CFG+DDIM kernel (HBM-bound);
-``cpu_baseline`` = the oracle CPU path (fp32 torch U-Net + numpy sampler) on
-this host, bounded sample, extrapolated.
+(latency: each group generates one image per bench step, so the timed region /
+K; max over ranks); ``throughput_images_per_s`` = all images / timed region;
+``e2e`` = the same latency through the public API with host x_T in and host x0
+out each run; ``roofline`` = the denoiser forward the GPU runs (B=2 at N=1, B=1
+per GPU in pairs) against MEASURED_PEAKS.json; ``forward_b1`` = the B=1 branch
+forward, the reference's sequential rho=2 one-GPU latency built from it and the
+predicted pair latency; ``sampler_roofline`` = the fused exchange+CFG+DDIM
+kernel (HBM-bound); ``cpu_baseline`` = the oracle CPU path (fp32 torch U-Net +
+numpy sampler) on this host over whole denoising steps, x50.
 
 ``--impl reference`` times the reference's CPU implementation of the path
 (the oracle port: numpy fp64 sampler trio of schedules.py / monitor.py plus the
@@ -133,9 +136,12 @@ def _max_over_ranks(ws, v):
 
 
 # --------------------------------------------------------------------------------
-def cpu_reference_sample(spec, n_forwards: int = 1, threads: int | None = None, weights=None):
-    """Oracle CPU path on this host: fp32 torch U-Net forward (one branch, B=1) and
-    the numpy fp64 sampler trio at the latent size. Returns (s/image, details)."""
+def cpu_reference_sample(spec, n_steps: int = 2, threads: int | None = None, weights=None):
+    """Oracle CPU path on this host, timed over ``n_steps`` whole denoising steps of the
+    reference's serial runner (engine.py:195-214 with config.py:174 rho=2): per step the
+    fp32 torch U-Net evaluates the conditional and then the unconditional branch (B=1
+    each, sequentially) and the numpy fp64 trio (rel_mae, cfg, ddim) updates the latent.
+    Returns (s/image = 50 x the measured mean step, details)."""
     import torch
     from oracle import sampler as osmp
     from oracle.unet_ref import UNetRef
@@ -150,28 +156,27 @@ def cpu_reference_sample(spec, n_forwards: int = 1, threads: int | None = None, 
     net = UNetRef(spec, weights)
     cond = synthetic_conditioning(1, spec.context_len, spec.cross_dim, spec.pooled_dim)
     hw = spec.latent_hw
-    x = torch.randn(1, spec.in_channels, hw, hw)
-    fwd = []
-    with torch.no_grad():
-        for _ in range(n_forwards):
-            t1 = time.perf_counter()
-            net(x, torch.tensor([500.0]), cond.context, cond.pooled)
-            fwd.append(time.perf_counter() - t1)
-    n = hw * hw * spec.in_channels
-    rng = np.random.default_rng(0)
-    ec, eu, xs = rng.standard_normal((1, n)), rng.standard_normal((1, n)), rng.standard_normal((1, n))
     _, _, abar, sig = osmp.schedule_tables("scaled-linear", STEPS_T, 0.00085, 0.012)
-    t1 = time.perf_counter()
-    reps = 20
-    for _ in range(reps):
-        m = osmp.rel_mae(ec, eu)
-        e = osmp.cfg(ec, eu, 5.0)
-        xs = osmp.ddim(xs, e, 25, abar, sig)
-    trio = (time.perf_counter() - t1) / reps
-    f = min(fwd)
-    per_image = STEPS_T * (2 * f + trio)         # reference serial: rho = 2 branch evaluations / step
-    return per_image, {"forward_s": f, "sampler_trio_s": trio, "threads": threads, "weight_init_s": init_s,
-                       "m": m}
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(1, spec.in_channels, hw, hw, generator=g).double().numpy().reshape(1, -1)
+    steps, fwd = [], []
+    with torch.no_grad():
+        for i in range(n_steps):
+            t = STEPS_T - i
+            t1 = time.perf_counter()
+            xt = torch.from_numpy(x.reshape(1, spec.in_channels, hw, hw)).float()
+            tt = torch.tensor([float(t * (1000 // STEPS_T))])
+            ec = net(xt, tt, cond.context, cond.pooled).double().numpy().reshape(1, -1)
+            t2 = time.perf_counter()
+            eu = net(xt, tt, cond.null_context, cond.null_pooled).double().numpy().reshape(1, -1)
+            fwd.append(time.perf_counter() - t2)
+            fwd.append(t2 - t1)
+            m = osmp.rel_mae(ec, eu)
+            x = osmp.ddim(x, osmp.cfg(ec, eu, 5.0), t, abar, sig)
+            steps.append(time.perf_counter() - t1)
+    step = sum(steps) / len(steps)
+    return STEPS_T * step, {"step_s": step, "forward_s": min(fwd), "steps_measured": n_steps, "threads": threads,
+                            "weight_init_s": init_s, "m": float(np.asarray(m).ravel()[0])}
 
 
 def run_reference_arm(args):
@@ -190,8 +195,9 @@ def run_reference_arm(args):
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
-    sample = (f"per step: one fp32 CPU forward of the SDXL-shaped U-Net at B=1 (one branch) + the numpy "
-              f"fp64 cfg/rel_mae/ddim trio at N=65536, extrapolated x{STEPS_T} steps x2 branches")
+    sample = (f"per bench step: one whole denoising step of the reference serial runner on the host cores "
+              f"(fp32 SDXL-shaped U-Net, conditional then unconditional branch at B=1, numpy fp64 "
+              f"rel_mae/cfg/ddim at N=65536), x{STEPS_T} steps per image")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
@@ -245,22 +251,39 @@ def sampler_roofline(hbm_peak):
     return res
 
 
-def forward_roofline(den, spec, reps=20):
+def _graph_time(run, reps):
     import torch
-    from paper_2602_21760_b200.denoiser.unet import unet_flops
-    x = torch.randn(1, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
-    den.load_input(x)
     for _ in range(3):
-        den.branches(x, 30, den.input_slot())
+        run()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps):
-        den.branches(x, 30, den.input_slot())
+        run()
     b.record()
     torch.cuda.synchronize()
-    t = a.elapsed_time(b) / 1e3 / reps
+    return a.elapsed_time(b) / 1e3 / reps
+
+
+def forward_roofline(den, spec, reps=20):
+    """Back-to-back replays of the B=2 (both branches) forward graph."""
+    import torch
+    from paper_2602_21760_b200.denoiser.unet import unet_flops
+    x = torch.randn(1, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
+    den.load_input(x)
+    t = _graph_time(lambda: den.branches(x, 30, den.input_slot()), reps)
     return t, unet_flops(spec, 2)
+
+
+def forward_b1(den, spec, reps=20):
+    """Back-to-back replays of the B=1 conditional-branch forward graph: the work one GPU
+    of a condition-partitioned pair does per step, and half of the reference serial
+    runner's rho=2 step (engine.py:195-214, config.py:174: branches evaluated in turn)."""
+    import torch
+    from paper_2602_21760_b200.denoiser.unet import unet_flops
+    x = torch.randn(1, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
+    t = _graph_time(lambda: den.conditional(x, 30), reps)
+    return t, unet_flops(spec, 1)
 
 
 def top_kernel_rooflines(bf16_peak, reps=20):
@@ -366,7 +389,7 @@ def time_pairs(args, spec, ws, rank, local):
     den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=STEPS_T, seed=0)   # same weights in a pair
     plan = pipelines.sdxl_plan(spec, variant="hybrid", steps=STEPS_T, seed=role.pair, denoiser=den,
                                clock="device")
-    sess = parallel.PairSession(plan, groups[role.pair])
+    sess = parallel.GroupSession(plan, groups[role.pair])
     for _ in range(args.warmup):
         sess.run()
     x_host = hp.initial_latents(plan)
@@ -419,29 +442,36 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    import paper_2602_21760_b200 as hp
-    from paper_2602_21760_b200 import pipelines
-    from paper_2602_21760_b200.denoiser import kernels as DK
+    import paper_2602_21760_b200 as hp  # noqa: F401
     from paper_2602_21760_b200.denoiser.weights import SDXL, TINY
     spec = SDXL if args.spec == "sdxl" else TINY
     hbm_peak, bf16_burst, bf16_sus, peak_src = _peaks()
 
     mode = "single" if ws == 1 else args.mode
-    mode_note = None
-    den = None
-    if mode == "pairs":
-        try:
-            res = time_pairs(args, spec, ws, rank, local)
-        except Exception as exc:   # visible in the JSON line, never silent
-            mode_note = f"pairs mode failed ({type(exc).__name__}: {exc}); measured as replicas"
-            mode = "replicas"
-            _barrier(ws)
-    if mode != "pairs":
-        res = time_replicas(args, spec, ws, rank, local)
-    den, dev_s, images, e2e_s, h2d, d2h, clocks, steps_per_image = res
-    value = dev_s / images
+    err = None
+    try:
+        res = time_pairs(args, spec, ws, rank, local) if mode == "pairs" else time_replicas(args, spec, ws, rank, local)
+    except Exception as exc:   # agreed across ranks below; never silently re-measured another way
+        err = f"{mode} run failed on rank {rank}: {type(exc).__name__}: {exc}"
+        res = None
+    if ws > 1:
+        import torch.distributed as dist
+        flag = torch.tensor([1.0 if err else 0.0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        if flag.item() and not err:
+            err = "another rank failed"
+    if err:
+        if rank == 0 or "rank" in err:
+            print(json.dumps({"metric": METRIC, "unit": UNIT, "n_gpus": ws, "error": err}), flush=True)
+        return 1
+    den, dev_s, images, e2e_s, h2d, d2h, clocks, _ = res
+    # latency per image: every step each group (pair / replica) generates one image
+    # concurrently, so the per-image latency is the timed region over the K steps
+    value = dev_s / args.steps
+    e2e_value = e2e_s / args.steps
 
-    fwd_s, fwd_flops = forward_roofline(den, spec)
+    fwd_s, fwd_flops = forward_roofline(den, spec) if mode != "pairs" else (None, None)
+    b1_s, b1_flops = forward_b1(den, spec)
     launches_fwd = (den.g_both.launches if mode != "pairs"
                     else max(den.g_cond.launches, getattr(getattr(den, "g_uncond", None), "launches", 0)))
     samp = sampler_roofline(hbm_peak) if rank == 0 else {}
@@ -452,15 +482,24 @@ def main():
             import torch.distributed as dist
             dist.destroy_process_group()
         return 0
-    achieved_fwd = fwd_flops / fwd_s / 1e12
+    k1_s = samp[65536]["us"] * 1e-6 if samp else 0.0
     if mode != "pairs":
         # per GPU over the timed region itself: each rank ran K generations of 50 steps, each
         # step one B=2 forward (+ one sampler launch, counted in the time, not the FLOPs)
         achieved = fwd_flops * STEPS_T * args.steps / dev_s / 1e12
         achieved_src = "timed region: K x 50 denoiser forwards / CUDA-event time of the K generations"
+        roof_flops, roof_kernel = fwd_flops, "denoiser forward (tcgen05 GEMM/conv + attention), B=2 (both branches)"
     else:
-        achieved = achieved_fwd
-        achieved_src = "isolated forward graph replays (hybrid plans mix branch layouts per step)"
+        achieved = b1_flops / b1_s / 1e12
+        achieved_src = "isolated B=1 branch-forward graph replays (the per-GPU work of a pair)"
+        roof_flops, roof_kernel = b1_flops, "denoiser forward, B=1 (one branch per GPU)"
+    # what a condition-partitioned pair would take on this clock: one B=1 forward per GPU
+    # per step + the eps exchange (bf16 latent over NVLink: bytes / 770 GB/s measured peer
+    # copy + an assumed 5 us flag round trip) + the fused sampler kernel
+    numel = spec.latent_hw * spec.latent_hw * spec.in_channels
+    xch_s = numel * 2 / 770e9 + 5e-6
+    pair_pred = STEPS_T * (b1_s + xch_s + k1_s)
+    seq_rho2 = STEPS_T * (2 * b1_s + k1_s)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
@@ -471,18 +510,24 @@ def main():
                    "plan": ("hybrid on condition-partitioned pairs (L=12, g=4e-4, tau_cap=15, k=5)"
                             if mode == "pairs" else "serial (CFG batched B=2)"),
                    "parallelism": f"{mode}x{ws}" if ws > 1 else "single",
-                   "mode_note": mode_note,
                    "params_b": 2.567 if spec.name == "sdxl" else None,
                    "l2": "working set (5.1 GB of bf16 weights per step) >> 126 MB L2"},
-        "e2e": {"value": e2e_s / images, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(args.steps * STEPS_T * (launches_fwd + 1)),
-        "roofline": {"bound": "tensor", "kernel": "denoiser forward (tcgen05 GEMM/conv + attention), B=2",
+        "roofline": {"bound": "tensor", "kernel": roof_kernel,
                      "achieved": achieved, "achieved_source": achieved_src,
-                     "achieved_isolated_forward": achieved_fwd,
                      "peak": bf16_sus, "unit": "TFLOP/s", "frac": achieved / bf16_sus,
                      "peak_kind": f"{peak_src} sustained", "frac_of_burst": achieved / bf16_burst,
-                     "flops_per_launch": fwd_flops, "forward_ms": fwd_s * 1e3, **_forward_traffic(),
+                     "flops_per_launch": roof_flops,
+                     "forward_ms": fwd_s * 1e3 if fwd_s else None, **_forward_traffic(),
                      "top_kernels": top, "top_kernels_peak": f"{peak_src} burst bf16 {bf16_burst}"},
+        "forward_b1": {"ms": b1_s * 1e3, "tflops": b1_flops / b1_s / 1e12,
+                       "frac_of_sustained": b1_flops / b1_s / 1e12 / bf16_sus, "flops": b1_flops,
+                       "sequential_rho2_s_per_image": seq_rho2,
+                       "predicted_pair_latency_s": pair_pred,
+                       "predicted_pair_speedup_vs_batched": (value / pair_pred) if mode == "single" else None,
+                       "predicted_pair_speedup_vs_sequential": seq_rho2 / pair_pred,
+                       "model": "50 x (B=1 forward + exchange (numel*2 B / 770 GB/s + 5 us) + sampler kernel)"},
         "sampler_roofline": {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_src,
                              "sizes": list(samp.values())},
         "clocks": clocks.summary(),
@@ -490,11 +535,12 @@ def main():
     }
     if ws == 1 and not args.no_cpu_baseline:
         try:
-            v, det = cpu_reference_sample(spec, 1)
+            v, det = cpu_reference_sample(spec, 2)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": det["threads"], "kind": "port",
-                                    "sample": "one fp32 CPU forward of the same-shape U-Net at B=1 + the numpy fp64 "
-                                              "cfg/rel_mae/ddim trio at the latent size; x50 steps x2 branches",
-                                    "forward_s": det["forward_s"], "sampler_trio_s": det["sampler_trio_s"]}
+                                    "sample": f"{det['steps_measured']} whole denoising steps of the serial runner "
+                                              "(fp32 CPU U-Net, cond then uncond branch at B=1, numpy fp64 "
+                                              "rel_mae/cfg/ddim at the latent size), mean step x50",
+                                    "step_s": det["step_s"], "forward_s": det["forward_s"]}
         except Exception as exc:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"failed: {exc}"}
@@ -502,7 +548,6 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
-    _ = DK
     return 0
 
 

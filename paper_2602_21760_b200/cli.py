@@ -8,7 +8,8 @@ on the GPU through the fused sampler; ``--denoiser`` swaps the analytic GMM
 for a neural network at the seam (then the curve's score_ratio column repeats
 the measured rel-MAE, the identity the reference's criterion 01 pins for
 exact scores); ``--clock device`` exports CUDA-event timings in trace.csv /
-trace.json instead of the model clock.
+trace.json instead of the model clock; ``calibrate`` (no reference
+counterpart) derives tau_cap from measured curves.
 """
 from __future__ import annotations
 
@@ -56,6 +57,23 @@ def _denoiser_for(name, cfg, plan):
     return pipelines.build_sd3_denoiser(spec, n_prompts=n, steps=plan.schedule.T)
 
 
+def _net_plan_fields(name, plan):
+    """Schedule, sampler, latent prior and conditions of a network at the seam: the
+    config keeps T, seeds, variant, switch, devices and link; the network brings its
+    own noise schedule (SDXL scaled-linear DDIM, SD3 flow-matching Euler) and a
+    latent-shaped prior with one component per prompt (pipelines.latent_prior)."""
+    from . import pipelines
+    from .denoiser.weights import SD3, SDXL, TINY, TINY_DIT
+    from .mixture import Condition
+    spec = {"sdxl": SDXL, "tiny": TINY, "sd3": SD3, "tiny-dit": TINY_DIT}[name]
+    dit = name in ("sd3", "tiny-dit")
+    T, n = plan.schedule.T, len(plan.conditions)
+    return dict(schedule=pipelines.sd3_schedule(T) if dit else pipelines.sdxl_schedule(T),
+                sampler="euler" if dit else "ddim",
+                mixture=pipelines.latent_prior(n, spec.latent_hw * spec.latent_hw * spec.in_channels),
+                conditions=tuple(Condition((i,)) for i in range(n)))
+
+
 def _plan(cfg, args, **kw):
     from dataclasses import replace
     plan = cfg.to_plan(**kw)
@@ -63,7 +81,7 @@ def _plan(cfg, args, **kw):
     if getattr(args, "denoiser", None) not in (None, "gmm"):
         if den is None:
             den = args._den = _denoiser_for(args.denoiser, cfg, plan)
-        plan = replace(plan, denoiser=den)
+        plan = replace(plan, denoiser=den, **_net_plan_fields(args.denoiser, plan))
     if getattr(args, "clock", None):
         plan = replace(plan, clock=args.clock)
     if getattr(args, "pipeline_numerics", None):
@@ -185,6 +203,45 @@ def detect(args) -> int:
     return 0
 
 
+def calibrate_tau_cap(curves, switch, T: int, margin: int = 1) -> dict:
+    """tau_cap from measured discrepancy curves: replay each
+    curve through the controller with the cap out of the way (tau_cap = T - k - 1)
+    to find the step at which the slope detector fires by itself (natural tau1),
+    then cap one ``margin`` past the latest natural firing so the cap never
+    pre-empts detection on these trajectories. Curves on which the detector never
+    fires keep the configured cap (reported as ``binding``)."""
+    from .monitor import SwitchConfig
+    loose = SwitchConfig(L=switch.L, g_slope=switch.g_slope, tau_cap=max(1, T - switch.k - 1), k=switch.k)
+    per = []
+    for name, pairs in curves:
+        state, _ = replay_series(pairs, loose)
+        fired = state.tau1 is not None and state.tau1 < loose.tau_cap
+        ms = dict(pairs)
+        t_fire = T - state.tau1 + 1 if fired else None
+        g = ((ms[t_fire] - ms[t_fire + switch.L]) / switch.L
+             if fired and t_fire + switch.L in ms else None)
+        per.append({"curve": name, "natural_tau1": state.tau1 if fired else None,
+                    "t_at_firing": t_fire, "slope_at_firing": g,
+                    "slope_margin": None if g is None else switch.g_slope - g})
+    natural = [c["natural_tau1"] for c in per if c["natural_tau1"] is not None]
+    binding = len(natural) < len(per)
+    tau_cap = switch.tau_cap if binding else min(max(natural) + margin, T - switch.k - 1)
+    cal = SwitchConfig(L=switch.L, g_slope=switch.g_slope, tau_cap=tau_cap, k=switch.k)
+    for c, (_, pairs) in zip(per, curves):
+        st, labels = replay_series(pairs, cal)
+        c["detect"] = {"tau1": st.tau1, "tau2": st.tau2, "stages": [x.value for x in labels]}
+    return {"L": switch.L, "g_slope": switch.g_slope, "k": switch.k, "T": T, "margin": margin,
+            "configured_tau_cap": switch.tau_cap, "tau_cap": tau_cap, "cap_binding": binding, "curves": per}
+
+
+def calibrate(args) -> int:
+    cfg = _config(args.config)
+    curves = [(path, read_series_csv(path)) for path in args.series]
+    T = max(t for _, pairs in curves for t, _ in pairs)
+    sys.stdout.write(_dump(calibrate_tau_cap(curves, cfg.switch, T, args.margin)))
+    return 0
+
+
 def _k_values(text: str) -> list:
     try:
         return sorted({int(tok) for tok in text.replace(" ", "").split(",") if tok})
@@ -233,6 +290,8 @@ def _parser() -> argparse.ArgumentParser:
                       ("--out", dict(help="output directory"))]),
         "curve": (curve, "emit the discrepancy curve CSV", [("--out", dict(required=True))]),
         "detect": (detect, "replay switch detection over a series CSV", [("--series", dict(required=True))]),
+        "calibrate": (calibrate, "tau_cap from measured discrepancy curves (natural slope detection)",
+                      [("--series", dict(required=True, nargs="+")), ("--margin", dict(type=int, default=1))]),
         "sweep": (sweep, "sweep the pipelined-window width k",
                   [("--k", dict(required=True)), ("--out", dict(help="destination CSV; stdout if omitted"))]),
     }

@@ -574,7 +574,9 @@ class GroupSession:
         b.record()
         torch.cuda.synchronize()
         sent = sum(nb for _, nb, _, _ in ops.msgs)
-        red = torch.tensor([a.elapsed_time(b) / 1e3, float(sent)], dtype=torch.float64)
+        # NCCL reduces device tensors only; gloo (CPU tests) host tensors
+        on = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        red = torch.tensor([a.elapsed_time(b) / 1e3, float(sent)], dtype=torch.float64, device=on)
         mx, tot = red[:1].clone(), red[1:].clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=self.group)
         dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=self.group)
@@ -621,7 +623,8 @@ def run_batch_level_distributed(plan: ExecutionPlan, exchange: str = "p2p") -> R
     sub = replace(plan, variant=PlanVariant.HYBRID, devices=plan.devices[:2], segment_fractions=None,
                   seed=plan.seed + role.pair)
     res = run_pair(sub, groups[role.pair], exchange)
-    lat = torch.tensor([res.latency_s], dtype=torch.float64)
+    lat = torch.tensor([res.latency_s], dtype=torch.float64,
+                       device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(lat, op=dist.ReduceOp.MAX)
     pairs = ws // 2
     latency = float(lat.item())

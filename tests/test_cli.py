@@ -89,3 +89,56 @@ def test_sweep_matches_reference(gold, tmp_path, capsys):
         for x, y in zip(fa[2:], fb[2:]):
             if x or y:
                 assert abs(float(x) - float(y)) <= 1e-9 * max(1.0, abs(float(y))), (a, b)
+
+
+def test_calibrate_on_reference_curve(gold, capsys):
+    """tau_cap calibration on the reference's own curve: the cap
+    lands one step past the natural firing, and the detect replay under it fires
+    naturally at the same step (the cap is not what switches)."""
+    d, out = gold
+    path = os.path.join(d, "curve.csv")
+    assert cli.main(["calibrate", "--series", path, path]) == 0
+    cal = json.loads(capsys.readouterr().out)
+    c = cal["curves"][0]
+    if cal["cap_binding"]:
+        assert c["natural_tau1"] is None and cal["tau_cap"] == cal["configured_tau_cap"]
+        return
+    assert cal["tau_cap"] == min(c["natural_tau1"] + 1, cal["T"] - cal["k"] - 1)
+    assert c["detect"]["tau1"] == c["natural_tau1"]
+    assert c["detect"]["tau2"] == c["natural_tau1"] + cal["k"]
+    assert 0.0 <= c["slope_at_firing"] < cal["g_slope"] and c["slope_margin"] > 0
+
+
+def test_calibrate_cap_binding_on_flat_start(tmp_path, capsys):
+    """A curve whose slope never enters [0, g) keeps the configured cap."""
+    p = tmp_path / "c.csv"
+    p.write_text("t,rel_mae\n" + "".join(f"{t},{0.5 + 0.01 * t}\n" for t in range(50, 0, -1)))
+    assert cli.main(["calibrate", "--series", str(p)]) == 0
+    cal = json.loads(capsys.readouterr().out)
+    assert cal["cap_binding"] and cal["tau_cap"] == cal["configured_tau_cap"]
+    assert cal["curves"][0]["detect"]["tau1"] == cal["configured_tau_cap"]
+
+
+@pytest.mark.gpu
+def test_curve_and_calibrate_on_tiny_unet(tmp_path, capsys):
+    """`curve --denoiser tiny` (BASELINE config 1 network at the seam, latent-shaped
+    prior and the network's own schedule) then `calibrate` over two seeds."""
+    paths = []
+    for s in (0, 1):
+        cfg = tmp_path / f"c{s}.json"
+        cfg.write_text(json.dumps({"variant": "serial", "schedule": {"T": 20}, "seeds": [s],
+                                   "condition_batch": 1, "switch": {"L": 4, "g_slope": 4e-4, "tau_cap": 8, "k": 5}}))
+        out = tmp_path / f"curve{s}.csv"
+        assert cli.main(["curve", "--config", str(cfg), "--denoiser", "tiny", "--out", str(out)]) == 0
+        rows = out.read_text().splitlines()
+        assert rows[0] == cli.CURVE_HEADER and len(rows) == 21
+        ts = [int(r.split(",")[0]) for r in rows[1:]]
+        assert ts == list(range(20, 0, -1))
+        assert all(float(r.split(",")[1]) > 0 for r in rows[1:])
+        paths.append(str(out))
+    capsys.readouterr()
+    assert cli.main(["calibrate", "--config", str(cfg), "--series", *paths]) == 0
+    cal = json.loads(capsys.readouterr().out)
+    assert cal["T"] == 20 and 1 <= cal["tau_cap"] <= 20 - 5 - 1
+    for c in cal["curves"]:
+        assert c["detect"]["tau1"] <= cal["tau_cap"]

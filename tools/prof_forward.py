@@ -1,6 +1,9 @@
 """Run SDXL-shaped U-Net forwards eagerly (no CUDA graph) for ncu launch lists.
 
-    python tools/prof_forward.py [n_forwards] [tiny]
+    python tools/prof_forward.py [n_forwards] [tiny] [b1]
+
+``b1``: the B=1 conditional-branch forward (one GPU of a condition-partitioned
+pair) instead of the B=2 CFG batch.
 
 Prints the number of our kernel launches per forward so ncu's -s can skip the
 warm-up forward.
@@ -23,7 +26,10 @@ def main():
     den.load_input(x)
     for i in range(n):
         before = K.LAUNCHES
-        den.branches(x, 30, den.input_slot())
+        if "b1" in sys.argv:
+            den.conditional(x, 30)
+        else:
+            den.branches(x, 30, den.input_slot())
         torch.cuda.synchronize()
         print(f"forward {i}: {K.LAUNCHES - before} launches", flush=True)
 
