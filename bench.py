@@ -238,6 +238,7 @@ def sampler_roofline(hbm_peak):
         times = []
         for _ in range(20):
             flush.zero_()                                    # evict L2 (> 126 MB)
+            torch.cuda._sleep(100000)                        # GPU busy while the host enqueues: device time only
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             launch()

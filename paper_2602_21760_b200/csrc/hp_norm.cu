@@ -6,7 +6,9 @@
 // on the other images in the batch. Normally one launch: an image's statistics
 // CTAs meet at an in-kernel barrier (all resident: occupancy-checked), each CTA
 // having staged its pixel chunk in shared memory with bulk async copies when the
-// chunk is >= 16 KB. LayerNorm is one warp per row with an
+// chunk is >= 16 KB. The barrier words belong to the launch (a slot per stream
+// for eager launches, a fresh slot per captured graph node) and the launch is
+// cooperative, so co-residency is guaranteed by the driver, not assumed. LayerNorm is one warp per row with an
 // exact two-pass mean/variance from registers and optional adaLN modulation.
 // Everything else is a 16-byte-vectorised streaming kernel.
 #include <cuda_runtime.h>
@@ -14,6 +16,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <math.h>
+#include <mutex>
+#include <unordered_map>
 #include "hybridpar_b200_denoiser.h"
 #include "hp_common.cuh"
 #include "hp_tc.cuh"
@@ -839,26 +843,54 @@ __global__ void cast_kernel(const bf16* __restrict__ x, float* __restrict__ y, i
 
 inline int ok() { return cudaGetLastError() == cudaSuccess ? HP_OK : HP_ERR_CUDA; }
 
-// barrier words of the single-launch GroupNorm: [image][count, generation], zeroed
-// once, never reset by the host (the last arriver resets the count)
+// barrier words of the single-launch GroupNorm: [image][count, generation]. A slot is
+// zeroed once when the pool is made and left consistent by every use (the last
+// arriver resets the count), so only CONCURRENT launches must not share one: eager
+// launches take one slot per stream (launches on a stream are ordered: each
+// gn_fused_kernel waits for its predecessor with griddepcontrol.wait before it
+// arrives), every launch captured into a CUDA graph a slot of its own (graph replays
+// on different streams may overlap). Pools are per device; an exhausted pool sends
+// the launch to the two-kernel path.
 constexpr int kGnMaxImages = 64;
-unsigned* g_gn_bar = nullptr;
+constexpr int kGnSlotWords = 2 * kGnMaxImages;
+constexpr int kGnSlots = 4096;
+struct GnBarPool {
+  unsigned* base = nullptr;
+  int next = 0;
+  std::unordered_map<cudaStream_t, unsigned*> per_stream;
+};
+unsigned* gn_bar_slot(cudaStream_t st, bool capturing) {
+  static std::mutex mu;
+  static std::unordered_map<int, GnBarPool> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  GnBarPool& pool = pools[dev];
+  if (!pool.base) {
+    if (capturing) return nullptr;                 // no allocation inside a capture
+    const size_t bytes = (size_t)kGnSlots * kGnSlotWords * sizeof(unsigned);
+    if (cudaMalloc(&pool.base, bytes) != cudaSuccess) { pool.base = nullptr; return nullptr; }
+    if (cudaMemset(pool.base, 0, bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return nullptr;
+  }
+  if (!capturing) {
+    auto it = pool.per_stream.find(st);
+    if (it != pool.per_stream.end()) return it->second;
+  }
+  if (pool.next >= kGnSlots) return nullptr;
+  unsigned* slot = pool.base + (size_t)(pool.next++) * kGnSlotWords;
+  if (!capturing) pool.per_stream[st] = slot;
+  return slot;
+}
 
 constexpr size_t kGnSmemMax = 112 * 1024;   // staged chunk + scratch limit: two CTAs per SM
 constexpr size_t kGnSmemMin = 16 * 1024;    // smaller chunks: direct loads are faster
 
 // 0: two-kernel path; 1: single launch reading global memory; 2: single launch with the
 // chunk staged in shared memory (`smem` bytes)
-int gn_fused_mode(int ctas, size_t smem, cudaStream_t st) {
+int gn_fused_mode(int ctas, size_t smem) {
   static bool disabled = getenv("HP_GN_FUSED") && getenv("HP_GN_FUSED")[0] == '0';
   static bool no_smem = getenv("HP_GN_SMEM") && getenv("HP_GN_SMEM")[0] == '0';
   if (disabled) return 0;
-  if (!g_gn_bar) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return 0;
-    if (cudaMalloc(&g_gn_bar, 2 * kGnMaxImages * sizeof(unsigned)) != cudaSuccess) { g_gn_bar = nullptr; return 0; }
-    if (cudaMemset(g_gn_bar, 0, 2 * kGnMaxImages * sizeof(unsigned)) != cudaSuccess) return 0;
-  }
   static int sms = 0;
   static bool attr = false;
   if (!sms) {
@@ -868,7 +900,8 @@ int gn_fused_mode(int ctas, size_t smem, cudaStream_t st) {
     attr = cudaFuncSetAttribute(gn_fused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kGnSmemMax) == cudaSuccess;
   }
-  // every CTA resident (occupancy-checked): the in-kernel barrier cannot deadlock
+  // every CTA resident: checked here, and the launch is cooperative (the driver
+  // refuses it rather than run it partially resident, e.g. under MPS limits)
   int per_sm = 0;
   if (!no_smem && attr && smem <= kGnSmemMax &&
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gn_fused_kernel<true>, kGnThreads, smem) ==
@@ -903,14 +936,34 @@ int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_
   }();
   const bool stage = gn_chunk_bytes(hw, splits, C) >= smem_min;
   const size_t smem = gn_smem_bytes(hw, splits, C);
-  const int mode = n <= kGnMaxImages ? gn_fused_mode(n * splits, stage ? smem : kGnSmemMax + 1, st) : 0;
+  int mode = n <= kGnMaxImages ? gn_fused_mode(n * splits, stage ? smem : kGnSmemMax + 1) : 0;
+  unsigned* bar = nullptr;
+  if (mode) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return HP_ERR_CUDA;
+    bar = gn_bar_slot(st, cs != cudaStreamCaptureStatusNone);
+    if (!bar) mode = 0;
+  }
   if (mode) {
     const auto kern = mode == 2 ? gn_fused_kernel<true> : gn_fused_kernel<false>;
-    hp_launch_pdl(kern, dim3(splits, n), dim3(kGnThreads), mode == 2 ? smem : 0, st, static_cast<const bf16*>(x1),
-                  c1, static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups, splits, stats, eps, gamma, beta, do_silu,
-                  static_cast<bf16*>(y), g_gn_bar);
-    if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
-    return ok();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(splits, n);
+    cfg.blockDim = dim3(kGnThreads);
+    cfg.dynamicSmemBytes = mode == 2 ? smem : 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = hp_pdl_enabled() ? 2 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<const bf16*>(x1), c1,
+                                             static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups, splits, stats,
+                                             eps, gamma, beta, do_silu, static_cast<bf16*>(y), bar);
+    if (e == cudaSuccess) return ok();
+    if (e != cudaErrorCooperativeLaunchTooLarge) return HP_ERR_CUDA;
+    (void)cudaGetLastError();                      // refused (not co-resident): two-kernel path
   }
   hp_launch_pdl(gn_stats_kernel, dim3(splits, n), dim3(kGnThreads), 0, st, static_cast<const bf16*>(x1), c1,
                                                           static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups,

@@ -158,6 +158,44 @@ def test_group_norm_batch_invariant(hw, c):
     assert torch.equal(both[hw:], one)
 
 
+def test_group_norm_concurrent_streams_and_graphs():
+    """Single-launch GroupNorms in flight at once on two streams, and inside two CUDA
+    graphs replayed on two streams, each with its own barrier slot: every output
+    matches the reference (a shared barrier would mix the images' arrivals)."""
+    n, hw, c = 2, 4096, 640
+    xs = [rnd(n * hw, c, s=2.0) + 0.5 * i for i in range(2)]
+    g, b = torch.randn(c, device="cuda"), torch.randn(c, device="cuda")
+    refs = [F.group_norm(x.float().view(n, hw, c).permute(0, 2, 1), 32, g, b, eps=1e-5).permute(0, 2, 1)
+            .reshape(n * hw, c) for x in xs]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [torch.empty(n * hw, c, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    torch.cuda.synchronize()
+    for _ in range(20):
+        for i in range(2):
+            with torch.cuda.stream(streams[i]):
+                K.group_norm(xs[i], n, hw, c, g, b, out=outs[i])
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        close(o, r)
+    graphs = []
+    for i in range(2):
+        K.group_norm(xs[i], n, hw, c, g, b, out=outs[i])        # warm (attributes, pool)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            K.group_norm(xs[i], n, hw, c, g, b, out=outs[i])
+        graphs.append(gr)
+    for o in outs:
+        o.zero_()
+    torch.cuda.synchronize()
+    for _ in range(20):
+        for i in range(2):
+            with torch.cuda.stream(streams[i]):
+                graphs[i].replay()
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        close(o, r)
+
+
 @pytest.mark.parametrize("c", [640, 1280, 1536])
 def test_layer_norm(c):
     x = rnd(700, c) + 1.0
