@@ -3,7 +3,8 @@
 // Two kernels (hp_attention picks one):
 //   attn_single_kernel   S_kv <= 128 (cross-attention, causal text-encoder
 //                        attention): two query tiles per CTA, 2 CTAs/SM.
-//   attn_stream_kernel   everything else: two softmax "streams" per CTA, each
+//   attn_stream_kernel   everything else, persistent (one CTA per SM walks the
+//                        work units): two softmax "streams" per CTA, each
 //                        with its own score-MMA and PV-MMA issuing warp; the
 //                        128-score row is pulled into registers in one TMEM
 //                        load and S released at once, so S(i+1) = Q K(i+1)^T
@@ -19,8 +20,8 @@
 // polynomial on the FMA pipe (P is rounded to bf16 anyway); P is stored to TMEM as
 // bf16 pairs and read by a TS-MMA (O += P V, V MN-major straight from its TMA tile).
 // Round-2 measurements (tools/attn_ab.py, tools/micro/attn_trace.cu, profiles/r02):
-// S=4096 B=2 H=10: 151 -> 128 us; S=1024 B=2 H=20: 30 -> 27.5 us; SD3 S=4429 B=2
-// H=24: 420 -> 342 us. The period per 128-key block pair is ~2500 clk against
+// S=4096 B=2 H=10: 151 -> 128 us; S=1024 B=2 H=20: 30 -> 25.8 us; SD3 S=4429 B=2
+// H=24: 420 -> 307 us. The period per 128-key block pair is ~2500 clk against
 // ~1240 clk of tensor work (PV at N=64 runs at 45 clk per K=16 step, not 32) and
 // ~1300 clk of MUFU: the softmax's issue/latency chain is the limit.
 #include <cuda.h>
@@ -46,7 +47,7 @@ constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;            // log2 units
 
 struct AttnParams {
-  int sq, skv, heads;
+  int sq, skv, heads, batch;
   int causal;
   int q_col0, k_col0, v_col0;
   __nv_bfloat16* o; long long ldo;
@@ -328,20 +329,24 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 // FMNMX3 tree for the row max, exp2 (5/8 MUFU, 3/8 FMA polynomial) with four
 // partial sums, then the O rescale (lazy, > 2^8 only) once PV(i-1) is done, P
 // stored to TMEM, p_full arrive.
+// Persistent: one CTA per SM walks work units (PAIR: 256 queries of one (head,
+// batch); SPLIT: 128) round-robin, so barrier init, TMEM allocation and the launch
+// happen once, and the next unit's Q / K / V loads and first score MMA overlap the
+// current unit's last blocks and epilogue (Q double-buffered). Every unit is
+// computed the same way wherever it runs: batch-invariant.
 constexpr int kStrThreads = 512;
-constexpr int kStrSplitStages = 3, kStrPairStages = 5;
+constexpr int kStrSplitStages = 2, kStrPairStages = 4;
 template <bool SPLIT> struct StrCfg {
-  static constexpr int kNq = SPLIT ? 1 : 2;                   // Q tiles in smem
+  static constexpr int kNq = SPLIT ? 1 : 2;                   // Q tiles per unit
   static constexpr int kSlots = SPLIT ? 2 * kStrSplitStages : kStrPairStages;
-  static constexpr size_t kSmem = 1024 + (size_t)kTileBytes * (kNq + 2 * kSlots) + 256 + 4 * kBQ * 4;
+  static constexpr size_t kSmem = 1024 + (size_t)kTileBytes * (2 * kNq + 2 * kSlots) + 256 + 4 * kBQ * 4;
 };
 
 #ifdef HP_ATTN_TRACE
-// event timeline of CTA (0,0,0) for tools/micro/attn_trace.cu: [stream][event][block]
+// event timeline of CTA 0 for tools/micro/attn_trace.cu: [stream][event][block]
 __device__ long long g_attn_trace[2][12][256];
 #define HP_TRACE(cond, q, ev, i) \
-  do { if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 256) \
-         g_attn_trace[q][ev][i] = clock64(); } while (0)
+  do { if ((cond) && blockIdx.x == 0 && (i) < 256) g_attn_trace[q][ev][i] = clock64(); } while (0)
 #else
 #define HP_TRACE(cond, q, ev, i) do {} while (0)
 #endif
@@ -351,14 +356,16 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                    const __grid_constant__ CUtensorMap tmV, AttnParams p) {
   using Cfg = StrCfg<SPLIT>;
   constexpr int kSlots = Cfg::kSlots;
+  constexpr int kNq = Cfg::kNq;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + Cfg::kNq * kTileBytes;                    // [slot]
+  uint8_t* sQ = smem;                                          // [2 units][kNq tiles]
+  uint8_t* sK = sQ + 2 * kNq * kTileBytes;                     // [slot]
   uint8_t* sV = sK + kSlots * kTileBytes;                      // [slot]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kSlots * kTileBytes);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = q_full + 1;                              // [kSlots]
+  uint64_t* q_full = bars;                                     // [2]
+  uint64_t* q_empty = q_full + 2;                              // [2]
+  uint64_t* kv_full = q_empty + 2;                             // [kSlots]
   uint64_t* kv_empty = kv_full + kSlots;                       // [kSlots]
   uint64_t* s_full = kv_empty + kSlots;                        // [stream]
   uint64_t* s_free = s_full + 2;
@@ -368,21 +375,25 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   float* s_ml = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);   // [stream][2][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int q0 = blockIdx.x * Cfg::kNq * kBQ;
   const int J = p.n_kv;
   const int jh = SPLIT ? (J + 1) / 2 : J;
-  // blocks of stream q: [jb(q), jb(q) + nj(q))
+  const int n_qt = (p.sq + kNq * kBQ - 1) / (kNq * kBQ);
+  const int n_units = n_qt * p.heads * p.batch;
+  // blocks of stream q within a unit: [jb(q), jb(q) + nj(q))
   auto jb = [&](int q) { return SPLIT ? q * jh : 0; };
   auto nj = [&](int q) { return SPLIT ? (q == 0 ? jh : J - jh) : J; };
-  // ring slot and phase of the i-th block of stream q
-  auto slot = [&](int q, int i) { return SPLIT ? q * kStrSplitStages + i % kStrSplitStages : i % kStrPairStages; };
-  auto phase = [&](int i) { return SPLIT ? (i / kStrSplitStages) & 1 : (i / kStrPairStages) & 1; };
+  // ring slot / phase of stream q's running block index g (over all units of this CTA)
+  auto slot = [&](int q, int g) { return SPLIT ? q * kStrSplitStages + g % kStrSplitStages : g % kStrPairStages; };
+  auto phase = [&](int g) { return SPLIT ? (g / kStrSplitStages) & 1 : (g / kStrPairStages) & 1; };
+  // unit u -> (query tile, head, batch)
+  auto unit_q0 = [&](int u) { return (u % n_qt) * kNq * kBQ; };
+  auto unit_h = [&](int u) { return (u / n_qt) % p.heads; };
+  auto unit_b = [&](int u) { return u / (n_qt * p.heads); };
 
   if (warp == 8 && lane == 0) {
     prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < kSlots; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], SPLIT ? 2 : 4); }   // S and PV commits per stream
+    for (int i = 0; i < 2; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 2); }   // both S issuers
+    for (int s = 0; s < kSlots; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], SPLIT ? 2 : 4); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1); mbar_init(&s_free[i], 4); mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1);
     }
@@ -399,66 +410,79 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   if (warp >= 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
   if (warp == 8 || (SPLIT && warp == 9)) {
-    // K/V producer(s): warp 8 feeds stream 0 (and, PAIR, the shared ring), warp 9
-    // stream 1 (SPLIT), so one stream's full ring never stalls the other's loads
+    // producers: warp 8 loads Q and stream 0's K/V (PAIR: the shared ring), warp 9
+    // stream 1's K/V (SPLIT), so one stream's full ring never stalls the other's loads
     if (lane == 0) {
       const int q = warp - 8;
-      if (q == 0) {
-        mbar_arrive_expect_tx(q_full, Cfg::kNq * kTileBytes);
+      int g = 0;
+      for (int u = blockIdx.x, k = 0; u < n_units; u += gridDim.x, ++k) {
+        const int h = unit_h(u), b = unit_b(u);
+        if (q == 0) {
+          const int qs = k & 1;
+          mbar_wait_park(&q_empty[qs], ((k >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&q_full[qs], kNq * kTileBytes);
 #pragma unroll
-        for (int t = 0; t < Cfg::kNq; ++t)
-          tma_load_3d(sQ + t * kTileBytes, &tmQ, q_full, p.q_col0 + h * kD, q0 + t * kBQ, b);
-      }
-      for (int i = 0; i < nj(q); ++i) {
-        const int s = slot(q, i), g = jb(q) + i;
-        mbar_wait_park(&kv_empty[s], phase(i) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[s], 2 * kTileBytes);
-        tma_load_3d(sK + s * kTileBytes, &tmK, &kv_full[s], p.k_col0 + h * kD, g * kBK, b);
-        tma_load_3d(sV + s * kTileBytes, &tmV, &kv_full[s], p.v_col0 + h * kD, g * kBK, b);
+          for (int t = 0; t < kNq; ++t)
+            tma_load_3d(sQ + (qs * kNq + t) * kTileBytes, &tmQ, &q_full[qs], p.q_col0 + h * kD,
+                        unit_q0(u) + t * kBQ, b);
+        }
+        for (int i = 0; i < nj(q); ++i, ++g) {
+          const int s = slot(q, g), j = jb(q) + i;
+          mbar_wait_park(&kv_empty[s], phase(g) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[s], 2 * kTileBytes);
+          tma_load_3d(sK + s * kTileBytes, &tmK, &kv_full[s], p.k_col0 + h * kD, j * kBK, b);
+          tma_load_3d(sV + s * kTileBytes, &tmV, &kv_full[s], p.v_col0 + h * kD, j * kBK, b);
+        }
       }
     }
   } else if (warp == 10 || warp == 11) {
-    // S issuer of stream q: S(i) as soon as K(i) is in and the softmax holds S(i-1)
+    // S issuer of stream q: S(g) as soon as K(g) is in and the softmax holds S(g-1)
     // in registers. tcgen05.mma holds the issuing thread until the tensor pipe takes
     // the instruction, so S and PV get separate issuers: a queued PV never delays S.
     const int q = warp - 10;
     if (lane == 0) {
-      mbar_wait_park(q_full, 0);
-      const uint64_t dq = sdesc_sw128_kmajor(sQ + (SPLIT ? 0 : q * kTileBytes));
       const uint32_t t_s = tmem + q * kBK;
-      const int n = nj(q);
-      for (int i = 0; i < n; ++i) {
-        mbar_wait_park(&kv_full[slot(q, i)], phase(i));
-        HP_TRACE(true, q, 0, i);
-        if (i > 0) mbar_wait_park(&s_free[q], (i - 1) & 1);
-        HP_TRACE(true, q, 1, i);
-        tc_fence_after();
-        const uint64_t dk = sdesc_sw128_kmajor(sK + slot(q, i) * kTileBytes);
+      int g = 0;
+      for (int u = blockIdx.x, k = 0; u < n_units; u += gridDim.x, ++k) {
+        const int qs = k & 1;
+        mbar_wait(&q_full[qs], (k >> 1) & 1);
+        const uint64_t dq = sdesc_sw128_kmajor(sQ + (qs * kNq + (SPLIT ? 0 : q)) * kTileBytes);
+        for (int i = 0; i < nj(q); ++i, ++g) {
+          mbar_wait(&kv_full[slot(q, g)], phase(g));
+          HP_TRACE(true, q, 0, g);
+          if (g > 0) mbar_wait(&s_free[q], (g - 1) & 1);
+          HP_TRACE(true, q, 1, g);
+          tc_fence_after();
+          const uint64_t dk = sdesc_sw128_kmajor(sK + slot(q, g) * kTileBytes);
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) umma_bf16(t_s, dq + 2 * k, dk + 2 * k, kIdescS, k > 0 ? 1u : 0u);
-        umma_commit(&s_full[q]);
-        umma_commit(&kv_empty[slot(q, i)]);
-        HP_TRACE(true, q, 2, i);
+          for (int kk = 0; kk < kD / 16; ++kk) umma_bf16(t_s, dq + 2 * kk, dk + 2 * kk, kIdescS, kk > 0 ? 1u : 0u);
+          umma_commit(&s_full[q]);
+          umma_commit(&kv_empty[slot(q, g)]);
+          if (i == nj(q) - 1) umma_commit(&q_empty[qs]);      // this unit's Q is read
+          HP_TRACE(true, q, 2, g);
+        }
       }
     }
   } else if (warp == 12 || warp == 13) {
-    // PV issuer of stream q: O_q += P_q(i) V(i) once the softmax published P(i)
+    // PV issuer of stream q: O_q (+)= P_q(g) V(g) once the softmax published P(g)
     const int q = warp - 12;
     if (lane == 0) {
       const uint32_t t_o = tmem + 256 + q * kD, t_p = tmem + 384 + q * 64;
-      const int n = nj(q);
-      for (int i = 0; i < n; ++i) {
-        mbar_wait_park(&p_full[q], i & 1);
-        HP_TRACE(true, q, 3, i);
-        tc_fence_after();
-        const uint8_t* v = sV + slot(q, i) * kTileBytes;
+      int g = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        for (int i = 0; i < nj(q); ++i, ++g) {
+          mbar_wait(&p_full[q], g & 1);
+          HP_TRACE(true, q, 3, g);
+          tc_fence_after();
+          const uint8_t* v = sV + slot(q, g) * kTileBytes;
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          const uint64_t dv = sdesc_sw128_mnmajor(v + k * 2048, 8192);
-          umma_bf16_ts(t_o, t_p + 8 * k, dv, kIdescO, (i > 0 || k > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t dv = sdesc_sw128_mnmajor(v + kk * 2048, 8192);
+            umma_bf16_ts(t_o, t_p + 8 * kk, dv, kIdescO, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&o_done[q]);
+          umma_commit(&kv_empty[slot(q, g)]);
         }
-        umma_commit(&o_done[q]);
-        umma_commit(&kv_empty[slot(q, i)]);
       }
     }
   }
@@ -472,145 +496,154 @@ attn_stream_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t t_s = tmem + lane_base + q * kBK;
     const uint32_t t_o = tmem + lane_base + 256 + q * kD;
     const uint32_t t_p = tmem + lane_base + 384 + q * 64;
-    float m_run = -INFINITY, l_run = 0.f;
     const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
-    const int n = nj(q);
-    for (int i = 0; i < n; ++i) {
-      HP_TRACE(quarter == 0 && lane == 0, q, 4, i);
-      mbar_wait_park(&s_full[q], i & 1);
-      HP_TRACE(quarter == 0 && lane == 0, q, 5, i);
-      tc_fence_after();
-      uint32_t r[128];
-      tmem_ld_x32_at(t_s + 0, r, 0);
-      tmem_ld_x32_at(t_s + 32, r, 32);
-      tmem_ld_x32_at(t_s + 64, r, 64);
-      tmem_ld_x32_at(t_s + 96, r, 96);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[q]);           // the MMA warp may overwrite S now
-      HP_TRACE(quarter == 0 && lane == 0, q, 6, i);
-      if (MASK) {
-        const int valid = min(kBK, p.skv - (jb(q) + i) * kBK);
-        if (valid < kBK) {
-#pragma unroll
-          for (int e = 0; e < 128; ++e)
-            if (e >= valid) r[e] = __float_as_uint(-INFINITY);
-        }
-      }
-      // row max: 8 independent chains (FMNMX3 pairs), then a small tree
-      float mx[8];
-#pragma unroll
-      for (int a = 0; a < 8; ++a) mx[a] = __uint_as_float(r[a]);
-#pragma unroll
-      for (int e = 8; e < 128; e += 8) {
-#pragma unroll
-        for (int a = 0; a < 8; ++a) mx[a] = fmaxf(mx[a], __uint_as_float(r[e + a]));
-      }
-      const float m_blk = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * p.scale_log2;
-      // lazy rescale: move the reference max only when it grows by > 2^8
-      const bool grow = (i == 0) || (m_blk > m_run + kRescaleThreshold);
-      const float m_new = grow ? fmaxf(m_run, m_blk) : m_run;
-      const float alpha = grow ? ex2f(m_run - m_new) : 1.0f;     // i == 0: 2^-inf = 0
-      const uint64_t negm2 = pack2(-m_new, -m_new);
-      uint64_t sum2[4] = {0ull, 0ull, 0ull, 0ull};
-      uint32_t packed[64];
-#pragma unroll
-      for (int e = 0; e < 128; e += 2) {
-        const uint64_t x2 = ffma2(pack2u(r[e], r[e + 1]), scale2, negm2);
-        uint64_t e2;
-        const int pr = (e >> 1) & 7;
-        if (pr == 3 || pr == 7) e2 = exp2_poly2(x2);   // 2 of 8 pairs on the FMA pipe
-        else e2 = pack2(ex2f(lo2(x2)), ex2f(hi2(x2)));
-        sum2[(e >> 1) & 3] = fadd2(sum2[(e >> 1) & 3], e2);
-        packed[e >> 1] = pack_bf16(lo2(e2), hi2(e2));
-      }
-      HP_TRACE(quarter == 0 && lane == 0, q, 7, i);
-      const uint64_t s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
-      l_run = l_run * alpha + (lo2(s01) + hi2(s01));
-      m_run = m_new;
-      if (i > 0) {
-        // PV(i-1) must be complete before O is rescaled or P is overwritten
-        mbar_wait_park(&o_done[q], (i - 1) & 1);
-        HP_TRACE(quarter == 0 && lane == 0, q, 8, i);
+    int g = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const int h = unit_h(u), b = unit_b(u), q0 = unit_q0(u);
+      float m_run = -INFINITY, l_run = 0.f;
+      const int n = nj(q);
+      for (int i = 0; i < n; ++i, ++g) {
+        HP_TRACE(quarter == 0 && lane == 0, q, 4, g);
+        mbar_wait(&s_full[q], g & 1);
+        HP_TRACE(quarter == 0 && lane == 0, q, 5, g);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, grow)) {
-          uint32_t o[32];
+        uint32_t r[128];
+        tmem_ld_x32_at(t_s + 0, r, 0);
+        tmem_ld_x32_at(t_s + 32, r, 32);
+        tmem_ld_x32_at(t_s + 64, r, 64);
+        tmem_ld_x32_at(t_s + 96, r, 96);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[q]);           // the S issuer may overwrite S now
+        HP_TRACE(quarter == 0 && lane == 0, q, 6, g);
+        if (MASK) {
+          const int valid = min(kBK, p.skv - (jb(q) + i) * kBK);
+          if (valid < kBK) {
 #pragma unroll
-          for (int c = 0; c < kD / 32; ++c) {
-            tmem_ld_32x32b_x32(t_o + c * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st_32x32b_x32(t_o + c * 32, o);
+            for (int e = 0; e < 128; ++e)
+              if (e >= valid) r[e] = __float_as_uint(-INFINITY);
           }
         }
+        // row max: 8 independent chains (FMNMX3 pairs), then a small tree
+        float mx[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) mx[a] = __uint_as_float(r[a]);
+#pragma unroll
+        for (int e = 8; e < 128; e += 8) {
+#pragma unroll
+          for (int a = 0; a < 8; ++a) mx[a] = fmaxf(mx[a], __uint_as_float(r[e + a]));
+        }
+        const float m_blk = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                  fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * p.scale_log2;
+        // lazy rescale: move the reference max only when it grows by > 2^8
+        const bool grow = (i == 0) || (m_blk > m_run + kRescaleThreshold);
+        const float m_new = grow ? fmaxf(m_run, m_blk) : m_run;
+        const float alpha = grow ? ex2f(m_run - m_new) : 1.0f;     // i == 0: 2^-inf = 0
+        const uint64_t negm2 = pack2(-m_new, -m_new);
+        uint64_t sum2[4] = {0ull, 0ull, 0ull, 0ull};
+        uint32_t packed[64];
+#pragma unroll
+        for (int e = 0; e < 128; e += 2) {
+          const uint64_t x2 = ffma2(pack2u(r[e], r[e + 1]), scale2, negm2);
+          uint64_t e2;
+          const int pr = (e >> 1) & 7;
+          if (pr == 3 || pr == 7) e2 = exp2_poly2(x2);   // 2 of 8 pairs on the FMA pipe
+          else e2 = pack2(ex2f(lo2(x2)), ex2f(hi2(x2)));
+          sum2[(e >> 1) & 3] = fadd2(sum2[(e >> 1) & 3], e2);
+          packed[e >> 1] = pack_bf16(lo2(e2), hi2(e2));
+        }
+        HP_TRACE(quarter == 0 && lane == 0, q, 7, g);
+        const uint64_t s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
+        l_run = l_run * alpha + (lo2(s01) + hi2(s01));
+        m_run = m_new;
+        if (i > 0) {
+          // PV(g-1) must be complete before O is rescaled or P is overwritten (for
+          // i == 0 the previous unit's epilogue already waited for its last PV)
+          mbar_wait(&o_done[q], (g - 1) & 1);
+          HP_TRACE(quarter == 0 && lane == 0, q, 8, g);
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, grow)) {
+            uint32_t o[32];
+#pragma unroll
+            for (int c = 0; c < kD / 32; ++c) {
+              tmem_ld_32x32b_x32(t_o + c * 32, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+              tmem_st_32x32b_x32(t_o + c * 32, o);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[e] = packed[c * 16 + e];
+          tmem_st_32x32b_x16(t_p + c * 16, pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[q]);
+        HP_TRACE(quarter == 0 && lane == 0, q, 9, g);
       }
+      // ---- epilogue of this unit: O / l -> bf16 rows ----
+      mbar_wait(&o_done[q], (g - 1) & 1);
+      tc_fence_after();
+      if constexpr (!SPLIT) {
+        const int qrow = q0 + q * kBQ + row;
+        const float inv = 1.0f / l_run;
+        uint32_t o[32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
+        for (int c = 0; c < kD / 32; ++c) {
+          tmem_ld_32x32b_x32(t_o + c * 32, o);
+          tmem_ld_wait();
+          if (qrow < p.sq) {
+            __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + c * 32;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) pk[e] = packed[c * 16 + e];
-        tmem_st_32x32b_x16(t_p + c * 16, pk);
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[q]);
-      HP_TRACE(quarter == 0 && lane == 0, q, 9, i);
-    }
-    mbar_wait_park(&o_done[q], (n - 1) & 1);
-    tc_fence_after();
-    if constexpr (!SPLIT) {
-      const int qrow = q0 + q * kBQ + row;
-      const float inv = 1.0f / l_run;
-      uint32_t o[32];
-#pragma unroll
-      for (int c = 0; c < kD / 32; ++c) {
-        tmem_ld_32x32b_x32(t_o + c * 32, o);
+            for (int qq = 0; qq < 4; ++qq) {
+              uint4 w = make_uint4(pack_bf16(__uint_as_float(o[8 * qq]) * inv, __uint_as_float(o[8 * qq + 1]) * inv),
+                                   pack_bf16(__uint_as_float(o[8 * qq + 2]) * inv, __uint_as_float(o[8 * qq + 3]) * inv),
+                                   pack_bf16(__uint_as_float(o[8 * qq + 4]) * inv, __uint_as_float(o[8 * qq + 5]) * inv),
+                                   pack_bf16(__uint_as_float(o[8 * qq + 6]) * inv, __uint_as_float(o[8 * qq + 7]) * inv));
+              reinterpret_cast<uint4*>(dst)[qq] = w;
+            }
+          }
+        }
+      } else {
+        // merge the two halves: warpgroup q writes output columns [32q, 32q + 32) of
+        // its rows from both streams' O, so both warpgroups meet before (statistics
+        // exchange) and after (neither O may be overwritten while the other reads it)
+        s_ml[(q * 2 + 0) * kBQ + row] = m_run;
+        s_ml[(q * 2 + 1) * kBQ + row] = l_run;
+        tc_fence_before();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        tc_fence_after();
+        const float m0 = s_ml[0 * kBQ + row], l0 = s_ml[1 * kBQ + row];
+        const float m1 = s_ml[2 * kBQ + row], l1 = s_ml[3 * kBQ + row];
+        const float m = fmaxf(m0, m1);
+        const float a0 = ex2f(m0 - m), a1 = ex2f(m1 - m);
+        const float inv = 1.0f / (a0 * l0 + a1 * l1);
+        const float w0 = a0 * inv, w1 = a1 * inv;
+        const int qrow = q0 + row;
+        uint32_t o0[32], o1[32];
+        tmem_ld_32x32b_x32(tmem + lane_base + 256 + q * 32, o0);
+        tmem_ld_32x32b_x32(tmem + lane_base + 256 + kD + q * 32, o1);
         tmem_ld_wait();
+        tc_fence_before();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         if (qrow < p.sq) {
-          __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + c * 32;
+          __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + q * 32;
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {
-            uint4 u = make_uint4(pack_bf16(__uint_as_float(o[8 * qq]) * inv, __uint_as_float(o[8 * qq + 1]) * inv),
-                                 pack_bf16(__uint_as_float(o[8 * qq + 2]) * inv, __uint_as_float(o[8 * qq + 3]) * inv),
-                                 pack_bf16(__uint_as_float(o[8 * qq + 4]) * inv, __uint_as_float(o[8 * qq + 5]) * inv),
-                                 pack_bf16(__uint_as_float(o[8 * qq + 6]) * inv, __uint_as_float(o[8 * qq + 7]) * inv));
-            reinterpret_cast<uint4*>(dst)[qq] = u;
+            float v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              v[e] = fmaf(__uint_as_float(o0[8 * qq + e]), w0, __uint_as_float(o1[8 * qq + e]) * w1);
+            reinterpret_cast<uint4*>(dst)[qq] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
+                                                           pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
           }
-        }
-      }
-    } else {
-      // merge the two halves: both warpgroups reach every O column of their rows
-      s_ml[(q * 2 + 0) * kBQ + row] = m_run;
-      s_ml[(q * 2 + 1) * kBQ + row] = l_run;
-      tc_fence_before();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      tc_fence_after();
-      const float m0 = s_ml[0 * kBQ + row], l0 = s_ml[1 * kBQ + row];
-      const float m1 = s_ml[2 * kBQ + row], l1 = s_ml[3 * kBQ + row];
-      const float m = fmaxf(m0, m1);
-      const float a0 = ex2f(m0 - m), a1 = ex2f(m1 - m);
-      const float inv = 1.0f / (a0 * l0 + a1 * l1);
-      const float w0 = a0 * inv, w1 = a1 * inv;
-      const int qrow = q0 + row;
-      // warpgroup q writes output columns [32q, 32q + 32)
-      uint32_t o0[32], o1[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + q * 32, o0);
-      tmem_ld_32x32b_x32(tmem + lane_base + 256 + kD + q * 32, o1);
-      tmem_ld_wait();
-      if (qrow < p.sq) {
-        __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + q * 32;
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          float v[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            v[e] = fmaf(__uint_as_float(o0[8 * qq + e]), w0, __uint_as_float(o1[8 * qq + e]) * w1);
-          reinterpret_cast<uint4*>(dst)[qq] = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]),
-                                                         pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
         }
       }
     }
@@ -714,7 +747,7 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
       !map3(&tv, d->v, d->ldv, d->skv, d->batch))
     return HP_ERR_CUDA;
   AttnParams p{};
-  p.sq = d->sq; p.skv = d->skv; p.heads = d->heads;
+  p.sq = d->sq; p.skv = d->skv; p.heads = d->heads; p.batch = d->batch;
   p.causal = d->causal ? 1 : 0;
   if (p.causal && d->skv > kBK) return HP_ERR_UNSUPPORTED;    // single key block only (text encoders)
   p.q_col0 = (int)d->q_col0; p.k_col0 = (int)d->k_col0; p.v_col0 = (int)d->v_col0;
@@ -725,15 +758,16 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (p.n_kv == 1) return launch_single(grid, st, tq, tk, tv, p);
   const bool mask = (d->skv % kBK) != 0;
-  // one query tile per CTA (split-KV) when the two-tile grid would leave a short last wave
-  const int pair_ctas = grid.x * grid.y * grid.z;
+  // persistent CTAs over work units; split-KV units (one query tile, half the keys per
+  // stream) when the two-tile units would leave a short last round on the SMs
+  const int pair_units = grid.x * grid.y * grid.z;
   const int sms = num_sms_attn();
-  const int tail = pair_ctas % sms;
+  const int tail = pair_units % sms;
   const int mode = attn_mode();
   const bool split = mode == 2 || (mode == 0 && tail != 0 && tail * 2 < sms);
-  if (split) {
-    dim3 g1((d->sq + kBQ - 1) / kBQ, d->heads, d->batch);
+  const int units = split ? (int)((d->sq + kBQ - 1) / kBQ) * d->heads * d->batch : pair_units;
+  const dim3 g1(units < sms ? units : sms);
+  if (split)
     return mask ? launch_stream<true, true>(g1, st, tq, tk, tv, p) : launch_stream<true, false>(g1, st, tq, tk, tv, p);
-  }
-  return mask ? launch_stream<false, true>(grid, st, tq, tk, tv, p) : launch_stream<false, false>(grid, st, tq, tk, tv, p);
+  return mask ? launch_stream<false, true>(g1, st, tq, tk, tv, p) : launch_stream<false, false>(g1, st, tq, tk, tv, p);
 }

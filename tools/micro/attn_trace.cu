@@ -30,7 +30,7 @@ int main(int argc, char** argv) {
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   const char* names[12] = {"kv", "sfree_ok", "S_iss", "p_ok", "sm_wait", "s_ok", "sfree", "exp", "o_ok", "p_full",
                            "", ""};
-  const long long t0 = t[0][0][0];
+  const long long t0 = t[0][0][0];  // CTA 0, stream 0, first block
   const int J = (S + 127) / 128;
   for (int q = 0; q < 2; ++q) {
     printf("stream %d\n  i ", q);
