@@ -48,6 +48,38 @@ UNIT = "s/image"
 STEPS_T = 50
 
 
+class Workload:
+    """One BASELINE.json config as a bench workload (``--spec``): the network spec,
+    steps, builders and analytic FLOPs."""
+
+    def __init__(self, key):
+        from paper_2602_21760_b200 import pipelines
+        from paper_2602_21760_b200.denoiser import weights as Wm
+        self.key = key
+        self.dit = key == "sd3"
+        self.spec = {"sdxl": Wm.SDXL, "sdxl2048": Wm.SDXL_2048, "tiny": Wm.TINY, "sd3": Wm.SD3}[key]
+        self.T = {"sdxl": 50, "sdxl2048": 50, "tiny": 20, "sd3": 28}[key]
+        self.build = pipelines.build_sd3_denoiser if self.dit else pipelines.build_sdxl_denoiser
+        self.plan = pipelines.sd3_plan if self.dit else pipelines.sdxl_plan
+        px = {"sdxl": "1024^2", "sdxl2048": "2048^2", "tiny": "tiny 64x64-latent", "sd3": "1024^2"}[key]
+        net = "SD3" if self.dit else "SDXL"
+        self.metric = METRIC if key == "sdxl" else f"{net} {px} {self.T}-step latency (s/image)"
+        self.name = {"sdxl": "sdxl-1024-50step-cfg", "sdxl2048": "sdxl-2048-50step-cfg", "tiny": "tiny-unet-20step-cfg",
+                     "sd3": "sd3-1024-28step-fm-euler-cfg"}[key]
+        self.sampler = "flow-matching Euler" if self.dit else "DDIM"
+
+    def flops(self, n):
+        if self.dit:
+            from paper_2602_21760_b200.denoiser.mmdit import mmdit_flops
+            return mmdit_flops(self.spec, n)
+        from paper_2602_21760_b200.denoiser.unet import unet_flops
+        return unet_flops(self.spec, n)
+
+    @property
+    def latent(self):
+        return [self.spec.latent_hw, self.spec.latent_hw, self.spec.in_channels]
+
+
 def _forward_traffic():
     """DRAM bytes of one forward from the committed ncu launch list (profiles/):
     dram__bytes_read.sum + dram__bytes_write.sum summed over the forward's kernels."""
@@ -136,62 +168,73 @@ def _max_over_ranks(ws, v):
 
 
 # --------------------------------------------------------------------------------
-def cpu_reference_sample(spec, n_steps: int = 2, threads: int | None = None, weights=None):
+def cpu_reference_sample(wl, n_steps: int = 2, threads: int | None = None, weights=None):
     """Oracle CPU path on this host, timed over ``n_steps`` whole denoising steps of the
     reference's serial runner (engine.py:195-214 with config.py:174 rho=2): per step the
-    fp32 torch U-Net evaluates the conditional and then the unconditional branch (B=1
-    each, sequentially) and the numpy fp64 trio (rel_mae, cfg, ddim) updates the latent.
-    Returns (s/image = 50 x the measured mean step, details)."""
+    fp32 torch network (U-Net or MMDiT restatement) evaluates the conditional and then
+    the unconditional branch (B=1 each, sequentially) and the numpy fp64 trio (rel_mae,
+    cfg, ddim / fm-euler) updates the latent. Returns (s/image = T x the measured mean
+    step, details)."""
     import torch
     from oracle import sampler as osmp
-    from oracle.unet_ref import UNetRef
-    from paper_2602_21760_b200.denoiser.weights import init_weights, synthetic_conditioning, unet_param_specs
+    from paper_2602_21760_b200.denoiser.weights import (init_weights, mmdit_param_specs, synthetic_conditioning,
+                                                         unet_param_specs)
+    spec, T = wl.spec, wl.T
     threads = threads or os.cpu_count() or 1
     torch.set_num_threads(threads)
     t0 = time.perf_counter()
     if weights is None:
         dev = "cuda" if torch.cuda.is_available() else "cpu"
-        weights = {k: v.cpu() for k, v in init_weights(unet_param_specs(spec), seed=0, device=dev).items()}
+        specs = mmdit_param_specs(spec) if wl.dit else unet_param_specs(spec)
+        weights = {k: v.cpu() for k, v in init_weights(specs, seed=0, device=dev).items()}
     init_s = time.perf_counter() - t0
-    net = UNetRef(spec, weights)
-    cond = synthetic_conditioning(1, spec.context_len, spec.cross_dim, spec.pooled_dim)
-    hw = spec.latent_hw
-    _, _, abar, sig = osmp.schedule_tables("scaled-linear", STEPS_T, 0.00085, 0.012)
+    hw, c = spec.latent_hw, spec.in_channels
+    if wl.dit:
+        from oracle.mmdit_ref import MMDiTRef
+        net = MMDiTRef(spec, weights)
+        cond = synthetic_conditioning(1, spec.ctx_len, spec.ctx_dim, spec.pooled_dim)
+        fwd_in = lambda xn, tt, ctx, pool: net(xn.reshape(1, hw, hw, c), tt, ctx, pool)  # noqa: E731
+    else:
+        from oracle.unet_ref import UNetRef
+        net = UNetRef(spec, weights)
+        cond = synthetic_conditioning(1, spec.context_len, spec.cross_dim, spec.pooled_dim)
+        fwd_in = lambda xn, tt, ctx, pool: net(xn.reshape(1, c, hw, hw), tt, ctx, pool)  # noqa: E731
+    _, _, abar, sig = osmp.schedule_tables("scaled-linear", T, 0.00085, 0.012)
     g = torch.Generator().manual_seed(0)
-    x = torch.randn(1, spec.in_channels, hw, hw, generator=g).double().numpy().reshape(1, -1)
+    x = torch.randn(1, hw * hw * c, generator=g).double().numpy()
     steps, fwd = [], []
     with torch.no_grad():
         for i in range(n_steps):
-            t = STEPS_T - i
+            t = T - i
             t1 = time.perf_counter()
-            xt = torch.from_numpy(x.reshape(1, spec.in_channels, hw, hw)).float()
-            tt = torch.tensor([float(t * (1000 // STEPS_T))])
-            ec = net(xt, tt, cond.context, cond.pooled).double().numpy().reshape(1, -1)
+            xt = torch.from_numpy(x).float()
+            tt = torch.tensor([float(t * (1000 // T))])
+            ec = fwd_in(xt, tt, cond.context, cond.pooled).double().numpy().reshape(1, -1)
             t2 = time.perf_counter()
-            eu = net(xt, tt, cond.null_context, cond.null_pooled).double().numpy().reshape(1, -1)
+            eu = fwd_in(xt, tt, cond.null_context, cond.null_pooled).double().numpy().reshape(1, -1)
             fwd.append(time.perf_counter() - t2)
             fwd.append(t2 - t1)
             m = osmp.rel_mae(ec, eu)
-            x = osmp.ddim(x, osmp.cfg(ec, eu, 5.0), t, abar, sig)
+            e = osmp.cfg(ec, eu, 5.0)
+            x = osmp.euler(x, e, 1.0 / T) if wl.dit else osmp.ddim(x, e, t, abar, sig)
             steps.append(time.perf_counter() - t1)
     step = sum(steps) / len(steps)
-    return STEPS_T * step, {"step_s": step, "forward_s": min(fwd), "steps_measured": n_steps, "threads": threads,
-                            "weight_init_s": init_s, "m": float(np.asarray(m).ravel()[0])}
+    return T * step, {"step_s": step, "forward_s": min(fwd), "steps_measured": n_steps, "threads": threads,
+                      "weight_init_s": init_s, "m": float(np.asarray(m).ravel()[0])}
 
 
 def run_reference_arm(args):
     ws, rank, local = _dist()
     if rank != 0:
         return 0
-    from paper_2602_21760_b200.denoiser.weights import SDXL
     import torch
-    weights = None
+    wl = Workload("sdxl")
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     from paper_2602_21760_b200.denoiser.weights import init_weights, unet_param_specs
-    weights = {k: v.cpu() for k, v in init_weights(unet_param_specs(SDXL), seed=0, device=dev).items()}
+    weights = {k: v.cpu() for k, v in init_weights(unet_param_specs(wl.spec), seed=0, device=dev).items()}
     vals = []
     for i in range(args.warmup + args.steps):
-        v, det = cpu_reference_sample(SDXL, 1, weights=weights)
+        v, det = cpu_reference_sample(wl, 1, weights=weights)
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -266,25 +309,25 @@ def _graph_time(run, reps):
     return a.elapsed_time(b) / 1e3 / reps
 
 
-def forward_roofline(den, spec, reps=20):
-    """Back-to-back replays of the B=2 (both branches) forward graph."""
+def forward_roofline(den, wl, reps=20):
+    """Back-to-back replays of the CFG-batched (both branches, all prompts) forward graph."""
     import torch
-    from paper_2602_21760_b200.denoiser.unet import unet_flops
-    x = torch.randn(1, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
+    spec = wl.spec
+    x = torch.randn(den.B, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
     den.load_input(x)
-    t = _graph_time(lambda: den.branches(x, 30, den.input_slot()), reps)
-    return t, unet_flops(spec, 2)
+    t = _graph_time(lambda: den.branches(x, min(wl.T - 1, 30), den.input_slot()), reps)
+    return t, wl.flops(2 * den.B)
 
 
-def forward_b1(den, spec, reps=20):
+def forward_b1(den, wl, reps=20):
     """Back-to-back replays of the B=1 conditional-branch forward graph: the work one GPU
     of a condition-partitioned pair does per step, and half of the reference serial
     runner's rho=2 step (engine.py:195-214, config.py:174: branches evaluated in turn)."""
     import torch
-    from paper_2602_21760_b200.denoiser.unet import unet_flops
-    x = torch.randn(1, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
-    t = _graph_time(lambda: den.conditional(x, 30), reps)
-    return t, unet_flops(spec, 1)
+    spec = wl.spec
+    x = torch.randn(den.B, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
+    t = _graph_time(lambda: den.conditional(x, min(wl.T - 1, 30)), reps)
+    return t, wl.flops(den.B)
 
 
 def top_kernel_rooflines(bf16_peak, reps=20):
@@ -336,13 +379,14 @@ def top_kernel_rooflines(bf16_peak, reps=20):
     return out
 
 
-def time_replicas(args, spec, ws, rank, local):
-    """Every GPU generates its own images with the serial (CFG-batched) plan."""
+def time_replicas(args, wl, ws, rank, local):
+    """Every GPU generates its own images (``--prompts`` per run, one CFG batch) with
+    the serial plan."""
     import torch
     import paper_2602_21760_b200 as hp
-    from paper_2602_21760_b200 import pipelines
-    den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=STEPS_T, seed=rank)
-    plan = pipelines.sdxl_plan(spec, variant="serial", steps=STEPS_T, seed=rank, denoiser=den, clock="device")
+    den = wl.build(wl.spec, n_prompts=args.prompts, steps=wl.T, seed=rank)
+    plan = wl.plan(wl.spec, variant="serial", steps=wl.T, n_prompts=args.prompts, seed=rank, denoiser=den,
+                   clock="device")
     for _ in range(args.warmup):
         hp.run_plan(plan)
     torch.cuda.synchronize()
@@ -373,10 +417,10 @@ def time_replicas(args, spec, ws, rank, local):
     e2e_s = _max_over_ranks(ws, a2.elapsed_time(b2) / 1e3)
     h2d = int(x_host.nbytes)
     d2h = int(last.x0.nbytes) + 16 * len(last.series)
-    return den, dev_s, args.steps * ws, e2e_s, h2d, d2h, clocks, 1
+    return den, dev_s, args.steps * ws * args.prompts, e2e_s, h2d, d2h, clocks, 1
 
 
-def time_pairs(args, spec, ws, rank, local):
+def time_pairs(args, wl, ws, rank, local):
     """Condition-partitioned pairs over NVLink: ranks (2p, 2p+1) generate one image
     together with the hybrid plan (cond / uncond branch per GPU, fused exchange)."""
     import torch
@@ -387,9 +431,9 @@ def time_pairs(args, spec, ws, rank, local):
         raise RuntimeError(f"pairs mode needs an even GPU count, got {ws}")
     groups = [dist.new_group([2 * p, 2 * p + 1]) for p in range(ws // 2)]
     role = parallel.pair_role(rank)
-    den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=STEPS_T, seed=0)   # same weights in a pair
-    plan = pipelines.sdxl_plan(spec, variant="hybrid", steps=STEPS_T, seed=role.pair, denoiser=den,
-                               clock="device")
+    den = wl.build(wl.spec, n_prompts=args.prompts, steps=wl.T, seed=0)   # same weights in a pair
+    plan = wl.plan(wl.spec, variant="hybrid", steps=wl.T, n_prompts=args.prompts, seed=role.pair, denoiser=den,
+                   clock="device")
     sess = parallel.GroupSession(plan, groups[role.pair])
     for _ in range(args.warmup):
         sess.run()
@@ -420,7 +464,7 @@ def time_pairs(args, spec, ws, rank, local):
     e2e_s = _max_over_ranks(ws, a2.elapsed_time(b2) / 1e3)
     h2d = int(x_host.nbytes)
     d2h = int(last.x0.nbytes) + 16 * len(last.series)
-    return den, dev_s, args.steps * (ws // 2), e2e_s, h2d, d2h, clocks, 1
+    return den, dev_s, args.steps * (ws // 2) * args.prompts, e2e_s, h2d, d2h, clocks, 1
 
 
 def main():
@@ -430,7 +474,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="pairs", choices=["replicas", "pairs"])
-    ap.add_argument("--spec", default="sdxl", choices=["sdxl", "tiny"])
+    ap.add_argument("--spec", default="sdxl", choices=["sdxl", "sdxl2048", "sd3", "tiny"],
+                    help="BASELINE config: sdxl (config 2, the headline), sdxl2048 (config 4), sd3 (configs 3/5), "
+                         "tiny (config 1 network)")
+    ap.add_argument("--prompts", type=int, default=1, help="prompts (images) per generation (config 5: 8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -444,14 +491,14 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2602_21760_b200 as hp  # noqa: F401
-    from paper_2602_21760_b200.denoiser.weights import SDXL, TINY
-    spec = SDXL if args.spec == "sdxl" else TINY
+    wl = Workload(args.spec)
+    spec = wl.spec
     hbm_peak, bf16_burst, bf16_sus, peak_src = _peaks()
 
     mode = "single" if ws == 1 else args.mode
     err = None
     try:
-        res = time_pairs(args, spec, ws, rank, local) if mode == "pairs" else time_replicas(args, spec, ws, rank, local)
+        res = time_pairs(args, wl, ws, rank, local) if mode == "pairs" else time_replicas(args, wl, ws, rank, local)
     except Exception as exc:   # agreed across ranks below; never silently re-measured another way
         err = f"{mode} run failed on rank {rank}: {type(exc).__name__}: {exc}"
         res = None
@@ -463,20 +510,20 @@ def main():
             err = "another rank failed"
     if err:
         if rank == 0 or "rank" in err:
-            print(json.dumps({"metric": METRIC, "unit": UNIT, "n_gpus": ws, "error": err}), flush=True)
+            print(json.dumps({"metric": wl.metric, "unit": UNIT, "n_gpus": ws, "error": err}), flush=True)
         return 1
     den, dev_s, images, e2e_s, h2d, d2h, clocks, _ = res
     # latency per image: every step each group (pair / replica) generates one image
     # concurrently, so the per-image latency is the timed region over the K steps
-    value = dev_s / args.steps
-    e2e_value = e2e_s / args.steps
+    value = dev_s / args.steps / args.prompts
+    e2e_value = e2e_s / args.steps / args.prompts
 
-    fwd_s, fwd_flops = forward_roofline(den, spec) if mode != "pairs" else (None, None)
-    b1_s, b1_flops = forward_b1(den, spec)
+    fwd_s, fwd_flops = forward_roofline(den, wl) if mode != "pairs" else (None, None)
+    b1_s, b1_flops = forward_b1(den, wl)
     launches_fwd = (den.g_both.launches if mode != "pairs"
                     else max(den.g_cond.launches, getattr(getattr(den, "g_uncond", None), "launches", 0)))
     samp = sampler_roofline(hbm_peak) if rank == 0 else {}
-    top = top_kernel_rooflines(bf16_burst) if rank == 0 else []
+    top = top_kernel_rooflines(bf16_burst) if rank == 0 and wl.key == "sdxl" else []
 
     if rank != 0:
         if ws > 1:
@@ -487,34 +534,35 @@ def main():
     if mode != "pairs":
         # per GPU over the timed region itself: each rank ran K generations of 50 steps, each
         # step one B=2 forward (+ one sampler launch, counted in the time, not the FLOPs)
-        achieved = fwd_flops * STEPS_T * args.steps / dev_s / 1e12
+        achieved = fwd_flops * wl.T * args.steps / dev_s / 1e12
         achieved_src = "timed region: K x 50 denoiser forwards / CUDA-event time of the K generations"
-        roof_flops, roof_kernel = fwd_flops, "denoiser forward (tcgen05 GEMM/conv + attention), B=2 (both branches)"
+        roof_flops, roof_kernel = fwd_flops, (f"denoiser forward (tcgen05 GEMM/conv + attention), "
+                                              f"B={2 * args.prompts} (both branches)")
     else:
         achieved = b1_flops / b1_s / 1e12
         achieved_src = "isolated B=1 branch-forward graph replays (the per-GPU work of a pair)"
-        roof_flops, roof_kernel = b1_flops, "denoiser forward, B=1 (one branch per GPU)"
+        roof_flops, roof_kernel = b1_flops, f"denoiser forward, B={args.prompts} (one branch per GPU)"
     # what a condition-partitioned pair would take on this clock: one B=1 forward per GPU
     # per step + the eps exchange (bf16 latent over NVLink: bytes / 770 GB/s measured peer
     # copy + an assumed 5 us flag round trip) + the fused sampler kernel
     numel = spec.latent_hw * spec.latent_hw * spec.in_channels
-    xch_s = numel * 2 / 770e9 + 5e-6
-    pair_pred = STEPS_T * (b1_s + xch_s + k1_s)
-    seq_rho2 = STEPS_T * (2 * b1_s + k1_s)
+    xch_s = args.prompts * numel * 2 / 770e9 + 5e-6
+    pair_pred = wl.T * (b1_s + xch_s + k1_s) / args.prompts
+    seq_rho2 = wl.T * (2 * b1_s + k1_s) / args.prompts
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "metric": wl.metric, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{spec.name}-1024-50step-cfg" if spec.name == "sdxl" else f"{spec.name}-50step",
-                   "latent": [spec.latent_hw, spec.latent_hw, spec.in_channels], "T": STEPS_T,
-                   "guidance_w": 5.0, "images": images,
-                   "plan": ("hybrid on condition-partitioned pairs (L=12, g=4e-4, tau_cap=15, k=5)"
-                            if mode == "pairs" else "serial (CFG batched B=2)"),
+        "config": {"workload": wl.name, "latent": wl.latent, "T": wl.T, "sampler": wl.sampler,
+                   "guidance_w": 5.0, "images": images, "prompts_per_generation": args.prompts,
+                   "plan": ("hybrid on condition-partitioned pairs" if mode == "pairs"
+                            else f"serial (CFG batched B={2 * args.prompts})"),
                    "parallelism": f"{mode}x{ws}" if ws > 1 else "single",
-                   "params_b": 2.567 if spec.name == "sdxl" else None,
+                   "params_b": round(sum(p.numel() for p in den.net.W.values()) / 1e9, 3)
+                   if hasattr(den.net, "W") else None,
                    "l2": "working set (5.1 GB of bf16 weights per step) >> 126 MB L2"},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": int(args.steps * STEPS_T * (launches_fwd + 1)),
+        "gpu_launches": int(args.steps * wl.T * (launches_fwd + 1)),
         "roofline": {"bound": "tensor", "kernel": roof_kernel,
                      "achieved": achieved, "achieved_source": achieved_src,
                      "peak": bf16_sus, "unit": "TFLOP/s", "frac": achieved / bf16_sus,
@@ -536,11 +584,12 @@ def main():
     }
     if ws == 1 and not args.no_cpu_baseline:
         try:
-            v, det = cpu_reference_sample(spec, 2)
+            v, det = cpu_reference_sample(wl, 2)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": det["threads"], "kind": "port",
                                     "sample": f"{det['steps_measured']} whole denoising steps of the serial runner "
-                                              "(fp32 CPU U-Net, cond then uncond branch at B=1, numpy fp64 "
-                                              "rel_mae/cfg/ddim at the latent size), mean step x50",
+                                              f"(fp32 CPU {'MMDiT' if wl.dit else 'U-Net'}, cond then uncond branch "
+                                              f"at B=1, numpy fp64 rel_mae/cfg/{'euler' if wl.dit else 'ddim'} at "
+                                              f"the latent size), mean step x{wl.T} (one prompt)",
                                     "step_s": det["step_s"], "forward_s": det["forward_s"]}
         except Exception as exc:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",

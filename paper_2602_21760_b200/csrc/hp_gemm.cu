@@ -652,6 +652,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 // work: the 1-CTA kernel is L2-bandwidth-bound on B200 (LTS cap), this is not.
 //   warp 0  TMA producer (both CTAs)   warp 1  MMA issuer (leader CTA)
 //   warp 2  TMEM allocator (both)      warps 4..7  epilogue (both, own rows)
+#ifdef HP_GEMM_TRACE
+// event timeline of the pair kernel's cluster 0 (tools/micro/gemm_trace.cu): [event][rank]
+__device__ long long g_gemm_trace[16][2];
+#define HP_GTRACE(ev) do { if (blockIdx.x < 2) g_gemm_trace[ev][blockIdx.x] = clock64(); } while (0)
+#else
+#define HP_GTRACE(ev) do {} while (0)
+#endif
 constexpr int kEpRuntime = -1;   // epilogue flavour chosen per tile at run time (kAmAny instances)
 template <int BN, int STAGES, int AM, int EP>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -683,6 +690,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   float* scolsum = sbias + 2 * BN;                                               // [2][BN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) HP_GTRACE(0);
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
@@ -701,7 +709,9 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   cluster_barrier();                 // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) HP_GTRACE(1);
   pdl_wait();
+  if (threadIdx.x == 0) HP_GTRACE(2);
   pdl_trigger();
 
   auto decode = [&](int tile, int& bt, int& m0, int& n0) {
@@ -734,6 +744,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+          if (it == 0) HP_GTRACE(3);
           const uint32_t fb = mapa_shared(&full[s], 0);
           uint8_t* a_dst = smA + s * kABytes;
           if (p.mode == HP_A_PLAIN) {
@@ -776,6 +787,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&full[s], ph);
+          if (it == 0) HP_GTRACE(4);
           tc_fence_after();
           const uint64_t da = sdesc_sw128_kmajor(smA + s * kABytes);
 #pragma unroll
@@ -789,6 +801,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           umma_commit_pair(&empty[s], 0x3);
         }
         umma_commit_pair(&tfull[acc], 0x3);
+        if (local == 0) HP_GTRACE(5);
       }
     }
   } else if (warp >= 4) {
@@ -823,6 +836,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       if (fold && my_row < p.M) fold_row_stats(p, my_row, f_mean, f_rstd);
       prefetch_res_row<BN>(p, bt, my_row, n0);     // residual lines in flight while the MMAs finish
       mbar_wait(&tfull[acc], use & 1);
+      if (et == 0 && local == 0) HP_GTRACE(6);
       tc_fence_after();
       const uint32_t t_acc = tmem_base + acc * BN;
       if constexpr (EP != kEpRuntime) {            // one epilogue flavour compiled in
@@ -843,10 +857,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster_relaxed(mapa_shared(&tempty[acc], 0));   // the leader's TMEM-free barrier
+      if (et == 0 && local == 0) HP_GTRACE(7);
     }
   }
   tc_fence_before();
   cluster_barrier();                 // all MMAs consumed, both epilogues done
+  if (threadIdx.x == 0) HP_GTRACE(8);
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
 }

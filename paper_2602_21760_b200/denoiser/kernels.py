@@ -227,7 +227,7 @@ def attention(q, k, v, out, *, batch, heads, sq, skv, scale, q_col0=0, k_col0=0,
     d.o, d.ldo = _p(out), out.stride(0)
     d.batch, d.heads, d.sq, d.skv, d.scale = batch, heads, sq, skv, float(scale)
     d.causal = 1 if causal else 0
-    check(lib.hp_attention(C.byref(d), _s()), "hp_attention")
+    check(lib.hp_attention(C.byref(d), _s()), f"hp_attention B={batch} H={heads} Sq={sq} Skv={skv}")
     return out
 
 
@@ -240,7 +240,7 @@ def group_norm(x, n, hw, c, gamma, beta, *, groups=32, eps=1e-5, silu=False, x2=
     if stats is None:
         stats = torch.empty(2 * n * groups * 256, dtype=torch.float32, device=x.device)
     check(lib.hp_group_norm(_p(x), c, _p(x2), c2, n, hw, groups, eps, _p(gamma), _p(beta), int(silu),
-                            _p(out), _p(stats), _s()), "hp_group_norm")
+                            _p(out), _p(stats), _s()), f"hp_group_norm n={n} hw={hw} C={C_}")
     return out
 
 
@@ -394,14 +394,22 @@ def timestep_embedding(t, dim, max_period=10000.0):
     return out
 
 
+SMALL_MAX_M = 8      # csrc/hp_norm.cu kSmallMaxM
+
+
 def linear_small(x, w, bias=None, *, act_in=ACT_NONE, act_out=ACT_NONE, out=None):
     lib = N.load()
     M, K = x.shape
     Nn = w.shape[0]
     if out is None:
         out = torch.empty((M, Nn), dtype=torch.float32, device=x.device)
-    check(lib.hp_linear_small(_p(x), M, K, _p(w), _p(bias), Nn, act_in, act_out, _p(out), _s()),
-          "hp_linear_small")
+    # the kernel keeps up to SMALL_MAX_M input rows in shared memory; larger batches
+    # (e.g. 8 prompts x 2 CFG branches) run as row chunks (rows are independent)
+    for r0 in range(0, M, SMALL_MAX_M):
+        m = min(SMALL_MAX_M, M - r0)
+        xs, ys = x[r0:r0 + m], out[r0:r0 + m]
+        check(lib.hp_linear_small(_p(xs), m, K, _p(w), _p(bias), Nn, act_in, act_out, _p(ys), _s()),
+              "hp_linear_small")
     return out
 
 

@@ -248,6 +248,9 @@ def test_small_ops():
     bs = torch.randn(1280, device="cuda")
     ys = K.linear_small(xs, ws, bs, act_in=K.ACT_SILU)
     assert (ys - (F.silu(xs) @ ws.float().t() + bs)).abs().max().item() < 1e-3
+    xb = torch.randn(19, 320, device="cuda")               # > 8 rows: chunked (8 prompts x CFG)
+    yb = K.linear_small(xb, ws, bs, act_out=K.ACT_SILU)
+    assert (yb - F.silu(xb @ ws.float().t() + bs)).abs().max().item() < 1e-3
     lat = rnd(2, 8, 8, 16)
     tok = K.patchify(lat, 2, 8, 8, 16, 2)
     ref = lat.view(2, 4, 2, 4, 2, 16).permute(0, 1, 3, 2, 4, 5).reshape(-1)
