@@ -125,6 +125,13 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 // S_q, P_0 overwrites Q_0|Q_1 and P_1 overwrites K|X after both score MMAs, so the
 // CTA needs 256 TMEM columns and 97 KB of smem and two CTAs share an SM (one's
 // TMA -> MMA -> softmax -> PV -> store chain overlaps the other's).
+#ifdef HP_ATTN_TRACE
+__device__ long long g_single_trace[16];
+#define HP_STRACE(cond, ev) do { if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) \
+                                   g_single_trace[ev] = clock64(); } while (0)
+#else
+#define HP_STRACE(cond, ev) do {} while (0)
+#endif
 constexpr int kSingleThreads = 320;
 constexpr uint32_t kSingleCols = 256;
 constexpr size_t kSingleSmem = (size_t)kTileBytes * 5 + 256;
@@ -152,6 +159,7 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  HP_STRACE(threadIdx.x == 0, 0);
   const int h = blockIdx.y, b = blockIdx.z;
   const int q0 = blockIdx.x * 2 * kBQ;
 
@@ -168,6 +176,7 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
+  HP_STRACE(threadIdx.x == 0, 1);
   pdl_trigger();
 
   if (warp == kTmaWarp) {
@@ -183,6 +192,7 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     if (lane == 0) {
       mbar_wait(q_full, 0);
       mbar_wait(kv_full, 0);
+      HP_STRACE(true, 2);
       tc_fence_after();
       const uint64_t dk = sdesc_sw128_kmajor(sK);
       for (int q = 0; q < 2; ++q) {
@@ -191,6 +201,7 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem + q * kBK, dq + 2 * k, dk + 2 * k, kIdescS, k > 0 ? 1u : 0u);
         umma_commit(&s_full[q]);
       }
+      HP_STRACE(true, 3);
       for (int q = 0; q < 2; ++q) {
         mbar_wait(&p_full[q], 0);
         tc_fence_after();
@@ -213,6 +224,7 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t t_o = t_s;                 // O_q overwrites S_q
     const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
     mbar_wait(&s_full[q], 0);
+    HP_STRACE(threadIdx.x == 0, 4);
     tc_fence_after();
     // keys this row may see: the sequence end and, when causal, the row's own position
     const int valid = p.causal ? min(min(kBK, p.skv), q0 + q * kBQ + row + 1) : min(kBK, p.skv);
@@ -277,7 +289,9 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&p_full[q]);
+    HP_STRACE(threadIdx.x == 0, 5);
     mbar_wait(&o_done[q], 0);
+    HP_STRACE(threadIdx.x == 0, 6);
     tc_fence_after();
     const int qrow = q0 + q * kBQ + row;
     const float inv = 1.0f / l;
@@ -299,8 +313,10 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       }
     }
   }
+  HP_STRACE(threadIdx.x == 0, 7);
   tc_fence_before();
   __syncthreads();
+  HP_STRACE(threadIdx.x == 0, 8);
   tc_fence_after();
   if (warp == kMmaWarp) tmem_dealloc<kSingleCols>(tmem);
 }

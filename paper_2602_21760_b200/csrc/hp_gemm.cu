@@ -653,9 +653,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 //   warp 0  TMA producer (both CTAs)   warp 1  MMA issuer (leader CTA)
 //   warp 2  TMEM allocator (both)      warps 4..7  epilogue (both, own rows)
 #ifdef HP_GEMM_TRACE
-// event timeline of the pair kernel's cluster 0 (tools/micro/gemm_trace.cu): [event][rank]
-__device__ long long g_gemm_trace[16][2];
-#define HP_GTRACE(ev) do { if (blockIdx.x < 2) g_gemm_trace[ev][blockIdx.x] = clock64(); } while (0)
+// per-launch event ring of the pair kernel's first cluster (tools/gemm_ring.py): globaltimer
+// ns per event; [slot][0..8] events, [slot][9..12] M, N, K, block_n
+constexpr int kRing = 4096;
+__device__ unsigned long long g_gemm_ring[kRing][13];
+__device__ unsigned int g_gemm_ctr;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define HP_GTRACE(ev) do { if (blockIdx.x == 0 && g_slot >= 0) g_gemm_ring[g_slot % kRing][ev] = gtime(); } while (0)
 #else
 #define HP_GTRACE(ev) do {} while (0)
 #endif
@@ -690,6 +698,16 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   float* scolsum = sbias + 2 * BN;                                               // [2][BN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef HP_GEMM_TRACE
+  __shared__ int s_slot;
+  if (threadIdx.x == 0) s_slot = blockIdx.x == 0 ? (int)atomicAdd(&g_gemm_ctr, 1u) : -1;
+  __syncthreads();
+  const int g_slot = s_slot;
+  if (threadIdx.x == 0 && g_slot >= 0) {
+    g_gemm_ring[g_slot % kRing][9] = p.M; g_gemm_ring[g_slot % kRing][10] = p.N;
+    g_gemm_ring[g_slot % kRing][11] = p.K; g_gemm_ring[g_slot % kRing][12] = BN;
+  }
+#endif
   if (threadIdx.x == 0) HP_GTRACE(0);
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -710,8 +728,9 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) HP_GTRACE(1);
-  pdl_wait();
-  if (threadIdx.x == 0) HP_GTRACE(2);
+  // the TMA producer (warp 0, lane 0) waits for the previous kernel only after it has
+  // staged the weight (B) tiles of its first k-blocks: weights never depend on it
+  if (threadIdx.x != 0) pdl_wait();
   pdl_trigger();
 
   auto decode = [&](int tile, int& bt, int& m0, int& n0) {
@@ -726,6 +745,23 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------ TMA producer (both CTAs) ------------------------------
+      // B of the first tile's first k-blocks before the PDL wait (stage s = k-block s; the
+      // stage's expect_tx covers A and B, A follows once the previous kernel is done)
+      const int pre = cluster_id < num_tiles ? min(STAGES, p.num_kb) : 0;
+      if (pre > 0) {
+        int bt, m0, n0;
+        decode(cluster_id, bt, m0, n0);
+        const int nb = n0 + (int)rank * (kSubN / 2) + (p.mode == HP_A_UPCONV ? bt * p.N : 0);
+        for (int kb = 0; kb < pre; ++kb) {
+          if (leader) mbar_arrive_expect_tx(&full[kb], 2 * kStageBytes);
+          const uint32_t fb = mapa_shared(&full[kb], 0);
+#pragma unroll
+          for (int sub = 0; sub < kSub; ++sub)
+            tma_load_2d_pair(smB + kb * kBHalfBytes + sub * kSubBytes, &tmB, fb, kb * BK, nb + sub * kSubN);
+        }
+      }
+      pdl_wait();
+      HP_GTRACE(2);
       uint32_t it = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
         int bt, m0, n0;
@@ -742,8 +778,11 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+          const bool staged = (int)it < pre;         // B already in flight, expect_tx done
+          if (!staged) {
+            mbar_wait(&empty[s], ph ^ 1);
+            if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+          }
           if (it == 0) HP_GTRACE(3);
           const uint32_t fb = mapa_shared(&full[s], 0);
           uint8_t* a_dst = smA + s * kABytes;
@@ -767,9 +806,11 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
               tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, 2 * x0 + dx - 1, 2 * y0 + dy - 1, img);
             }
           }
+          if (!staged) {
 #pragma unroll
-          for (int sub = 0; sub < kSub; ++sub)
-            tma_load_2d_pair(smB + s * kBHalfBytes + sub * kSubBytes, &tmB, fb, kb * BK, nb + sub * kSubN);
+            for (int sub = 0; sub < kSub; ++sub)
+              tma_load_2d_pair(smB + s * kBHalfBytes + sub * kSubBytes, &tmB, fb, kb * BK, nb + sub * kSubN);
+          }
         }
       }
     }
@@ -920,7 +961,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   cluster_barrier();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();
+  if (threadIdx.x != 0) pdl_wait();          // the producer waits after staging its weights
   pdl_trigger();
 
   float f_mean = 0.f, f_rstd = 1.f;
@@ -935,12 +976,26 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         x0 = rem - y0 * p.out_w;
       }
       const uint32_t nb = n0 + pr * (kSubN / 2);
+      // weights of the first k-blocks before the PDL wait (they never depend on the
+      // previous kernel); A follows once it is done
+      const int pre = min(STAGES, kb_hi - kb_lo);
+      for (int i = 0; i < pre; ++i) {
+        if (leader) mbar_arrive_expect_tx(&full[i], 2 * kStageBytes);
+        const uint32_t fb = mapa_shared(&full[i], rank & ~1u);
+#pragma unroll
+        for (int sub = 0; sub < 2; ++sub)
+          tma_load_2d_pair(smB + i * kBHalfBytes + sub * kSubBytes, &tmB, fb, (kb_lo + i) * BK, nb + sub * kSubN);
+      }
+      pdl_wait();
       uint32_t it = 0;
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+        const bool staged = (int)it < pre;
+        if (!staged) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes);
+        }
         const uint32_t fb = mapa_shared(&full[s], rank & ~1u);
         uint8_t* a_dst = smA + s * kABytes;
         if (p.mode == HP_A_PLAIN) {
@@ -952,9 +1007,11 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           if (p.mode == HP_A_CONV3X3) tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, x0 + dx - 1, y0 + dy - 1, img);
           else tma_load_4d_pair(a_dst, &tmA, fb, cb * BK, 2 * x0 + dx - 1, 2 * y0 + dy - 1, img);
         }
+        if (!staged) {
 #pragma unroll
-        for (int sub = 0; sub < 2; ++sub)
-          tma_load_2d_pair(smB + s * kBHalfBytes + sub * kSubBytes, &tmB, fb, kb * BK, nb + sub * kSubN);
+          for (int sub = 0; sub < 2; ++sub)
+            tma_load_2d_pair(smB + s * kBHalfBytes + sub * kSubBytes, &tmB, fb, kb * BK, nb + sub * kSubN);
+        }
       }
     }
   } else if (warp == 1) {
@@ -1450,3 +1507,14 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
 }
 
 }  // extern "C"
+
+#ifdef HP_GEMM_TRACE
+#include <string.h>
+// trace builds only (tools/gemm_ring.py): copy the launch ring / counter to the host
+extern "C" int hp_debug_symbol(const char* name, void* dst, size_t bytes) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  if (!strcmp(name, "g_gemm_ring")) return cudaMemcpyFromSymbol(dst, g_gemm_ring, bytes) == cudaSuccess ? 0 : -1;
+  if (!strcmp(name, "g_gemm_ctr")) return cudaMemcpyFromSymbol(dst, g_gemm_ctr, bytes) == cudaSuccess ? 0 : -1;
+  return -2;
+}
+#endif

@@ -11,7 +11,8 @@
 
 int main(int argc, char** argv) {
   const int B = argc > 1 ? atoi(argv[1]) : 1, H = argc > 2 ? atoi(argv[2]) : 2, S = argc > 3 ? atoi(argv[3]) : 16384;
-  const size_t n = (size_t)B * S * H * 64;
+  const int SKV = argc > 4 ? atoi(argv[4]) : S;   // <= 128: the single-block kernel
+  const size_t n = (size_t)B * (S > SKV ? S : SKV) * H * 64;
   std::vector<__nv_bfloat16> h(n);
   for (size_t i = 0; i < n; ++i) h[i] = __float2bfloat16((float)((i * 2654435761u) % 2001) / 1000.f - 1.f);
   void *q, *k, *v, *o;
@@ -22,9 +23,30 @@ int main(int argc, char** argv) {
   hp_attn_desc d{};
   d.q = q; d.k = k; d.v = v; d.o = o;
   d.ldq = d.ldk = d.ldv = d.ldo = H * 64;
-  d.batch = B; d.heads = H; d.sq = S; d.skv = S; d.scale = 0.125f;
+  d.batch = B; d.heads = H; d.sq = S; d.skv = SKV; d.scale = 0.125f;
   for (int r = 0; r < 3; ++r) hp_attention(&d, nullptr);
   cudaDeviceSynchronize();
+  if (SKV <= 128) {
+    // graph of 20 launches: per-launch time and the last launch's CTA-0 timeline
+    cudaStream_t st; cudaStreamCreate(&st);
+    cudaGraph_t gr; cudaGraphExec_t ge;
+    cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+    for (int r = 0; r < 20; ++r) hp_attention(&d, st);
+    cudaStreamEndCapture(st, &gr);
+    cudaGraphInstantiate(&ge, gr, 0);
+    cudaGraphLaunch(ge, st); cudaStreamSynchronize(st);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0, st); cudaGraphLaunch(ge, st); cudaEventRecord(e1, st); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    long long st16[16];
+    cudaMemcpyFromSymbol(st16, g_single_trace, sizeof(st16));
+    const char* nm[9] = {"entry", "pdl passed", "Q,K,V landed", "S issued", "softmax got S", "P published",
+                         "O ready", "stored", "CTA done"};
+    printf("single-block B=%d H=%d Sq=%d Skv=%d: %.2f us per launch (graph); CTA 0:", B, H, S, SKV, ms * 1e3 / 20);
+    for (int e = 0; e < 9; ++e) printf(" %s %lld |", nm[e], st16[e] - st16[0]);
+    printf("\n");
+    return 0;
+  }
   static long long t[2][12][256];
   cudaMemcpyFromSymbol(t, g_attn_trace, sizeof(t));
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));

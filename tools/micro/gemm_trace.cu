@@ -1,4 +1,4 @@
-// Event timeline (clock64, cycles from kernel entry) of cluster 0 of the CTA-pair GEMM,
+// Event timeline (globaltimer ns from kernel entry) of cluster 0 of the CTA-pair GEMM,
 // built from the product kernel with HP_GEMM_TRACE: setup done (barriers, TMEM), PDL
 // wait passed, first TMA issued, first stage landed, first tile's MMAs issued,
 // accumulator ready in the epilogue, epilogue done, final cluster barrier.
@@ -32,16 +32,17 @@ int main(int argc, char** argv) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0, st); cudaGraphLaunch(ge, st); cudaEventRecord(e1, st); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
-  long long t[16][2];
-  cudaMemcpyFromSymbol(t, g_gemm_trace, sizeof(t));
+  static unsigned long long ring[kRing][13];
+  unsigned int ctr = 0;
+  cudaMemcpyFromSymbol(ring, g_gemm_ring, sizeof(ring));
+  cudaMemcpyFromSymbol(&ctr, g_gemm_ctr, sizeof(ctr));
+  const unsigned long long* last = ring[(ctr - 1) % kRing];
   printf("%s; %ldx%ldx%ld bn=%d: %.2f us per launch in the graph\n", cudaGetErrorString(cudaGetLastError()), M, N, K,
          bn, ms * 1e3 / 20);
   const char* nm[9] = {"entry", "setup done", "pdl wait passed", "first TMA issued", "first stage landed",
                        "tile 0 MMAs issued", "acc ready (epi)", "epilogue done", "final barrier"};
-  for (int r = 0; r < 2; ++r) {
-    printf("rank %d:", r);
-    for (int e = 0; e < 9; ++e) printf("  %s %lld", nm[e], t[e][r] ? t[e][r] - t[0][r] : -1);
-    printf("\n");
-  }
+  printf("last launch, cluster 0 leader (ns from entry):");
+  for (int e = 0; e < 9; ++e) printf("  %s %lld", nm[e], last[e] ? (long long)(last[e] - last[0]) : -1);
+  printf("\n");
   return 0;
 }
