@@ -322,6 +322,12 @@ __device__ __forceinline__ void image_barrier(unsigned* cnt, unsigned* gen, unsi
 // SMEM: the CTA first copies its pixel chunk of each input into shared memory with
 // bulk async copies (all of it in flight at once), reduces it from there and
 // normalises it from there (no second global read).
+#ifdef HP_GN_TRACE
+__device__ long long g_gn_trace[8];
+#define HP_NTRACE(ev) do { if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_gn_trace[ev] = clock64(); } while (0)
+#else
+#define HP_NTRACE(ev) do {} while (0)
+#endif
 template <bool SMEM>
 __global__ void __launch_bounds__(kGnThreads)
 gn_fused_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2, int c2, int64_t hw,
@@ -329,7 +335,9 @@ gn_fused_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
                 const float* __restrict__ beta, int do_silu, bf16* __restrict__ y, unsigned* __restrict__ bar) {
   extern __shared__ __align__(128) uint8_t gn_chunk[];
   __shared__ uint64_t ld_bar;
+  HP_NTRACE(0);
   pdl_wait();
+  HP_NTRACE(1);
   pdl_trigger();
   const int n = blockIdx.y, split = blockIdx.x;
   const int64_t p_begin = hw * split / splits, p_end = hw * (split + 1) / splits;
@@ -368,18 +376,22 @@ gn_fused_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
     }
     __syncthreads();
     mbar_wait(&ld_bar, 0);
+    HP_NTRACE(2);
     ch1 = d1;
     ch2 = g2 ? d2 : nullptr;
   }
   gn_stats_block(ch1, c1, ch2, c2, npx, groups, splits, part, n, split, sm, sm + cmax, sm + 2 * cmax,
                  sm + 2 * cmax + kGnThreads * 8);
   __syncthreads();
+  HP_NTRACE(3);
   if (threadIdx.x == 0) image_barrier(bar + 2 * n, bar + 2 * n + 1, (unsigned)splits);
   __syncthreads();
+  HP_NTRACE(4);
   double* dp = reinterpret_cast<double*>(sm + 2 * cmax);               // [2][kGnThreads] doubles
   float* s_mean = sm + 2 * cmax + 4 * kGnThreads;
   gn_apply_block(ch1, c1, ch2, c2, hw, groups, splits, part, eps, gamma, beta, do_silu, y + (int64_t)n * hw * (c1 + c2),
                  n, p_begin, p_begin, 1, p_end, s_mean, s_mean + 64, dp, dp + kGnThreads, sm, sm + cmax);
+  HP_NTRACE(5);
 }
 
 // ---------------------------------------------------------------------------
