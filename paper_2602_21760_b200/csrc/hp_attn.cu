@@ -774,13 +774,16 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (p.n_kv == 1) return launch_single(grid, st, tq, tk, tv, p);
   const bool mask = (d->skv % kBK) != 0;
-  // persistent CTAs over work units; split-KV units (one query tile, half the keys per
-  // stream) when the two-tile units would leave a short last round on the SMs
+  // persistent CTAs over work units. The unit kind depends on the key count only, never
+  // on batch or heads, so an image's rows are computed the same way whatever else is in
+  // the batch (the condition-partitioned B=1 forwards equal the CFG-batched B=2 one):
+  // split-KV units (one query tile, half the keys per stream, merged in the CTA) up to
+  // 32 key blocks, where the finer units balance the SMs better (S=1024 / 4096), two-tile
+  // units with shared K/V beyond (SD3's S=4429, S=16384), where K/V sharing wins.
   const int pair_units = grid.x * grid.y * grid.z;
   const int sms = num_sms_attn();
-  const int tail = pair_units % sms;
   const int mode = attn_mode();
-  const bool split = mode == 2 || (mode == 0 && tail != 0 && tail * 2 < sms);
+  const bool split = mode == 2 || (mode == 0 && p.n_kv <= 32);
   const int units = split ? (int)((d->sq + kBQ - 1) / kBQ) * d->heads * d->batch : pair_units;
   const dim3 g1(units < sms ? units : sms);
   if (split)

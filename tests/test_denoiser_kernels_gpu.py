@@ -89,19 +89,33 @@ def test_conv3x3_implicit_gemm(n, h, w, c, co, stride):
 
 
 # dispatch (csrc/hp_attn.cu hp_attention): one key block -> single-block CTAs;
-# else two-query-tile CTAs ("pair") unless that grid leaves a short last wave
-# (tail*2 < 148 SMs) -> split-KV CTAs. Each path with and without the
-# partial-key-block mask (S_kv % 128 != 0):
+# up to 32 key blocks -> persistent split-KV units; beyond -> persistent two-tile
+# units sharing K/V. Each path with and without the partial-key-block mask
+# (S_kv % 128 != 0):
 ATTN_SHAPES = [
     (1, 1, 128, 128), (2, 4, 256, 77),                    # single block
     (2, 3, 256, 256), (1, 2, 1024, 1024),                 # split-KV, unmasked
     (2, 2, 333, 333), (2, 1, 130, 500),                   # split-KV, masked
     (2, 10, 4096, 4096), (2, 20, 1024, 1024),             # split-KV at the SDXL-1024 shapes (B=2)
-    (1, 37, 1024, 1024), (1, 20, 1024, 1024),             # pair, unmasked (grid 148: no tail / tail 80)
-    (2, 24, 4429, 4429),                                  # pair, masked: SD3-1024 joint attention
+    (1, 37, 1024, 1024), (1, 20, 1024, 1024),             # split-KV, B=1 (one branch per GPU)
+    (2, 24, 4429, 4429),                                  # two-tile, masked: SD3-1024 joint attention
     (1, 24, 4429, 4429),                                  # SD3 at B=1 (one branch per GPU)
-    (1, 2, 16384, 16384),                                 # SDXL-2048 level-1 sequence length
+    (1, 2, 16384, 16384),                                 # two-tile, unmasked: SDXL-2048 level 1
 ]
+
+
+@pytest.mark.parametrize("H,S", [(20, 1024), (10, 4096), (24, 4429)])
+def test_attention_batch_invariant(H, S):
+    """Image 1's rows of a B=2 launch equal a B=1 launch on image 1 bit for bit (the unit
+    kind and split points depend on the key count only)."""
+    torch.manual_seed(S + H)
+    q, k, v = rnd(2 * S, H * 64), rnd(2 * S, H * 64), rnd(2 * S, H * 64)
+    o2 = torch.empty_like(q)
+    K.attention(q, k, v, o2, batch=2, heads=H, sq=S, skv=S, scale=0.125)
+    o1 = torch.empty(S, H * 64, dtype=torch.bfloat16, device="cuda")
+    K.attention(q[S:].contiguous(), k[S:].contiguous(), v[S:].contiguous(), o1, batch=1, heads=H, sq=S, skv=S,
+                scale=0.125)
+    assert torch.equal(o2[S:], o1)
 
 
 @pytest.mark.parametrize("B,H,sq,skv", ATTN_SHAPES)
