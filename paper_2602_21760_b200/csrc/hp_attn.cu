@@ -162,6 +162,8 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   HP_STRACE(threadIdx.x == 0, 0);
   const int h = blockIdx.y, b = blockIdx.z;
   const int q0 = blockIdx.x * 2 * kBQ;
+  const int ns = min(kBK, (p.skv + 15) & ~15);        // key columns computed (multiple of 16)
+  const int nchunk = (ns + 31) / 32;                  // 32-column softmax chunks that hold keys
 
   if (warp == kTmaWarp && lane == 0) {
     prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
@@ -195,18 +197,19 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
       HP_STRACE(true, 2);
       tc_fence_after();
       const uint64_t dk = sdesc_sw128_kmajor(sK);
+      // only the keys that exist: N = S_kv rounded up to 16 (77 -> 80 for the text context)
+      const uint32_t idesc_s = idesc_bf16_f32(kBQ, (uint32_t)ns, 0);
       for (int q = 0; q < 2; ++q) {
         const uint64_t dq = sdesc_sw128_kmajor(sQ + q * kTileBytes);
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem + q * kBK, dq + 2 * k, dk + 2 * k, kIdescS, k > 0 ? 1u : 0u);
+        for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem + q * kBK, dq + 2 * k, dk + 2 * k, idesc_s, k > 0 ? 1u : 0u);
         umma_commit(&s_full[q]);
       }
       HP_STRACE(true, 3);
       for (int q = 0; q < 2; ++q) {
         mbar_wait(&p_full[q], 0);
         tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
+        for (int k = 0; k < ns / 16; ++k) {
           const uint64_t da = sdesc_sw128_kmajor(p_atom(q, k >> 2)) + 2 * (k & 3);
           const uint64_t dv = sdesc_sw128_mnmajor(sV + k * 2048, 8192);
           umma_bf16(tmem + q * kBK, da, dv, kIdescO, k > 0 ? 1u : 0u);
@@ -233,6 +236,7 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     float mx = -INFINITY;
 #pragma unroll
     for (int c = 0; c < kBK / 32; ++c) {
+      if (c >= nchunk) break;
       uint32_t r[32];
       tmem_ld_32x32b_x32(t_s + c * 32, r);
       tmem_ld_wait();
@@ -256,6 +260,7 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     // pass 2: P = 2^(s*scale - m) in packed fp32 pairs, 2 of 8 pairs on the FMA-pipe polynomial
 #pragma unroll
     for (int c = 0; c < kBK / 32; ++c) {
+      if (c * 32 >= ns) break;                       // the PV MMA reads keys < ns only
       uint32_t r[32];
       tmem_ld_32x32b_x32(t_s + c * 32, r);
       tmem_ld_wait();
