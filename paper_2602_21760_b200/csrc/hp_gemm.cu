@@ -938,6 +938,17 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   float* scolsum = sbias + BN;                                                   // [BN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef HP_GEMM_TRACE
+  __shared__ int s_slot;
+  if (threadIdx.x == 0) s_slot = blockIdx.x == 0 ? (int)atomicAdd(&g_gemm_ctr, 1u) : -1;
+  __syncthreads();
+  const int g_slot = s_slot;
+  if (threadIdx.x == 0 && g_slot >= 0) {
+    g_gemm_ring[g_slot % kRing][9] = p.M; g_gemm_ring[g_slot % kRing][10] = p.N;
+    g_gemm_ring[g_slot % kRing][11] = p.K; g_gemm_ring[g_slot % kRing][12] = 1000 + BN;   // split-K
+  }
+#endif
+  if (threadIdx.x == 0) HP_GTRACE(0);
   const uint32_t rank = cluster_ctarank();
   const uint32_t pr = rank & 1, kh = rank >> 1;          // CTA within pair, K half
   const bool leader = pr == 0;
@@ -987,6 +998,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
           tma_load_2d_pair(smB + i * kBHalfBytes + sub * kSubBytes, &tmB, fb, (kb_lo + i) * BK, nb + sub * kSubN);
       }
       pdl_wait();
+      HP_GTRACE(2);
       uint32_t it = 0;
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
         const int s = it % STAGES;
@@ -1020,6 +1032,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
+        if (it == 0) HP_GTRACE(4);
         tc_fence_after();
         const uint64_t da = sdesc_sw128_kmajor(smA + s * kABytes);
 #pragma unroll
@@ -1033,6 +1046,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
         umma_commit_pair(&empty[s], pair_mask);
       }
       umma_commit_pair(tfull, pair_mask);
+      HP_GTRACE(5);
     }
   } else if (warp >= 4) {
     const int et = threadIdx.x - 128;
@@ -1050,8 +1064,9 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     }
     const int my_row = m0 + quarter * 32 + lane;
     if (fold && my_row < p.M) fold_row_stats(p, my_row, f_mean, f_rstd);
-    prefetch_res_row<BN>(p, 0, my_row, n0);
+    prefetch_res_row<kSubN>(p, 0, my_row, n0 + h0);   // only the 160 columns this CTA finalises
     mbar_wait(tfull, 0);
+    if (et == 0) HP_GTRACE(6);
     tc_fence_after();
   }
   __syncwarp();
@@ -1082,6 +1097,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   __syncwarp();
   tc_fence_before();
   cluster_barrier();                   // #2: partials delivered
+  if (threadIdx.x == 128) HP_GTRACE(3);
   tc_fence_after();
   if (warp >= 4) {
     const int quarter = warp & 3;
@@ -1092,7 +1108,9 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   }
   __syncwarp();
   tc_fence_before();
+  if (threadIdx.x == 128) HP_GTRACE(7);
   cluster_barrier();                   // #3: nobody frees TMEM while its pair partner still reads
+  if (threadIdx.x == 0) HP_GTRACE(8);
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair<kTmemCols>(tmem_base);
 }

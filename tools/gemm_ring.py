@@ -73,7 +73,9 @@ def main():
     prev_end = None
     for i in range(start, n):
         r = ring[i % 4096].astype(np.int64)
-        key = f"M={r[9]} N={r[10]} K={r[11]} bn={r[12]}"
+        key = (f"M={r[9]} N={r[10]} K={r[11]} splitK bn={r[12] - 1000}" if r[12] >= 1000
+               else f"M={r[9]} N={r[10]} K={r[11]} bn={r[12]}")
+        # split-K: event 3 = partials exchanged (between acc ready and the epilogue)
         wait = (r[2] - r[0]) / 1e3
         gap = (r[2] - prev_end) / 1e3 if prev_end is not None else 0.0
         first_land = (r[4] - r[2]) / 1e3
@@ -81,6 +83,8 @@ def main():
         epi = (r[7] - r[6]) / 1e3
         tail = (r[8] - r[7]) / 1e3
         total = (r[8] - r[2]) / 1e3
+        if r[12] >= 1000:   # split-K: 'epi' split into exchange (acc ready -> partials in) + epilogue
+            key += f" [xch {(r[3] - r[6]) / 1e3:.2f} epi {(r[7] - r[3]) / 1e3:.2f}]"
         a = agg[key]
         a[0] += 1
         for j, v in enumerate((gap, first_land, loop, epi, tail, total)):
