@@ -83,7 +83,7 @@ class Workload:
 def _forward_traffic():
     """DRAM bytes of one forward from the committed ncu launch list (profiles/):
     dram__bytes_read.sum + dram__bytes_write.sum summed over the forward's kernels."""
-    path = os.path.join(ROOT, "profiles", "r01", "forward_r1i_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02", "forward_r2c_traffic.json")
     try:
         with open(path) as fh:
             t = json.load(fh)
@@ -331,8 +331,8 @@ def forward_b1(den, wl, reps=20):
 
 
 def top_kernel_rooflines(bf16_peak, reps=20):
-    """The step's two dominant kernels (profiles/r01/bench_r1j_summary.txt: split-KV
-    self-attention 19%, GEGLU GEMM 17%) at their SDXL shapes, each timed live with CUDA
+    """The step's dominant kernels (profiles/r02/timeline_shapes_b2.txt: GEGLU GEMM 15%,
+    self-attention S=1024 9% + S=4096 8%) at their SDXL shapes, each timed live with CUDA
     events around a CUDA graph of `reps` back-to-back launches on the launching stream
     (inputs L2-resident between launches: a per-kernel ceiling, not the in-step rate)."""
     import torch
@@ -363,11 +363,16 @@ def top_kernel_rooflines(bf16_peak, reps=20):
         us = graph_us(lambda: K.attention(q, kv, kv, o, batch=2, heads=H, sq=S, skv=S, scale=0.125,
                                           q_col0=0, k_col0=0, v_col0=H * 64))
         fl = 4.0 * 2 * H * S * S * 64
-        # the softmax bound: one exp2 per score, 5/8 of them on MUFU (16 / clk / SM at 1965 MHz)
-        mufu_us = 2.0 * H * S * S * 5 / 8 / (16 * 148 * 1.965e9) * 1e6
-        out.append({"kernel": f"attn_splitkv S={S} H={H} B=2 (x{n} per step)", "flops_per_launch": fl,
+        scores = 2.0 * H * S * S
+        # MUFU bound: 6 of 8 exp2 pairs on MUFU.EX2 (16 / clk / SM at 1965 MHz); softmax bound:
+        # the kernel's softmax instruction stream alone, 13.2 scores / clk / SM measured on B200
+        # (tools/micro/softmax_rate.cu), with perfect balance over the 148 SMs
+        mufu_us = scores * 6 / 8 / (16 * 148 * 1.965e9) * 1e6
+        soft_us = scores / (13.2 * 148 * 1.965e9) * 1e6
+        out.append({"kernel": f"attn_stream S={S} H={H} B=2 (x{n} per step)", "flops_per_launch": fl,
                     "us": us, "achieved": fl / us / 1e6, "frac": fl / us / 1e6 / bf16_peak,
-                    "mufu_bound_us": mufu_us, "frac_of_mufu_bound": mufu_us / us})
+                    "mufu_bound_us": mufu_us, "frac_of_mufu_bound": mufu_us / us,
+                    "softmax_bound_us": soft_us, "frac_of_softmax_bound": soft_us / us})
     M, N, Kd = 2048, 10240, 1280                                # level-2 GEGLU (x60 per step)
     a = torch.randn(M, Kd, device="cuda").bfloat16()
     w = (torch.randn(N, Kd, device="cuda") * Kd ** -0.5).bfloat16()
