@@ -26,9 +26,9 @@
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;
 constexpr int kVec = 4;                     // elements per thread per sweep
-constexpr int64_t kMaxBlocks = 148 * 4;     // B200 SM count x 4 (fixed => deterministic)
+constexpr int64_t kMaxBlocks = 148 * 8;     // B200 SM count x 8 (fixed => deterministic)
 
 // ------------------------------------------------------------------------
 // exact (non-contracted) arithmetic in the compute type
