@@ -175,3 +175,52 @@ def test_sdxl1024_50step_generation_vs_oracle_loop():
     assert [t for t, _ in res.series] == [t for t, _ in series]
     assert mx <= YARD_MAX * ymx and mean <= YARD_MEAN * ymean, (mx, ymx, mean, ymean)
     assert rel.max() <= 2e-2
+
+
+def test_sdxl1024_hybrid_stage_split_natural_switch_vs_oracle():
+    """BASELINE config 2's hybrid plan at full shape with NATURAL slope detection
+    (L=12, g=4e-4, k=5, tau_cap=32: the cap calibrated from the network's own
+    discrepancy curves, profiles/r02/calibration) and the stage-split window
+    (north_star iii), against the CPU-side staged loop (oracle.loop.run_staged,
+    pipeline="stage_split") over the fp32 oracle U-Net: the switch schedule (tau1,
+    tau2, every step's label, the recorded series keys) must match exactly, and
+    the slope margin at the firing step is printed next to the M_t error."""
+    from dataclasses import replace
+    from oracle import loop as oloop
+    from oracle.stage_ref import StagedNet
+    from oracle.unet_ref import UNetRef, net_timestep
+    from paper_2602_21760_b200.stages import network_fractions, stage_cuts
+    T, seed, w = 50, 0, 5.0
+    sw = dict(L=12, g_slope=4e-4, tau_cap=32, k=5)
+    W, cond = _unet_pair(SDXL)
+    den = pipelines.build_sdxl_denoiser(SDXL, n_prompts=1, steps=T, weights=W, conditioning=cond)
+    plan = pipelines.sdxl_plan(SDXL, variant="hybrid", steps=T, seed=seed, guidance=w, denoiser=den,
+                               clock="model", switch=sw)
+    plan = replace(plan, pipeline_numerics="stage_split")
+    res = hp.run_plan(plan)
+    cuts = stage_cuts(den.net.unit_flops, network_fractions(plan.segment_fractions))
+    x_T = hp.initial_latents(plan)
+    fr = plan.segment_fractions
+    del den, plan
+    torch.cuda.empty_cache()
+    sch = pipelines.sdxl_schedule(T)
+    net = StagedNet(UNetRef(SDXL, W), "unet", cond, SDXL, T, cuts, device="cuda", timestep=net_timestep)
+    xo, series, t1, t2, labels = oloop.run_staged(net, x_T, T, w, sch.alpha_bars, sch.sigmas, sw["L"],
+                                                  sw["g_slope"], sw["tau_cap"], sw["k"], fr,
+                                                  pipeline="stage_split")
+    assert t1 is not None and t1 < sw["tau_cap"], "the detector must fire by itself here"
+    assert (res.tau1, res.tau2) == (t1, t2), ((res.tau1, res.tau2), (t1, t2))
+    assert [s.value for s in res.stages] == labels
+    assert [t for t, _ in res.series] == [t for t, _ in series]
+    ms = dict(series)
+    t_fire = T - t1 + 1
+    g = (ms[t_fire] - ms[t_fire + sw["L"]]) / sw["L"]
+    m_gpu = np.array([m for _, m in res.series])
+    m_ref = np.array([m for _, m in series])
+    rel = np.abs(m_gpu - m_ref) / np.abs(m_ref)
+    mx, mean, _, _ = _report(f"sdxl1024 hybrid stage_split x0 (tau1={t1}, tau2={t2})", torch.from_numpy(res.x0),
+                             torch.from_numpy(xo))
+    print(f"PARITY sdxl1024 hybrid natural switch: slope at firing {g:.4g} (g_slope {sw['g_slope']}, "
+          f"margin {sw['g_slope'] - g:.3g}), M_t max rel err {rel.max():.3g}")
+    assert rel.max() <= 2e-2
+    assert mx <= 2.5e-2 and mean <= 5e-3, (mx, mean)
