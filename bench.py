@@ -68,6 +68,14 @@ class Workload:
                      "sd3": "sd3-1024-28step-fm-euler-cfg"}[key]
         self.sampler = "flow-matching Euler" if self.dit else "DDIM"
 
+    @property
+    def params(self) -> int:
+        """Parameter count of the network (analytic, from its parameter specs)."""
+        import math
+        from paper_2602_21760_b200.denoiser.weights import mmdit_param_specs, unet_param_specs
+        specs = mmdit_param_specs(self.spec) if self.dit else unet_param_specs(self.spec)
+        return sum(math.prod(shape) for _, shape, _ in specs)
+
     def flops(self, n):
         if self.dit:
             from paper_2602_21760_b200.denoiser.mmdit import mmdit_flops
@@ -162,7 +170,7 @@ def _max_over_ranks(ws, v):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -439,7 +447,10 @@ def time_pairs(args, wl, ws, rank, local):
     den = wl.build(wl.spec, n_prompts=args.prompts, steps=wl.T, seed=0)   # same weights in a pair
     plan = wl.plan(wl.spec, variant="hybrid", steps=wl.T, n_prompts=args.prompts, seed=role.pair, denoiser=den,
                    clock="device")
-    sess = parallel.GroupSession(plan, groups[role.pair])
+    # HP_BENCH_SHARED_GPU=1 (validation only): every rank on GPU 0 over gloo with host-side
+    # flag waits, so the multi-process pair path runs end to end on a one-GPU box
+    shared = os.environ.get("HP_BENCH_SHARED_GPU") == "1"
+    sess = parallel.GroupSession(plan, groups[role.pair], wait="host" if shared else "device")
     for _ in range(args.warmup):
         sess.run()
     x_host = hp.initial_latents(plan)
@@ -491,10 +502,16 @@ def main():
 
     import torch
     ws, rank, local = _dist()
+    shared = os.environ.get("HP_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2602_21760_b200 as hp  # noqa: F401
     wl = Workload(args.spec)
     spec = wl.spec
@@ -509,7 +526,7 @@ def main():
         res = None
     if ws > 1:
         import torch.distributed as dist
-        flag = torch.tensor([1.0 if err else 0.0], device="cuda")
+        flag = torch.tensor([1.0 if err else 0.0], device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(flag, op=dist.ReduceOp.MAX)
         if flag.item() and not err:
             err = "another rank failed"
@@ -536,6 +553,7 @@ def main():
             dist.destroy_process_group()
         return 0
     k1_s = samp[65536]["us"] * 1e-6 if samp else 0.0
+    den_weight_gb = wl.params * 2 / 1e9
     if mode != "pairs":
         # per GPU over the timed region itself: each rank ran K generations of 50 steps, each
         # step one B=2 forward (+ one sampler launch, counted in the time, not the FLOPs)
@@ -563,9 +581,9 @@ def main():
                    "plan": ("hybrid on condition-partitioned pairs" if mode == "pairs"
                             else f"serial (CFG batched B={2 * args.prompts})"),
                    "parallelism": f"{mode}x{ws}" if ws > 1 else "single",
-                   "params_b": round(sum(p.numel() for p in den.net.W.values()) / 1e9, 3)
-                   if hasattr(den.net, "W") else None,
-                   "l2": "working set (5.1 GB of bf16 weights per step) >> 126 MB L2"},
+                   "params_b": round(wl.params / 1e9, 3),
+                   "l2": (f"working set ({den_weight_gb:.1f} GB of bf16 weights per step) >> 126 MB L2"
+                          if den_weight_gb > 0.126 else "weights fit in L2 (small network)")},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(args.steps * wl.T * (launches_fwd + 1)),
         "roofline": {"bound": "tensor", "kernel": roof_kernel,
@@ -573,7 +591,8 @@ def main():
                      "peak": bf16_sus, "unit": "TFLOP/s", "frac": achieved / bf16_sus,
                      "peak_kind": f"{peak_src} sustained", "frac_of_burst": achieved / bf16_burst,
                      "flops_per_launch": roof_flops,
-                     "forward_ms": fwd_s * 1e3 if fwd_s else None, **_forward_traffic(),
+                     "forward_ms": fwd_s * 1e3 if fwd_s else None,
+                     **(_forward_traffic() if wl.key == "sdxl" else {"traffic": None}),
                      "top_kernels": top, "top_kernels_peak": f"{peak_src} burst bf16 {bf16_burst}"},
         "forward_b1": {"ms": b1_s * 1e3, "tflops": b1_flops / b1_s / 1e12,
                        "frac_of_sustained": b1_flops / b1_s / 1e12 / bf16_sus, "flops": b1_flops,
