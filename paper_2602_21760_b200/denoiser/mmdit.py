@@ -76,6 +76,19 @@ class MMDiT:
             self.blocks.append(blk)
         self.nout_w, self.nout_b = _bf(g("norm_out.linear.weight")), _f32(g("norm_out.linear.bias"))
         self.out_w, self.out_b = _bf(g("proj_out.weight")), _f32(g("proj_out.bias"))
+        # every block's adaLN modulation weights (and norm_out's) stacked in forward order,
+        # so one GEMV per stage computes all of them at the HBM rate (they depend on the
+        # step's conditioning vector only); the per-block entries are row views into it
+        mw = torch.cat([blk["mod_w"] for blk in self.blocks] + [self.nout_w])
+        mb = torch.cat([blk["mod_b"] for blk in self.blocks] + [self.nout_b])
+        self.mod_w_all, self.mod_b_all = mw.contiguous(), mb.contiguous()
+        self.mod_rows = [0]
+        for blk in self.blocks:
+            self.mod_rows.append(self.mod_rows[-1] + blk["mod_w"].shape[0])
+        self.mod_rows.append(self.mod_rows[-1] + self.nout_w.shape[0])
+        for d, blk in enumerate(self.blocks):
+            blk["mod_w"] = self.mod_w_all[self.mod_rows[d]:self.mod_rows[d + 1]]
+            blk["mod_b"] = self.mod_b_all[self.mod_rows[d]:self.mod_rows[d + 1]]
         self.ctx_cache, self.pemb = {}, {}
 
     @staticmethod
@@ -131,6 +144,14 @@ class MMDiT:
         hid_c = torch.empty((n, L, s.mlp_ratio * H), dtype=torch.bfloat16, device=dev)
         scale = 1.0 / math.sqrt(H // heads)
         units = self.units
+        # modulation vectors of the blocks (and output norm) this stage runs: one GEMV over
+        # the stacked weight rows [r0, r1)
+        d0 = max(a, 1) - 1
+        d1 = min(b - 1, s.depth)                   # blocks [d0, d1); unit depth+1 is the output head
+        r0 = self.mod_rows[d0]
+        r1 = self.mod_rows[d1 + 1] if b == len(units) else self.mod_rows[d1]
+        mods = (K.linear_small(c, self.mod_w_all[r0:r1], self.mod_b_all[r0:r1], act_in=K.ACT_SILU)
+                if r1 > r0 else None)
         for i in range(a, b):
             u = units[i]
             if record is not None and i in record:
@@ -142,15 +163,17 @@ class MMDiT:
                 X[:, Ti:].copy_(self.ctx_cache[key])
                 continue
             if u[0] == "out":
-                nf = K.linear_small(c, self.nout_w, self.nout_b, act_in=K.ACT_SILU)     # [n, 2H]: scale, shift
-                Y = K.layer_norm_joint(X, H, T, Ti, nf[:, H:2 * H], nf[:, 0:H], nf[:, H:2 * H], nf[:, 0:H], 2 * H)
+                nf = mods[:, self.mod_rows[s.depth] - r0:self.mod_rows[s.depth + 1] - r0]   # [n, 2H]: scale, shift
+                Y = K.layer_norm_joint(X, H, T, Ti, nf[:, H:2 * H], nf[:, 0:H], nf[:, H:2 * H], nf[:, 0:H],
+                                       mods.shape[1])
                 o = K.gemm(Y[:, :Ti], self.out_w, bias=self.out_b)                       # [n, Ti, P*P*C]
                 v = K.patchify(o, n, Hl, Wl, C, P, inverse=True)
                 return {"eps": v.view(n, Hl, Wl, C)}
             blk = self.blocks[u[1]]
             last = blk["last"]
-            mod = K.linear_small(c, blk["mod_w"], blk["mod_b"], act_in=K.ACT_SILU)   # [n, 12H] (8H last)
-            ldm = mod.shape[1]
+            d = u[1]
+            mod = mods[:, self.mod_rows[d] - r0:self.mod_rows[d + 1] - r0]      # [n, 12H] (8H last)
+            ldm = mods.shape[1]
             mi = mod[:, :6 * H]
             mc = mod[:, 6 * H:]
             # image: shift_msa, scale_msa, gate_msa, shift_mlp, scale_mlp, gate_mlp

@@ -5,7 +5,7 @@ of one eager forward (kernels.check records each call's descriptor), then
 aggregated per (call, shape) with FLOPs and achieved TFLOP/s for GEMMs and
 attention, sorted by time.
 
-    python tools/timeline_shapes.py [b1] [out.txt]
+    python tools/timeline_shapes.py [b1] [sd3] [out.txt]
 """
 import collections
 import re
@@ -38,12 +38,14 @@ def flops(desc):
 
 def main():
     b1 = "b1" in sys.argv
-    out = [a for a in sys.argv[1:] if a != "b1"]
-    spec = Wm.SDXL
-    den = pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=50)
-    x = torch.randn(1, spec.latent_hw * spec.latent_hw * 4, device="cuda")
+    sd3 = "sd3" in sys.argv
+    out = [a for a in sys.argv[1:] if a not in ("b1", "sd3")]
+    spec = Wm.SD3 if sd3 else Wm.SDXL
+    den = (pipelines.build_sd3_denoiser(spec, n_prompts=1, steps=28) if sd3
+           else pipelines.build_sdxl_denoiser(spec, n_prompts=1, steps=50))
+    x = torch.randn(1, spec.latent_hw * spec.latent_hw * spec.in_channels, device="cuda")
     den.load_input(x)
-    run = (lambda: den.conditional(x, 30)) if b1 else (lambda: den.branches(x, 30, den.input_slot()))
+    run = (lambda: den.conditional(x, 20)) if b1 else (lambda: den.branches(x, 20, den.input_slot()))
     for _ in range(3):
         run()
     torch.cuda.synchronize()
