@@ -508,10 +508,13 @@ def main():
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
+        # a bounded collective timeout: a rank that fails inside a collective (e.g. while
+        # the pair exchanges IPC handles) turns its partner's wait into an error, not a hang
+        from datetime import timedelta
         if shared:
-            dist.init_process_group("gloo")
+            dist.init_process_group("gloo", timeout=timedelta(minutes=10))
         else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=timedelta(minutes=10))
     import paper_2602_21760_b200 as hp  # noqa: F401
     wl = Workload(args.spec)
     spec = wl.spec
