@@ -224,3 +224,55 @@ def test_sdxl1024_hybrid_stage_split_natural_switch_vs_oracle():
           f"margin {sw['g_slope'] - g:.3g}), M_t max rel err {rel.max():.3g}")
     assert rel.max() <= 2e-2
     assert mx <= 2.5e-2 and mean <= 5e-3, (mx, mean)
+
+
+class _RefBranchesDiT:
+    """oracle.loop denoiser protocol over MMDiTRef on CUDA (NHWC latents, FM timestep)."""
+
+    def __init__(self, net, cond, spec, T):
+        self.net, self.c, self.s, self.T = net, cond, spec, T
+
+    def branches(self, x, t):
+        B = x.shape[0]
+        hw, ch = self.s.latent_hw, self.s.in_channels
+        xt = torch.from_numpy(np.asarray(x)).cuda().float().view(B, hw, hw, ch)
+        xt = torch.cat([xt, xt])
+        ctx = torch.cat([self.c.context[:B], self.c.null_context.expand(B, -1, -1)])
+        pooled = torch.cat([self.c.pooled[:B], self.c.null_pooled.expand(B, -1)])
+        tt = torch.full((2 * B,), 1000.0 * t / self.T, device="cuda")
+        with torch.no_grad():
+            e = self.net(xt, tt, ctx, pooled).reshape(2 * B, -1).double().cpu().numpy()
+        return e[:B], e[B:]
+
+
+def test_sd3_28step_euler_generation_vs_oracle_loop():
+    """BASELINE config 3's sampler end to end at full shape: 28 flow-matching Euler steps
+    with CFG through run_plan (serial) vs oracle.loop.run_exact(update="euler") over the
+    fp32 MMDiT, with the stock-torch bf16 network as the yardstick."""
+    from oracle import loop as oloop
+    from oracle.mmdit_ref import MMDiTRef
+    T, seed, w = 28, 0, 5.0
+    s = SD3
+    W = init_weights(mmdit_param_specs(s), seed=0, device="cuda")
+    cond = synthetic_conditioning(1, s.ctx_len, s.ctx_dim, s.pooled_dim, device="cuda")
+    den = pipelines.build_sd3_denoiser(s, n_prompts=1, steps=T, weights=W, conditioning=cond)
+    plan = pipelines.sd3_plan(s, variant="serial", steps=T, seed=seed, guidance=w, denoiser=den, clock="model")
+    res = hp.run_plan(plan)
+    x_T = hp.initial_latents(plan)
+    del den, plan
+    torch.cuda.empty_cache()
+    sch = pipelines.sd3_schedule(T)
+    xo, series = oloop.run_exact(_RefBranchesDiT(MMDiTRef(s, W), cond, s, T), x_T, T, w, sch.alpha_bars,
+                                 sch.sigmas, update="euler")
+    xy, _ = oloop.run_exact(_RefBranchesDiT(MMDiTRef(s, W, torch.bfloat16), cond, s, T), x_T, T, w,
+                            sch.alpha_bars, sch.sigmas, update="euler")
+    mx, mean, _, _ = _report("sd3 28-step x0 (serial, FM Euler, w=5)", torch.from_numpy(res.x0),
+                             torch.from_numpy(xo))
+    ymx, ymean, _, _ = _report("sd3 28-step x0 [torch bf16 yardstick]", torch.from_numpy(xy), torch.from_numpy(xo))
+    m_gpu = np.array([m for _, m in res.series])
+    m_ref = np.array([m for _, m in series])
+    rel = np.abs(m_gpu - m_ref) / np.abs(m_ref)
+    print(f"PARITY sd3 28-step M_t: max rel err {rel.max():.3g}")
+    assert [t for t, _ in res.series] == [t for t, _ in series]
+    assert mx <= YARD_MAX * ymx and mean <= YARD_MEAN * ymean, (mx, ymx, mean, ymean)
+    assert rel.max() <= 2e-2
