@@ -279,27 +279,42 @@ def sampler_roofline(hbm_peak):
         ob = torch.empty(n, dtype=torch.bfloat16, device="cuda")
         ws = K.workspace()
 
-        def launch():
+        # the exchange-fused form: eps_u sits behind a flag word (system-scope acquire
+        # by one thread per CTA before any CTA reads it). On one GPU the flag is
+        # pre-released and eps_u is local, so this times the acquire + the fused read
+        # path; the NVLink leg is bounded by the model below.
+        flag = torch.ones(1, dtype=torch.int32, device="cuda")
+
+        def launch(fused=False):
             K.sampler_step(x=x, eps_c=ec, eps_u=eu, x_out=out, x_out_bf16=ob, update=N.HP_UPDATE_DDIM, t=30,
                            w=5.0, c_sigma=c.c_sigma, c_sqrt_ab=c.c_sqrt_ab, c_sqrt_ab_prev=c.c_sqrt_ab_prev,
-                           c_sqrt_1m_ab_prev=c.c_sqrt_1m_ab_prev, ws=ws)
+                           c_sqrt_1m_ab_prev=c.c_sqrt_1m_ab_prev, ws=ws,
+                           wait_flag=flag if fused else None, wait_value=1 if fused else 0)
         for _ in range(5):
             launch()
+            launch(True)
         flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-        times = []
-        for _ in range(20):
-            flush.zero_()                                    # evict L2 (> 126 MB)
-            torch.cuda._sleep(100000)                        # GPU busy while the host enqueues: device time only
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            launch()
-            b.record()
-            torch.cuda.synchronize()
-            times.append(a.elapsed_time(b) / 1e3)
-        t = statistics.median(times)
+
+        def cold(fused):
+            times = []
+            for _ in range(20):
+                flush.zero_()                                # evict L2 (> 126 MB)
+                torch.cuda._sleep(100000)                    # GPU busy while the host enqueues: device time only
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                launch(fused)
+                b.record()
+                torch.cuda.synchronize()
+                times.append(a.elapsed_time(b) / 1e3)
+            return statistics.median(times)
+        t, tf = cold(False), cold(True)
         bytes_ = 14 * n       # x f32 in + eps_c, eps_u bf16 + x f32 out + x bf16 out
+        # fused over NVLink: 12 n local HBM bytes + 2 n peer bytes
+        nvl_bound = max(12 * n / (hbm_peak * 1e9), 2 * n / 900e9)
         res[n] = {"elements": n, "us": t * 1e6, "algorithmic_bytes": bytes_, "gbs": bytes_ / t / 1e9,
-                  "frac": bytes_ / t / 1e9 / hbm_peak}
+                  "frac": bytes_ / t / 1e9 / hbm_peak,
+                  "fused_flag_us": tf * 1e6, "fused_flag_frac": bytes_ / tf / 1e9 / hbm_peak,
+                  "fused_nvlink_bound_us": nvl_bound * 1e6}
     return res
 
 

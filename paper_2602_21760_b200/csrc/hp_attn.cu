@@ -2,7 +2,8 @@
 //
 // Two kernels (hp_attention picks one):
 //   attn_single_kernel   S_kv <= 128 (cross-attention, causal text-encoder
-//                        attention): two query tiles per CTA, 2 CTAs/SM.
+//                        attention): one query tile per CTA, each row's keys
+//                        split between two softmax warps, 3 CTAs/SM.
 //   attn_stream_kernel   everything else, persistent (one CTA per SM walks the
 //                        work units): two softmax "streams" per CTA, each
 //                        with its own score-MMA and PV-MMA issuing warp; the
@@ -119,12 +120,15 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, u
 }
 
 // Single-block kernel: every key fits one 128-key block (cross-attention, skv <=
-// 128, and the text encoders' causal attention). One CTA = two 128-query tiles;
-// 320 threads: warps 0-3 / 4-7 softmax of tile 0 / 1, warp 8 TMA, warp 9 MMA.
-// No rescale exists; O_q reuses S_q's TMEM columns once the softmax has consumed
-// S_q, P_0 overwrites Q_0|Q_1 and P_1 overwrites K|X after both score MMAs, so the
-// CTA needs 256 TMEM columns and 97 KB of smem and two CTAs share an SM (one's
-// TMA -> MMA -> softmax -> PV -> store chain overlaps the other's).
+// 128, and the text encoders' causal attention). One CTA = one 128-query tile, 288
+// threads: warps 0-7 softmax (warp w owns TMEM lane quarter w & 3 and key half
+// w >> 2, in 16-key units: 3 + 2 units for the 77-token context), warp 8 TMA + MMA
+// issue + TMEM allocation. The chain load -> score MMA -> softmax -> PV -> store is
+// pure latency at these sizes, so it is kept short: two warps per row halve the
+// softmax leg (row max and sum meet in shared memory), and three CTAs share an SM
+// so the tiles of a B=2 launch (320 at level 3) are all resident in one wave. P
+// overwrites Q (keys 0-63) and K (64-127) once the score MMA has read them; O
+// reuses the score columns in TMEM.
 #ifdef HP_ATTN_TRACE
 __device__ long long g_single_trace[16];
 #define HP_STRACE(cond, ev) do { if ((cond) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) \
@@ -132,47 +136,58 @@ __device__ long long g_single_trace[16];
 #else
 #define HP_STRACE(cond, ev) do {} while (0)
 #endif
-constexpr int kSingleThreads = 320;
-constexpr uint32_t kSingleCols = 256;
-constexpr size_t kSingleSmem = (size_t)kTileBytes * 5 + 256;
+constexpr int kSingleThreads = 288;
+constexpr uint32_t kSingleCols = 128;
+constexpr size_t kSingleSmem = (size_t)kTileBytes * 3 + 64 + 4 * 128 * 4;   // Q K V | barriers | max, sum
+
+__device__ __forceinline__ void tmem_ld_x16_at(uint32_t taddr, uint32_t* r, const int base) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : HP_R8(base), HP_R8(base + 8)
+      : "r"(taddr));
+}
 
 template <bool MASK>     // MASK: the key block is partial (or causal)
-__global__ void __launch_bounds__(kSingleThreads, 2)
+__global__ void __launch_bounds__(kSingleThreads, 3)
 attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, AttnParams p) {
-  constexpr int kTmaWarp = 8, kMmaWarp = 9;
+  constexpr int kIssueWarp = 8;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                       // 2 tiles
-  uint8_t* sK = sQ + 2 * kTileBytes;
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + kTileBytes;
   uint8_t* sV = sK + kTileBytes;
-  uint8_t* sX = sV + kTileBytes;            // spare tile: second atom of P_1
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + kTileBytes);
-  auto p_atom = [&](int q, int a) -> uint8_t* {       // 64-key SW128 atom a of P_q
-    return q == 0 ? sQ + a * kTileBytes : (a == 0 ? sK : sX);
-  };
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = q_full + 1;
-  uint64_t* s_full = kv_full + 1;          // [2] per query tile
-  uint64_t* p_full = s_full + 2;           // [2]
-  uint64_t* o_done = p_full + 2;           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kTileBytes);
+  uint64_t* qk_full = bars;
+  uint64_t* v_full = bars + 1;
+  uint64_t* s_full = bars + 2;
+  uint64_t* p_full = bars + 3;               // 8 softmax warps
+  uint64_t* o_done = bars + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+  float* s_max = reinterpret_cast<float*>(bars + 8);     // [half][row]
+  float* s_sum = s_max + 2 * kBQ;                        // [half][row]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   HP_STRACE(threadIdx.x == 0, 0);
   const int h = blockIdx.y, b = blockIdx.z;
-  const int q0 = blockIdx.x * 2 * kBQ;
+  const int q0 = blockIdx.x * kBQ;
   const int ns = min(kBK, (p.skv + 15) & ~15);        // key columns computed (multiple of 16)
-  const int nchunk = (ns + 31) / 32;                  // 32-column softmax chunks that hold keys
+  const int nu = ns >> 4;                             // 16-key units
 
-  if (warp == kTmaWarp && lane == 0) {
-    prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
-    mbar_init(q_full, 1);
-    mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_done[i], 1); }
-    fence_barrier_init();
+  if (warp == kIssueWarp) {
+    if (lane == 0) {
+      prefetch_tmap(&tmQ); prefetch_tmap(&tmK); prefetch_tmap(&tmV);
+      mbar_init(qk_full, 1);
+      mbar_init(v_full, 1);
+      mbar_init(s_full, 1);
+      mbar_init(p_full, 8);
+      mbar_init(o_done, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc<kSingleCols>(tmem_slot);
   }
-  if (warp == kMmaWarp) tmem_alloc<kSingleCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -181,140 +196,119 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   HP_STRACE(threadIdx.x == 0, 1);
   pdl_trigger();
 
-  if (warp == kTmaWarp) {
+  if (warp == kIssueWarp) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
-#pragma unroll
-      for (int q = 0; q < 2; ++q) tma_load_3d(sQ + q * kTileBytes, &tmQ, q_full, p.q_col0 + h * kD, q0 + q * kBQ, b);
-      mbar_arrive_expect_tx(kv_full, 2 * kTileBytes);
-      tma_load_3d(sK, &tmK, kv_full, p.k_col0 + h * kD, 0, b);
-      tma_load_3d(sV, &tmV, kv_full, p.v_col0 + h * kD, 0, b);
-    }
-  } else if (warp == kMmaWarp) {
-    if (lane == 0) {
-      mbar_wait(q_full, 0);
-      mbar_wait(kv_full, 0);
+      mbar_arrive_expect_tx(qk_full, 2 * kTileBytes);
+      tma_load_3d(sQ, &tmQ, qk_full, p.q_col0 + h * kD, q0, b);
+      tma_load_3d(sK, &tmK, qk_full, p.k_col0 + h * kD, 0, b);
+      mbar_arrive_expect_tx(v_full, kTileBytes);
+      tma_load_3d(sV, &tmV, v_full, p.v_col0 + h * kD, 0, b);
+      mbar_wait(qk_full, 0);
       HP_STRACE(true, 2);
       tc_fence_after();
-      const uint64_t dk = sdesc_sw128_kmajor(sK);
+      const uint64_t dq = sdesc_sw128_kmajor(sQ), dk = sdesc_sw128_kmajor(sK);
       // only the keys that exist: N = S_kv rounded up to 16 (77 -> 80 for the text context)
       const uint32_t idesc_s = idesc_bf16_f32(kBQ, (uint32_t)ns, 0);
-      for (int q = 0; q < 2; ++q) {
-        const uint64_t dq = sdesc_sw128_kmajor(sQ + q * kTileBytes);
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem + q * kBK, dq + 2 * k, dk + 2 * k, idesc_s, k > 0 ? 1u : 0u);
-        umma_commit(&s_full[q]);
-      }
+      for (int k = 0; k < kD / 16; ++k) umma_bf16(tmem, dq + 2 * k, dk + 2 * k, idesc_s, k > 0 ? 1u : 0u);
+      umma_commit(s_full);
       HP_STRACE(true, 3);
-      for (int q = 0; q < 2; ++q) {
-        mbar_wait(&p_full[q], 0);
-        tc_fence_after();
-        for (int k = 0; k < ns / 16; ++k) {
-          const uint64_t da = sdesc_sw128_kmajor(p_atom(q, k >> 2)) + 2 * (k & 3);
-          const uint64_t dv = sdesc_sw128_mnmajor(sV + k * 2048, 8192);
-          umma_bf16(tmem + q * kBK, da, dv, kIdescO, k > 0 ? 1u : 0u);
-        }
-        umma_commit(&o_done[q]);
+      mbar_wait(v_full, 0);
+      mbar_wait(p_full, 0);
+      tc_fence_after();
+      for (int k = 0; k < nu; ++k) {
+        const uint64_t da = sdesc_sw128_kmajor(k < 4 ? sQ : sK) + 2 * (k & 3);
+        const uint64_t dv = sdesc_sw128_mnmajor(sV + k * 2048, 8192);
+        umma_bf16(tmem, da, dv, kIdescO, k > 0 ? 1u : 0u);
       }
+      umma_commit(o_done);
     }
   } else {
     // ------------------------------ softmax ------------------------------
-    const int q = warp >> 2;                  // query tile of this warpgroup
-    const int quarter = warp & 3;
+    const int quarter = warp & 3, half = warp >> 2;
     const int row = quarter * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t t_s = tmem + lane_base + q * kBK;
-    const uint32_t t_o = t_s;                 // O_q overwrites S_q
+    const uint32_t t_s = tmem + ((uint32_t)(quarter * 32) << 16);
+    const int u0 = half ? (nu + 1) >> 1 : 0, u1 = half ? nu : (nu + 1) >> 1;
     const uint64_t scale2 = pack2(p.scale_log2, p.scale_log2);
-    mbar_wait(&s_full[q], 0);
+    // keys this row may see: the sequence end and, when causal, the row's own position
+    const int valid = p.causal ? min(min(kBK, p.skv), q0 + row + 1) : min(kBK, p.skv);
+    mbar_wait(s_full, 0);
     HP_STRACE(threadIdx.x == 0, 4);
     tc_fence_after();
-    // keys this row may see: the sequence end and, when causal, the row's own position
-    const int valid = p.causal ? min(min(kBK, p.skv), q0 + q * kBQ + row + 1) : min(kBK, p.skv);
-    // pass 1: row max straight from TMEM, 32 columns at a time (two CTAs share the
-    // SM's registers here, so the row is not held whole)
+    // pass 1: this half's row max, two units per TMEM round trip
     float mx = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < kBK / 32; ++c) {
-      if (c >= nchunk) break;
+    for (int u = u0; u < u1; u += 2) {
       uint32_t r[32];
-      tmem_ld_32x32b_x32(t_s + c * 32, r);
+      tmem_ld_x16_at(t_s + u * 16, r, 0);
+      if (u + 1 < u1) tmem_ld_x16_at(t_s + u * 16 + 16, r, 16);
       tmem_ld_wait();
-      if (MASK && valid < kBK) {
+      const int n = u + 1 < u1 ? 32 : 16;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
-      }
-#pragma unroll
-      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+      for (int i = 0; i < 32; ++i)
+        if (i < n && (!MASK || u * 16 + i < valid)) mx = fmaxf(mx, __uint_as_float(r[i]));
     }
+    s_max[half * kBQ + row] = mx;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    mx = fmaxf(s_max[row], s_max[kBQ + row]);
     const float m = mx * p.scale_log2;
     const uint64_t negm2 = pack2(-m, -m);
-    // P overwrites Q and K: both tiles' score MMAs must have finished reading them
-    // (the commit behind S_1 covers S_0 too)
-    if (q == 0) {
-      mbar_wait(&s_full[1], 0);
-      tc_fence_after();
-    }
+    // pass 2: P = 2^(s*scale - m) in packed fp32 pairs, 2 of 8 pairs on the FMA-pipe polynomial;
+    // P overwrites Q / K, which the score MMA (complete: s_full) no longer reads
     uint64_t sum2[4] = {0ull, 0ull, 0ull, 0ull};
-    // pass 2: P = 2^(s*scale - m) in packed fp32 pairs, 2 of 8 pairs on the FMA-pipe polynomial
-#pragma unroll
-    for (int c = 0; c < kBK / 32; ++c) {
-      if (c * 32 >= ns) break;                       // the PV MMA reads keys < ns only
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(t_s + c * 32, r);
+    for (int u = u0; u < u1; ++u) {
+      uint32_t r[16];
+      tmem_ld_x16_at(t_s + u * 16, r, 0);
       tmem_ld_wait();
-      if (MASK && valid < kBK) {
+      if (MASK && valid < (u + 1) * 16) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i >= valid) r[i] = __float_as_uint(-INFINITY);
+        for (int i = 0; i < 16; ++i)
+          if (u * 16 + i >= valid) r[i] = __float_as_uint(-INFINITY);
       }
-      uint32_t packed[16];
+      uint32_t packed[8];
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
+      for (int i = 0; i < 16; i += 2) {
         const uint64_t x2 = ffma2(pack2u(r[i], r[i + 1]), scale2, negm2);
         uint64_t e2;
-        const int pr = (i >> 1) & 7;
+        const int pr = i >> 1;
         if (pr == 3 || pr == 7) e2 = exp2_poly2(x2);
         else e2 = pack2(ex2f(lo2(x2)), ex2f(hi2(x2)));
-        sum2[(i >> 1) & 3] = fadd2(sum2[(i >> 1) & 3], e2);
-        packed[i / 2] = pack_bf16(lo2(e2), hi2(e2));
+        sum2[pr & 3] = fadd2(sum2[pr & 3], e2);
+        packed[pr] = pack_bf16(lo2(e2), hi2(e2));
       }
-      uint8_t* atom = p_atom(q, c >> 1) + row * 128;
+      uint8_t* atom = (u < 4 ? sQ : sK) + row * 128;
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const int chunk = ((c & 1) * 4 + qq) ^ (row & 7);
+      for (int qq = 0; qq < 2; ++qq) {
+        const int chunk = ((u & 3) * 2 + qq) ^ (row & 7);
         *reinterpret_cast<uint4*>(atom + chunk * 16) =
             make_uint4(packed[4 * qq], packed[4 * qq + 1], packed[4 * qq + 2], packed[4 * qq + 3]);
       }
     }
-    const uint64_t s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
-    const float l = lo2(s01) + hi2(s01);
     fence_proxy_async_smem();
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&p_full[q]);
+    if (lane == 0) mbar_arrive(p_full);
     HP_STRACE(threadIdx.x == 0, 5);
-    mbar_wait(&o_done[q], 0);
+    const uint64_t s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
+    s_sum[half * kBQ + row] = lo2(s01) + hi2(s01);
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const float inv = 1.0f / (s_sum[row] + s_sum[kBQ + row]);
+    mbar_wait(o_done, 0);
     HP_STRACE(threadIdx.x == 0, 6);
     tc_fence_after();
-    const int qrow = q0 + q * kBQ + row;
-    const float inv = 1.0f / l;
+    // O (64 columns, over the score columns): this warp stores its half of the row
     uint32_t o[32];
+    tmem_ld_32x32b_x32(t_s + half * 32, o);
+    tmem_ld_wait();
+    const int qrow = q0 + row;
+    if (qrow < p.sq) {
+      __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + half * 32;
 #pragma unroll
-    for (int c = 0; c < kD / 32; ++c) {
-      tmem_ld_32x32b_x32(t_o + c * 32, o);
-      tmem_ld_wait();
-      if (qrow < p.sq) {
-        __nv_bfloat16* dst = p.o + ((long long)b * p.sq + qrow) * p.ldo + h * kD + c * 32;
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          uint4 u = make_uint4(pack_bf16(__uint_as_float(o[8 * qq]) * inv, __uint_as_float(o[8 * qq + 1]) * inv),
-                               pack_bf16(__uint_as_float(o[8 * qq + 2]) * inv, __uint_as_float(o[8 * qq + 3]) * inv),
-                               pack_bf16(__uint_as_float(o[8 * qq + 4]) * inv, __uint_as_float(o[8 * qq + 5]) * inv),
-                               pack_bf16(__uint_as_float(o[8 * qq + 6]) * inv, __uint_as_float(o[8 * qq + 7]) * inv));
-          reinterpret_cast<uint4*>(dst)[qq] = u;
-        }
+      for (int qq = 0; qq < 4; ++qq) {
+        uint4 u = make_uint4(pack_bf16(__uint_as_float(o[8 * qq]) * inv, __uint_as_float(o[8 * qq + 1]) * inv),
+                             pack_bf16(__uint_as_float(o[8 * qq + 2]) * inv, __uint_as_float(o[8 * qq + 3]) * inv),
+                             pack_bf16(__uint_as_float(o[8 * qq + 4]) * inv, __uint_as_float(o[8 * qq + 5]) * inv),
+                             pack_bf16(__uint_as_float(o[8 * qq + 6]) * inv, __uint_as_float(o[8 * qq + 7]) * inv));
+        reinterpret_cast<uint4*>(dst)[qq] = u;
       }
     }
   }
@@ -323,7 +317,7 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
   __syncthreads();
   HP_STRACE(threadIdx.x == 0, 8);
   tc_fence_after();
-  if (warp == kMmaWarp) tmem_dealloc<kSingleCols>(tmem);
+  if (warp == kIssueWarp) tmem_dealloc<kSingleCols>(tmem);
 }
 
 // ---------------------------------------------------------------------------
@@ -777,7 +771,7 @@ extern "C" int hp_attention(const hp_attn_desc* d, void* stream) {
   p.n_kv = (d->skv + kBK - 1) / kBK;
   dim3 grid((d->sq + 2 * kBQ - 1) / (2 * kBQ), d->heads, d->batch);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p.n_kv == 1) return launch_single(grid, st, tq, tk, tv, p);
+  if (p.n_kv == 1) return launch_single(dim3((d->sq + kBQ - 1) / kBQ, d->heads, d->batch), st, tq, tk, tv, p);
   const bool mask = (d->skv % kBK) != 0;
   // persistent CTAs over work units. The unit kind depends on the key count only, never
   // on batch or heads, so an image's rows are computed the same way whatever else is in

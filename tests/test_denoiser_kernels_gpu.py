@@ -94,6 +94,8 @@ def test_conv3x3_implicit_gemm(n, h, w, c, co, stride):
 # (S_kv % 128 != 0):
 ATTN_SHAPES = [
     (1, 1, 128, 128), (2, 4, 256, 77),                    # single block
+    (2, 20, 1024, 77), (1, 3, 200, 16), (1, 2, 130, 100),  # single block: SDXL cross-attention, one 16-key
+                                                          # unit (second softmax half idle), odd unit count
     (2, 3, 256, 256), (1, 2, 1024, 1024),                 # split-KV, unmasked
     (2, 2, 333, 333), (2, 1, 130, 500),                   # split-KV, masked
     (2, 10, 4096, 4096), (2, 20, 1024, 1024),             # split-KV at the SDXL-1024 shapes (B=2)
@@ -104,17 +106,17 @@ ATTN_SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("H,S", [(20, 1024), (10, 4096), (24, 4429)])
-def test_attention_batch_invariant(H, S):
+@pytest.mark.parametrize("H,S,SKV", [(20, 1024, 1024), (10, 4096, 4096), (24, 4429, 4429), (20, 1024, 77)])
+def test_attention_batch_invariant(H, S, SKV):
     """Image 1's rows of a B=2 launch equal a B=1 launch on image 1 bit for bit (the unit
     kind and split points depend on the key count only)."""
-    torch.manual_seed(S + H)
-    q, k, v = rnd(2 * S, H * 64), rnd(2 * S, H * 64), rnd(2 * S, H * 64)
+    torch.manual_seed(S + H + SKV)
+    q, k, v = rnd(2 * S, H * 64), rnd(2 * SKV, H * 64), rnd(2 * SKV, H * 64)
     o2 = torch.empty_like(q)
-    K.attention(q, k, v, o2, batch=2, heads=H, sq=S, skv=S, scale=0.125)
+    K.attention(q, k, v, o2, batch=2, heads=H, sq=S, skv=SKV, scale=0.125)
     o1 = torch.empty(S, H * 64, dtype=torch.bfloat16, device="cuda")
-    K.attention(q[S:].contiguous(), k[S:].contiguous(), v[S:].contiguous(), o1, batch=1, heads=H, sq=S, skv=S,
-                scale=0.125)
+    K.attention(q[S:].contiguous(), k[SKV:].contiguous(), v[SKV:].contiguous(), o1, batch=1, heads=H, sq=S,
+                skv=SKV, scale=0.125)
     assert torch.equal(o2[S:], o1)
 
 
