@@ -80,6 +80,13 @@ typedef struct hp_gemm_desc {
     float* stats_out;
     const float* ln_stats; int32_t ln_parts; int32_t ln_part_n;
     const float* ln_colsum; float ln_fold_eps;
+    /* GroupNorm partials of the output (gn_part != NULL): for every 128-row block
+     * and 10-column segment, (sum, sum of squares) of the STORED bf16 values as two
+     * floats at gn_part[2 * (idx * (N / 10) + segment)], idx = image * gn_parts +
+     * block within the image, images of gn_rows rows (HP_A_UPCONV: gn_rows = input
+     * pixels per image, blocks phase-major). Requires N % 160 == 0, M % 128 == 0,
+     * no activation; consumed by hp_group_norm_parts. */
+    float* gn_part; int64_t gn_rows; int32_t gn_parts;
 } hp_gemm_desc;
 
 int hp_gemm(const hp_gemm_desc* d, void* stream);
@@ -111,6 +118,15 @@ int hp_attention(const hp_attn_desc* d, void* stream);
 int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_t n, int64_t hw,
                   int32_t groups, float eps, const float* gamma, const float* beta, int32_t silu,
                   void* y, float* stats, void* stream);
+/* GroupNorm(+SiLU) of x [n, hw, c] (bf16) whose statistics the producing GEMMs
+ * left as hp_gemm_desc.gn_part partials: channels [0, c1) from part1 (c1 / 10
+ * segments per partial row), channels [c1, c) from part2 (the second operand of
+ * a channel concat; NULL when c1 == c). hw / 128 partial rows per image. Folds
+ * the partials in fixed order (fp64), writes y [n, hw, c]. One launch, no
+ * grid-wide barrier. Group width c / groups must be a multiple of 10. */
+int hp_group_norm_parts(const void* x, int32_t c, int32_t n, int64_t hw, const float* part1, int32_t c1,
+                        const float* part2, int32_t groups, float eps, const float* gamma,
+                        const float* beta, int32_t silu, void* y, void* stream);
 /* LayerNorm over rows of bf16 [rows, c]; optional gamma/beta (fp32);
  * optional adaLN modulation y = norm*(1+scale[b]) + shift[b] with
  * b = row / rows_per_batch, scale/shift fp32 rows of length c (stride ldm). */

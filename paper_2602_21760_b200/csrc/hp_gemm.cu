@@ -79,6 +79,10 @@ struct GemmParams {
   bool vec256;                     // output (and residual) rows 32-byte aligned: 256-bit accesses
   float2* stats_out;
   const float2* ln_stats; int ln_parts; float ln_part_n; const float* ln_colsum; float ln_fold_eps;
+  // GroupNorm partials of the output (kEpiGn): (sum, sum of squares) per 128-row block and
+  // 10-column segment at gn_part[idx * gn_ld + segment], idx = image * gn_P + block of the
+  // image (upconv: phase-major within the image); gn_rows = rows per image per batch slice
+  float2* gn_part; int gn_rows; int gn_P; int gn_ld;
 };
 
 // mean / rstd of one row from its (mean, M2) partials, Chan's pairwise update in
@@ -117,7 +121,39 @@ __device__ __forceinline__ void prefetch_res_row(const GemmParams& p, int bt, in
 }
 
 // epilogue flavours (one template instance each, chosen per launch)
-constexpr int kEpiPlain = 0, kEpiStats = 1, kEpiFold = 2;
+constexpr int kEpiPlain = 0, kEpiStats = 1, kEpiFold = 2, kEpiGn = 3;
+constexpr int kGnSeg = 10;     // GroupNorm partial segment (columns): divides every SDXL group width
+
+// kEpiGn: GroupNorm partials of the STORED bf16 values, one (sum, sum of squares) per
+// 10-column segment over the CTA's 128 rows. Each thread runs its row through the segment
+// in column order (carried across 32-column chunks), a warp sums its 32 rows with a fixed
+// xor tree, the four warps' sums meet in shared memory in fixed order: a segment's value
+// depends on its columns and its 128-row block only, not on block_n, split-K or the rest
+// of the batch (hp_group_norm_parts folds them per image: batch-invariant). PH = the
+// 32-column chunk's index mod 5 (its first column mod 10 is 2 PH; tiles start at
+// multiples of 160); seg0 = the tile segment of the chunk's 5-chunk group.
+template <int PH>
+__device__ __forceinline__ void gn_chunk(const uint32_t (&w)[16], float& s1, float& s2, float2* gsm, int quarter,
+                                         int lane, int seg0) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float2 f = unpack_bf16(w[j >> 1]);
+    const float v = (j & 1) ? f.y : f.x;
+    s1 += v;
+    s2 = fmaf(v, v, s2);
+    if ((32 * PH + j) % kGnSeg == kGnSeg - 1) {
+      float a = s1, b = s2;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      if (lane == 0) gsm[quarter * 32 + seg0 + (32 * PH + j) / kGnSeg] = make_float2(a, b);
+      s1 = 0.f;
+      s2 = 0.f;
+    }
+  }
+}
 
 template <int BN>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& b, int& m0, int& n0) {
@@ -233,7 +269,7 @@ template <int BN, int EPI, int AM = kAmAny>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
                                               int lane, const float* sb, float* row_stats, const float* scs,
                                               float f_mean, float f_rstd, int c_begin = 0, int c_count = BN,
-                                              const float4* red = nullptr) {
+                                              const float4* red = nullptr, float2* gsm = nullptr, int gn_idx = 0) {
   constexpr bool kLean = AM != kAmAny;
   const bool v8 = kLean ? true : p.vec256;
   const int row = m0 + quarter * 32 + lane;
@@ -285,6 +321,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
   uint32_t rn[16];
   float st_sum = 0.f, st_sq = 0.f;            // LayerNorm partials of the stored (bf16) row
   float sh_k = 0.f, sh_s1 = 0.f, sh_s2 = 0.f;   // stats_out: sums shifted by the segment's first value
+  float g_s1 = 0.f, g_s2 = 0.f;                 // kEpiGn: the open 10-column segment of this row
   if (has_res) ld_row64(res_row, rn, v8);
   const long long drow = d_row_off(p, row);
   const int nch = c_count / 32;
@@ -370,6 +407,16 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     for (int q = 0; q < 16; ++q) w[q] = pack_bf16(lo2(v2[q]), hi2(v2[q]));
     if (kLean || p.probe_noepi != 2) st_row64(p.d + drow + col, w, v8);
     else if (w[0] == 0x7fc07fc0u) p.d[row] = __float2bfloat16(0.f);          // keep the math live
+    if constexpr (EPI == kEpiGn) {
+      const int q5 = c / 5;
+      switch (c - 5 * q5) {
+        case 0: gn_chunk<0>(w, g_s1, g_s2, gsm, quarter, lane, 16 * q5); break;
+        case 1: gn_chunk<1>(w, g_s1, g_s2, gsm, quarter, lane, 16 * q5); break;
+        case 2: gn_chunk<2>(w, g_s1, g_s2, gsm, quarter, lane, 16 * q5); break;
+        case 3: gn_chunk<3>(w, g_s1, g_s2, gsm, quarter, lane, 16 * q5); break;
+        default: gn_chunk<4>(w, g_s1, g_s2, gsm, quarter, lane, 16 * q5); break;
+      }
+    }
     if constexpr (EPI == kEpiStats) {
       if ((c * 32) % kStatW == 0) sh_k = unpack_bf16(w[0]).x;
 #pragma unroll
@@ -401,7 +448,18 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
     row_stats[0] = st_sum;
     row_stats[1] = st_sq;
   }
-
+  if constexpr (EPI == kEpiGn) {
+    // the tile's segments: the four row quarters summed in fixed order (epilogue warps only)
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    const int t = quarter * 32 + lane;
+    if (t < c_count / kGnSeg) {
+      const int sg = c_begin / kGnSeg + t;
+      const float2 a = gsm[sg], b = gsm[32 + sg], c2 = gsm[64 + sg], d2 = gsm[96 + sg];
+      p.gn_part[(long long)gn_idx * p.gn_ld + n0 / kGnSeg + sg] =
+          make_float2(((a.x + b.x) + c2.x) + d2.x, ((a.y + b.y) + c2.y) + d2.y);
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+  }
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -696,6 +754,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAcc);
   float* sbias = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);   // [2][BN]
   float* scolsum = sbias + 2 * BN;                                               // [2][BN]
+  float2* gsm = reinterpret_cast<float2*>(scolsum + 2 * BN);                    // [4][32] GroupNorm partials
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef HP_GEMM_TRACE
@@ -880,14 +939,24 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       if (et == 0 && local == 0) HP_GTRACE(6);
       tc_fence_after();
       const uint32_t t_acc = tmem_base + acc * BN;
+      const int gn_idx = p.gn_part ? (m0 / p.gn_rows) * p.gn_P + bt * (p.gn_rows / BM) + (m0 % p.gn_rows) / BM : 0;
       if constexpr (EP != kEpRuntime) {            // one epilogue flavour compiled in
         GemmParams q = p;                          // batched: this tile's image (or phase)
         if (p.batch > 1) batch_offsets(q, bt);
-        epilogue_tile<BN, EP, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
+        epilogue_tile<BN, EP, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd, 0, BN, nullptr,
+                                  gsm, gn_idx);
       } else if (p.batch > 1) {
         GemmParams q = p;
         batch_offsets(q, bt);
-        epilogue_tile<BN, kEpiPlain, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
+        bool done = false;
+        if constexpr (BN % 160 == 0) {             // the upsampler's GroupNorm partials
+          if (p.gn_part) {
+            epilogue_tile<BN, kEpiGn, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f, 0, BN,
+                                          nullptr, gsm, gn_idx);
+            done = true;
+          }
+        }
+        if (!done) epilogue_tile<BN, kEpiPlain, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, nullptr, 0.f, 1.f);
       } else if (fold) {
         epilogue_tile<BN, kEpiFold, AM>(p, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd);
       } else if (p.stats_out) {
@@ -936,6 +1005,7 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   float* sbias = reinterpret_cast<float*>(smem + STAGES * kStageBytes + 256);   // [BN]
   float* scolsum = sbias + BN;                                                   // [BN]
+  float2* gsm = reinterpret_cast<float2*>(scolsum + BN);                        // [4][32] GroupNorm partials
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef HP_GEMM_TRACE
@@ -1103,8 +1173,9 @@ gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const int quarter = warp & 3;
     const float* sb = (p.bias != nullptr || p.bias2 != nullptr) ? sbias : nullptr;
     const float4* red = reinterpret_cast<const float4*>(smA);
+    const int gn_idx = p.gn_part ? (m0 / p.gn_rows) * p.gn_P + (m0 % p.gn_rows) / BM : 0;
     epilogue_tile<BN, EP, kAmNone>(p, tmem_base, m0, n0, quarter, lane, sb, nullptr, scolsum, f_mean, f_rstd, h0,
-                                   kSubN, red);
+                                   kSubN, red, gsm, gn_idx);
   }
   __syncwarp();
   tc_fence_before();
@@ -1198,7 +1269,8 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& 
 
 template <int BN, int STAGES, int AM, int EP = kEpRuntime>
 int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
-  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + (BN / 2) * BK * 2) + 256 + 4 * BN * sizeof(float);
+  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + (BN / 2) * BK * 2) + 256 + 4 * BN * sizeof(float) +
+                         4 * 32 * sizeof(float2);
   static_assert(smem <= 227 * 1024, "pair GEMM smem");
   static bool attr_set = false;
   if (!attr_set) {
@@ -1230,7 +1302,8 @@ int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPar
 
 template <int STAGES, int EP>
 int launch_gemm_splitk(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, cudaStream_t st) {
-  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + 160 * BK * 2) + 256 + 2 * 320 * sizeof(float);
+  constexpr size_t smem = 1024 + (size_t)STAGES * (kABytes + 160 * BK * 2) + 256 + 2 * 320 * sizeof(float) +
+                         4 * 32 * sizeof(float2);
   static_assert(smem <= 227 * 1024, "split-K GEMM smem");
   static bool attr_set = false;
   if (!attr_set) {
@@ -1289,7 +1362,7 @@ bool splitk_ok(int64_t M, int64_t N, int64_t K, int act, int batch, int mode) {
 // M > 128) times the per-tile time, k-blocks x N / (measured main-loop rate of that
 // width), plus exposed epilogues (~5 k-blocks' worth each). 320 keeps one accumulator
 // (no epilogue/MMA overlap), so each of its tiles exposes one.
-int pick_bn(int64_t M, int64_t N, int64_t K, int act, int batch = 1, int mode = HP_A_PLAIN) {
+int pick_bn(int64_t M, int64_t N, int64_t K, int act, int batch = 1, int mode = HP_A_PLAIN, bool gn = false) {
   const int cands[5] = {320, 256, 160, 128, 64};
   int best = 0;
   double best_cost = 1e30;
@@ -1303,6 +1376,7 @@ int pick_bn(int64_t M, int64_t N, int64_t K, int act, int batch = 1, int mode = 
   if (pair && splitk_ok(M, N, K, act, batch, mode)) return 320;   // fixed choice (see splitk_ok)
   for (int bn : cands) {
     if (N % bn) continue;
+    if (gn && bn % 160) continue;                                  // GroupNorm partials: 160-column tile groups
     if (bn > 256 && (!pair || act == HP_ACT_GEGLU)) continue;    // 320 = two N=160 MMAs, pair kernel only
     if (act == HP_ACT_GEGLU && bn != 256 && bn != 128) continue;
     const int64_t tiles = mt * (N / bn);
@@ -1336,8 +1410,15 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   num_sms();
   const bool upconv = d->a_mode == HP_A_UPCONV;
   const int nbatch = upconv ? 4 : (d->batch > 1 ? d->batch : 1);
-  const int bn = d->block_n ? d->block_n : pick_bn(d->M * nbatch, d->N, d->K, d->act, nbatch, d->a_mode);
+  const bool gn = d->gn_part != nullptr;
+  const int bn = d->block_n ? d->block_n : pick_bn(d->M * nbatch, d->N, d->K, d->act, nbatch, d->a_mode, gn);
   if (bn == 0 || d->N % bn) return HP_ERR_UNSUPPORTED;
+  // GroupNorm partials: CTA-pair or split-K kernel, whole 128-row blocks of one image,
+  // 160-multiple tiles (segments never straddle a tile), plain epilogue values
+  if (gn && (bn % 160 || d->M % BM || (d->alpha != 0.0f && d->alpha != 1.0f) || d->M <= BM || !pair_enabled() || d->act != HP_ACT_NONE || d->ln_y ||
+             d->stats_out || d->ln_stats || d->colscale || d->gn_rows <= 0 || d->gn_rows % BM ||
+             d->M % d->gn_rows || d->gn_parts <= 0 || (reinterpret_cast<uintptr_t>(d->gn_part) & 7)))
+    return HP_ERR_UNSUPPORTED;
   if (d->act == HP_ACT_GEGLU && (bn % 64)) return HP_ERR_UNSUPPORTED;
   const int64_t n_out = d->act == HP_ACT_GEGLU ? d->N / 2 : d->N;
   if ((d->ldd % 8) || (d->residual && (d->ldr % 8)) || (n_out % 32)) return HP_ERR_UNSUPPORTED;
@@ -1391,6 +1472,8 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
         (reinterpret_cast<uintptr_t>(d->ln_stats) & 7) || (reinterpret_cast<uintptr_t>(d->ln_colsum) & 15))
       return HP_ERR_UNSUPPORTED;
   }
+  p.gn_part = reinterpret_cast<float2*>(d->gn_part);
+  p.gn_rows = (int)d->gn_rows; p.gn_P = d->gn_parts; p.gn_ld = (int)(d->N / kGnSeg);
   p.a_bs = d->a_bstride; p.d_bs = d->d_bstride; p.r_bs = d->r_bstride; p.cs_bs = d->cs_bstride;
   if (upconv) {      // output phases (py, px) of the 2x grid: see HP_A_UPCONV
     p.ldd = 2 * d->ldd;
@@ -1457,10 +1540,13 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   const bool lean2 = p.alpha == 1.0f && p.vec256 && p.probe_noepi == 0 && !p.ln_stats && !p.stats_out &&
                      !p.ln_mode && (bn == 256 || bn == 128 || bn == 64) &&
                      ((d->act == HP_ACT_GELU && !p.colscale) || (d->act == HP_ACT_NONE && (p.colscale || p.batch > 1)));
+  // GroupNorm partials: the lean instances (batch 1) or the batched runtime branch (upconv)
+  if (p.gn_part && (!pair || (p.batch == 1 && !lean))) return HP_ERR_UNSUPPORTED;
   if (pair && lean && bn == 320 && splitk_ok(d->M, d->N, d->K, d->act, p.batch, d->a_mode)) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
     return p.ln_stats ? launch_gemm_splitk<5, kEpiFold>(ta, tb, p, st)
          : p.stats_out ? launch_gemm_splitk<5, kEpiStats>(ta, tb, p, st)
+         : p.gn_part ? launch_gemm_splitk<5, kEpiGn>(ta, tb, p, st)
                        : launch_gemm_splitk<5, kEpiPlain>(ta, tb, p, st);
   }
   if (pair) {
@@ -1499,6 +1585,10 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
         case 64: return launch_gemm_pair<64, 8, kAmAny>(ta, tb, p, st);
         default: return HP_ERR_UNSUPPORTED;
       }
+    }
+    if (p.gn_part) {
+      if (bn == 320) return launch_gemm_pair<320, 5, kAmNone, kEpiGn>(ta, tb, p, st);
+      return launch_gemm_pair<160, 7, kAmNone, kEpiGn>(ta, tb, p, st);
     }
     const int ep = p.ln_stats ? kEpiFold : (p.stats_out ? kEpiStats : kEpiPlain);
 #define HP_PAIR_LEAN(BN_, ST_)                                                                          \

@@ -170,6 +170,12 @@ gn_stats_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
 // xa / xb: image n's first pixel row of each input (or a shared-memory chunk copy
 // whose row 0 is pixel `src_p0`); y: the output image base. Pixels p_first + r,
 // stepping p_mul * rows, up to p_end (image pixel indices).
+__device__ __forceinline__ void gn_normalise(const bf16* xa, int c1, const bf16* xb, int c2, int groups,
+                                             const float* __restrict__ gamma, const float* __restrict__ beta,
+                                             int do_silu, bf16* __restrict__ yo, int64_t src_p0, int64_t p_first,
+                                             int64_t p_mul, int64_t p_end, const float* s_mean, const float* s_rstd,
+                                             float* sa, float* sb);
+
 __device__ __forceinline__ void gn_apply_block(const bf16* xa, int c1, const bf16* xb, int c2, int64_t hw, int groups,
                                                int splits, const float* __restrict__ part, float eps,
                                                const float* __restrict__ gamma, const float* __restrict__ beta,
@@ -177,7 +183,6 @@ __device__ __forceinline__ void gn_apply_block(const bf16* xa, int c1, const bf1
                                                int64_t p_first, int64_t p_mul, int64_t p_end, float* s_mean,
                                                float* s_rstd, double* s_pa, double* s_pb, float* sa, float* sb) {
   const int C = c1 + c2;
-  const int V = C / 8;
   const int cg = C / groups;
   {
     // fold the per-split partials: kGnThreads/groups threads per group, fixed order;
@@ -216,6 +221,19 @@ __device__ __forceinline__ void gn_apply_block(const bf16* xa, int c1, const bf1
     }
   }
   __syncthreads();
+  gn_normalise(xa, c1, xb, c2, groups, gamma, beta, do_silu, yo, src_p0, p_first, p_mul, p_end, s_mean, s_rstd, sa,
+               sb);
+}
+
+// y = x * sa[c] + sb[c] (+ SiLU) from the per-group mean / rstd (see gn_apply_block)
+__device__ __forceinline__ void gn_normalise(const bf16* xa, int c1, const bf16* xb, int c2, int groups,
+                                             const float* __restrict__ gamma, const float* __restrict__ beta,
+                                             int do_silu, bf16* __restrict__ yo, int64_t src_p0, int64_t p_first,
+                                             int64_t p_mul, int64_t p_end, const float* s_mean, const float* s_rstd,
+                                             float* sa, float* sb) {
+  const int C = c1 + c2;
+  const int V = C / 8;
+  const int cg = C / groups;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     const int g = c / cg;
     const float a = s_rstd[g] * gamma[c];
@@ -287,6 +305,127 @@ gn_apply_kernel(const bf16* __restrict__ x1, int c1, const bf16* __restrict__ x2
                  part, eps, gamma, beta, do_silu, y + (int64_t)n * hw * (c1 + c2), n, 0,
                  (int64_t)blockIdx.x * (kGnThreads / min((c1 + c2) / 8, kGnThreads)), gridDim.x, hw, s_mean, s_rstd,
                  s_pa, s_pb, sa, sb);
+}
+
+// GroupNorm from the producing GEMMs' partials (hp_gemm gn_part): no statistics pass
+// and no grid-wide barrier. grid (chunks, n); each CTA folds its image's partials per
+// group in fixed order (kGnThreads / groups threads per group over (segment, block)
+// items, fp64, then the group's threads in order) and normalises its pixels. Channels
+// [0, c1) take their segments from part1, [c1, C) from part2 (a concat's second input).
+constexpr int kGnPartRows = 128;     // rows per partial (hp_gemm's 128-row block)
+constexpr int kGnPartSeg = 10;       // columns per partial segment
+constexpr int kGnPartsMaxThreads = 512;
+#ifndef HP_GN_PARTS_DEPTH
+#define HP_GN_PARTS_DEPTH 4
+#endif
+#ifndef HP_GN_PARTS_THREADS
+#define HP_GN_PARTS_THREADS 256
+#endif
+#ifndef HP_GN_PARTS_CTAS_PER_SM
+#define HP_GN_PARTS_CTAS_PER_SM 2
+#endif
+constexpr int kGnPartsDepth = HP_GN_PARTS_DEPTH;    // 16-byte loads in flight per thread
+__global__ void __launch_bounds__(kGnPartsMaxThreads)
+gn_parts_kernel(const bf16* __restrict__ x, int C, int64_t hw, const float2* __restrict__ part1, int c1,
+                const float2* __restrict__ part2, int groups, float eps, const float* __restrict__ gamma,
+                const float* __restrict__ beta, int do_silu, bf16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float s_mean[64], s_rstd[64];
+  __shared__ double s_pa[kGnThreads], s_pb[kGnThreads];
+  __shared__ __align__(16) float sa[kMaxC], sb[kMaxC];
+  const int n = blockIdx.y;
+  // thread -> fixed 8-channel vector j = t % V (its scale / shift stay in registers), pixels
+  // p0, p0 + step, ...; the block is a whole number of pixel rows of V threads (launcher)
+  const int V = C / 8, rows = (int)blockDim.x / V;
+  const int r = threadIdx.x / V, j = threadIdx.x % V, ch = j * 8;
+  const int64_t step = (int64_t)gridDim.x * rows, p0 = (int64_t)blockIdx.x * rows + r;
+  const bf16* xi = x + (int64_t)n * hw * C + ch;
+  bf16* yi = y + (int64_t)n * hw * C + ch;
+  // the thread's first kGnPartsDepth pixels are in flight during the fold
+  uint4 pre[kGnPartsDepth];
+#pragma unroll
+  for (int k = 0; k < kGnPartsDepth; ++k)
+    if (p0 + k * step < hw) pre[k] = *reinterpret_cast<const uint4*>(xi + (p0 + k * step) * C);
+  const int P = (int)(hw / kGnPartRows);
+  const int cg = C / groups, sg = cg / kGnPartSeg;
+  const int ns1 = c1 / kGnPartSeg, ns2 = (C - c1) / kGnPartSeg;
+  // per threads per group fold (the first per * groups threads of the block)
+  const int per = min((int)blockDim.x, kGnThreads) / groups;
+  const int g = threadIdx.x % groups, k = threadIdx.x / groups;
+  if (threadIdx.x < per * groups) {
+    double a = 0.0, b = 0.0;
+    if (k < per) {
+      // items of group g: segment g * sg + it / P, block it % P; eight loads per round
+      // (zeros past the end: exact), summed in item order
+      const int items = sg * P;
+      for (int i = k; i < items; i += 8 * per) {
+        float2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int it = i + u * per;
+          v[u] = make_float2(0.f, 0.f);
+          if (it < items) {
+            const int sgi = g * sg + it / P, rb = it % P;
+            v[u] = sgi < ns1 ? __ldg(part1 + ((int64_t)n * P + rb) * ns1 + sgi)
+                             : __ldg(part2 + ((int64_t)n * P + rb) * ns2 + (sgi - ns1));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { a += (double)v[u].x; b += (double)v[u].y; }
+      }
+    }
+    s_pa[threadIdx.x] = a;
+    s_pb[threadIdx.x] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x < groups) {
+    double ta = 0.0, tb = 0.0;
+    for (int kk = 0; kk < per; ++kk) { ta += s_pa[kk * groups + threadIdx.x]; tb += s_pb[kk * groups + threadIdx.x]; }
+    const double cnt = (double)hw * cg;
+    const double mean = ta / cnt;
+    double var = tb / cnt - mean * mean;
+    if (var < 0) var = 0;
+    s_mean[threadIdx.x] = (float)mean;
+    s_rstd[threadIdx.x] = (float)(1.0 / sqrt(var + (double)eps));
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float sc = s_rstd[c / cg] * gamma[c];
+    sa[c] = sc;
+    sb[c] = beta[c] - s_mean[c / cg] * sc;
+  }
+  __syncthreads();
+  float av[8], bv[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { av[q] = sa[ch + q]; bv[q] = sb[ch + q]; }
+  auto emit = [&](const uint4& u, int64_t p) {
+    const __nv_bfloat162* hv = reinterpret_cast<const __nv_bfloat162*>(&u);
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(hv[i]);
+      v[2 * i] = f.x; v[2 * i + 1] = f.y;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float o = fmaf(v[i], av[i], bv[i]);
+      v[i] = do_silu ? silu_fast(o) : o;
+    }
+    store8(yi + p * C, v);
+  };
+#pragma unroll
+  for (int q = 0; q < kGnPartsDepth; ++q)
+    if (p0 + q * step < hw) emit(pre[q], p0 + q * step);
+  int64_t p = p0 + kGnPartsDepth * step;
+  for (; p + (kGnPartsDepth - 1) * step < hw; p += kGnPartsDepth * step) {   // all loads in flight
+    uint4 u[kGnPartsDepth];
+#pragma unroll
+    for (int q = 0; q < kGnPartsDepth; ++q) u[q] = *reinterpret_cast<const uint4*>(xi + (p + q * step) * C);
+#pragma unroll
+    for (int q = 0; q < kGnPartsDepth; ++q) emit(u[q], p + q * step);
+  }
+  for (; p < hw; p += step) emit(*reinterpret_cast<const uint4*>(xi + p * C), p);
 }
 
 // Single-launch GroupNorm: the statistics CTAs of an image meet at a
@@ -1086,6 +1225,39 @@ int hp_group_norm(const void* x1, int32_t c1, const void* x2, int32_t c2, int32_
                                                           static_cast<const bf16*>(x2), x2 ? c2 : 0, hw, groups,
                                                           splits, stats, eps, gamma, beta, do_silu,
                                                           static_cast<bf16*>(y));
+  if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
+  return ok();
+}
+
+int hp_group_norm_parts(const void* x, int32_t c, int32_t n, int64_t hw, const float* part1, int32_t c1,
+                        const float* part2, int32_t groups, float eps, const float* gamma, const float* beta,
+                        int32_t do_silu, void* y, void* stream) {
+  if (!x || !y || !gamma || !beta || !part1 || (c1 < c && !part2)) return HP_ERR_PARAMETER;
+  if (c % 8 || c > kMaxC || groups < 1 || groups > 64 || c % groups || (c / groups) % kGnPartSeg ||
+      c1 % kGnPartSeg || c1 < 1 || c1 > c || n < 1 || hw < kGnPartRows || hw % kGnPartRows)
+    return HP_ERR_SHAPE;
+  if (!a16(x) || !a16(y) || (reinterpret_cast<uintptr_t>(part1) & 7) || (reinterpret_cast<uintptr_t>(part2) & 7))
+    return HP_ERR_UNSUPPORTED;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  // block = whole pixel rows of V = c / 8 threads (~256); every CTA folds its image's
+  // partials first, so the grid stays near two CTAs per SM (and >= 4 pixels per thread)
+  const int V = c / 8;
+  const int rows = V >= HP_GN_PARTS_THREADS ? 1 : (HP_GN_PARTS_THREADS + V / 2) / V;
+  const int threads = rows * V;
+  if (threads > kGnPartsMaxThreads) return HP_ERR_SHAPE;
+  int chunks = (int)((hw + kGnPartsDepth * rows - 1) / (kGnPartsDepth * rows));
+  const int cap = (HP_GN_PARTS_CTAS_PER_SM * sms + n - 1) / n;
+  if (chunks > cap) chunks = cap;
+  hp_launch_pdl(gn_parts_kernel, dim3(chunks, n), dim3(threads), 0, static_cast<cudaStream_t>(stream),
+                static_cast<const bf16*>(x), (int)c, hw, reinterpret_cast<const float2*>(part1), (int)c1,
+                reinterpret_cast<const float2*>(part2), (int)groups, eps, gamma, beta, (int)do_silu,
+                static_cast<bf16*>(y));
   if (cudaPeekAtLastError() != cudaSuccess) return HP_ERR_CUDA;
   return ok();
 }

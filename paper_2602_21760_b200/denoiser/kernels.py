@@ -53,6 +53,7 @@ class HpGemmDesc(C.Structure):
         ("ln_gamma", _VP), ("ln_beta", _VP), ("ln_eps", _F32), ("ln_y", _VP), ("ldy", _I64),
         ("stats_out", _VP),
         ("ln_stats", _VP), ("ln_parts", _I32), ("ln_part_n", _I32), ("ln_colsum", _VP), ("ln_fold_eps", _F32),
+        ("gn_part", _VP), ("gn_rows", _I64), ("gn_parts", _I32),
     ]
 
 
@@ -73,6 +74,7 @@ SIGNATURES = {
     "hp_gemm_stats_block_n": (_I32, [_I64, _I64, _I64]),
     "hp_attention": (C.c_int, [C.POINTER(HpAttnDesc), _VP]),
     "hp_group_norm": (C.c_int, [_VP, _I32, _VP, _I32, _I32, _I64, _I32, _F32, _VP, _VP, _I32, _VP, _VP, _VP]),
+    "hp_group_norm_parts": (C.c_int, [_VP, _I32, _I32, _I64, _VP, _I32, _VP, _I32, _F32, _VP, _VP, _I32, _VP, _VP]),
     "hp_layer_norm": (C.c_int, [_VP, _I64, _I32, _F32, _VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP]),
     "hp_layer_norm_joint": (C.c_int, [_VP, _I64, _I32, _F32, _VP, _VP, _VP, _VP, _I64, _I64, _I64, _VP, _VP]),
     "hp_silu": (C.c_int, [_VP, _VP, _I64, _VP]),
@@ -131,13 +133,37 @@ class FoldedLN:
         self.eps = float(eps)
 
 
+GN_SEG, GN_ROWS = 10, 128      # GroupNorm partial: 10 columns x 128 rows (hp_gemm gn_part)
+
+
+class GnParts:
+    """GroupNorm partials a GEMM left for its output (``gemm(gn_hw=...)``): (sum, sum of
+    squares) per 128-row block and 10-column segment; ``group_norm`` folds them instead
+    of re-reading the tensor for statistics. ``parts2`` / ``c1``: a channel concat whose
+    second input carries its own partials."""
+
+    def __init__(self, buf, hw, c, parts2=None, c1=None):
+        self.buf, self.hw, self.c = buf, hw, c
+        self.parts2, self.c1 = parts2, c if c1 is None else c1
+
+
+def gn_parts_ok(M, N, hw):
+    """Shapes whose producing GEMM can record GroupNorm partials."""
+    return N % 160 == 0 and hw % GN_ROWS == 0 and M % hw == 0 and M > GN_ROWS
+
+
+def _gn_buf(M, N, dev):
+    return torch.empty((M // GN_ROWS) * (N // GN_SEG) * 2, dtype=torch.float32, device=dev)
+
+
 def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, act=ACT_NONE,
-         alpha=1.0, block_n=0, conv=None, colscale=None, ln=None, stats_out=None, ln_fold=None):
+         alpha=1.0, block_n=0, conv=None, colscale=None, ln=None, stats_out=None, ln_fold=None, gn_hw=None):
     """out[M, N'] = residual + colscale * act(alpha * A @ W^T + bias).
     ``conv=(n, h, w, c, stride)`` reads A as NHWC. ``stats_out`` (RowStats):
     also record the output rows' LayerNorm partials; ``ln_fold=(RowStats,
     FoldedLN)``: A is un-normalised, LN applied in the epilogue (w, bias must
-    be the FoldedLN's)."""
+    be the FoldedLN's). ``gn_hw``: rows per image; also record GroupNorm
+    partials of the output (``out.hp_gn``, a GnParts) when the shape allows."""
     lib = N.load()
     _bf16(a, "A")
     _bf16(w, "W")
@@ -213,7 +239,15 @@ def gemm(a, w, *, out=None, bias=None, bias2=None, bias2_div=1, residual=None, a
         st, fold = ln_fold
         d.ln_stats, d.ln_parts, d.ln_part_n = _p(st.buf), st.parts, st.part_n
         d.ln_colsum, d.ln_fold_eps = _p(fold.colsum), fold.eps
+    gp = None
+    if gn_hw is not None and act == ACT_NONE and gn_parts_ok(M, Nn, gn_hw):
+        gp = GnParts(_gn_buf(M, Nn, a.device), gn_hw, Nn)
+        d.gn_part, d.gn_rows, d.gn_parts = _p(gp.buf), gn_hw, gn_hw // GN_ROWS
     check(lib.hp_gemm(C.byref(d), _s()), f"hp_gemm M={M} N={Nn} K={K}")
+    if gp is not None:
+        out.hp_gn = gp
+    elif getattr(out, "hp_gn", None) is not None:
+        del out.hp_gn                                # overwritten in place: its partials are stale
     return out
 
 
@@ -233,10 +267,21 @@ def attention(q, k, v, out, *, batch, heads, sq, skv, scale, q_col0=0, k_col0=0,
 
 def group_norm(x, n, hw, c, gamma, beta, *, groups=32, eps=1e-5, silu=False, x2=None, c2=0, out=None,
                stats=None):
+    """GroupNorm(+SiLU) over NHWC rows. When x carries its producer's GroupNorm partials
+    (``x.hp_gn``) for this very shape, one launch folds them (no statistics pass);
+    otherwise the statistics are computed here (hp_group_norm)."""
     lib = N.load()
     C_ = c + (c2 if x2 is not None else 0)
     if out is None:
         out = torch.empty((n * hw, C_), dtype=torch.bfloat16, device=x.device)
+    gp = getattr(x, "hp_gn", None)
+    if (gp is not None and x2 is None and gp.hw == hw and gp.c == c and x.shape[0] == n * hw
+            and (c // groups) % GN_SEG == 0 and x.is_contiguous()):
+        check(lib.hp_group_norm_parts(_p(x), c, n, hw, _p(gp.buf), gp.c1,
+                                      _p(gp.parts2.buf) if gp.parts2 is not None else None, groups, eps,
+                                      _p(gamma), _p(beta), int(silu), _p(out), _s()),
+              f"hp_group_norm_parts n={n} hw={hw} C={c}")
+        return out
     if stats is None:
         stats = torch.empty(2 * n * groups * 256, dtype=torch.float32, device=x.device)
     check(lib.hp_group_norm(_p(x), c, _p(x2), c2, n, hw, groups, eps, _p(gamma), _p(beta), int(silu),
@@ -306,9 +351,10 @@ def upconv_weights(w3):
     return torch.cat(ph, dim=0).to(torch.bfloat16).contiguous()
 
 
-def upsample_conv(x, n, h, w, c, w4, bias=None, out=None):
+def upsample_conv(x, n, h, w, c, w4, bias=None, out=None, gn=False):
     """conv3x3(nearest_upsample_2x(x)) in one tensor-core launch (HP_A_UPCONV):
-    x [n*h*w, c] NHWC low-res, w4 = upconv_weights(...) -> [n*2h*2w, co]."""
+    x [n*h*w, c] NHWC low-res, w4 = upconv_weights(...) -> [n*2h*2w, co].
+    ``gn``: also record the output's GroupNorm partials (``out.hp_gn``)."""
     lib = N.load()
     _bf16(x, "A")
     _bf16(w4, "W")
@@ -325,7 +371,14 @@ def upsample_conv(x, n, h, w, c, w4, bias=None, out=None):
     d.M, d.N, d.K = n * h * w, co, 4 * c
     d.bias = _p(bias)
     d.alpha = 1.0
+    gp = None
+    if gn and gn_parts_ok(n * 4 * h * w, co, 4 * h * w) and (h * w) % GN_ROWS == 0:
+        # partials per output image: 4 phases x (h*w / 128) blocks, phase-major
+        gp = GnParts(_gn_buf(n * 4 * h * w, co, x.device), 4 * h * w, co)
+        d.gn_part, d.gn_rows, d.gn_parts = _p(gp.buf), h * w, 4 * h * w // GN_ROWS
     check(lib.hp_gemm(C.byref(d), _s()), f"hp_gemm upconv n={n} {h}x{w} {c}->{co}")
+    if gp is not None:
+        out.hp_gn = gp
     return out
 
 
@@ -337,9 +390,15 @@ def upsample2x(x, n, h, w, c):
 
 
 def concat_channels(a, c1, b, c2, pixels):
+    """[a | b] along channels; when both inputs carry GroupNorm partials of the same
+    image size, the result carries both (``out.hp_gn``: channels [0, c1) from a's)."""
     lib = N.load()
     out = torch.empty((pixels, c1 + c2), dtype=torch.bfloat16, device=a.device)
     check(lib.hp_concat_channels(_p(a), c1, _p(b), c2, pixels, _p(out), _s()), "hp_concat_channels")
+    ga, gb = getattr(a, "hp_gn", None), getattr(b, "hp_gn", None)
+    if (ga is not None and gb is not None and ga.parts2 is None and gb.parts2 is None and ga.hw == gb.hw
+            and ga.c == c1 and gb.c == c2):
+        out.hp_gn = GnParts(ga.buf, ga.hw, c1 + c2, parts2=gb, c1=c1)
     return out
 
 

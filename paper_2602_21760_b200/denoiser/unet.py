@@ -6,6 +6,10 @@ kernels' layouts, accumulation fp32 in TMEM. Every op is one of our kernels:
   ResBlock      GN+SiLU -> conv3x3 (implicit GEMM; epilogue: bias + per-image
                 time-embedding bias) -> GN+SiLU -> conv3x3 (epilogue: bias +
                 residual = identity or 1x1-conv shortcut)
+  GroupNorm     statistics come from the producing GEMM's epilogue (per 128-row
+                block and 10-channel segment partials, ``gemm(gn_hw=)``), so a
+                GroupNorm is one normalise pass (``hp_group_norm_parts``); tensors
+                without partials (stage boundaries) take the two-pass path
   Transformer   GN -> proj_in GEMM -> [LN -> fused QKV GEMM -> attention ->
                 out GEMM(+residual) -> LN -> Q GEMM -> cross-attention over
                 per-run cached K/V -> out GEMM(+residual) -> LN -> GEGLU GEMM
@@ -73,7 +77,7 @@ class _UpConv(_Conv):
     def up(self, x, n, h, w):
         """x: [n*h*w, ci] low-res -> [n*2h*2w, co]"""
         if n * h * w > 128:                    # CTA-pair kernel (M > 128 rows)
-            return K.upsample_conv(x, n, h, w, self.ci, self.w4, self.b)
+            return K.upsample_conv(x, n, h, w, self.ci, self.w4, self.b, gn=True)
         return self(K.upsample2x(x, n, h, w, self.ci), n, 2 * h, 2 * w)
 
 
@@ -96,10 +100,10 @@ class _ResBlock:
         ci, co = self.c1.ci, self.c1.co
         hw = h * w
         y = K.group_norm(x, n, hw, ci, self.n1.g, self.n1.b, groups=groups, silu=True, stats=stats)
-        y = self.c1(y, n, h, w, bias2=tb, bias2_div=hw)
+        y = self.c1(y, n, h, w, bias2=tb, bias2_div=hw, gn_hw=hw)
         y = K.group_norm(y, n, hw, co, self.n2.g, self.n2.b, groups=groups, silu=True, stats=stats)
         res = self.short(x, n, h, w) if self.short is not None else x
-        return self.c2(y, n, h, w, residual=res)
+        return self.c2(y, n, h, w, residual=res, gn_hw=hw)
 
 
 class _Block:
@@ -164,7 +168,7 @@ class _Transformer:
         h = self.pin(y, stats_out=rs)
         for b in self.blocks:
             h = b(h, n, hw, ctx_len, key, rs)
-        return self.pout(h, residual=x)
+        return self.pout(h, residual=x, gn_hw=hw)
 
 
 class UNet:
@@ -296,6 +300,11 @@ class UNet:
             h, skips, (hh, ww) = None, [], (H, Wd)
         else:
             n, h, skips, (hh, ww) = state["n"], state["h"], list(state["skips"]), state["hw"]
+            # a stage entry: boundary tensors arrive without their producers' GroupNorm
+            # partials when they crossed GPUs, so drop them here too (fresh views) and the
+            # GroupNorms at every stage entry take the same two-pass path in-process or not
+            h = h.view(h.shape)
+            skips = [t.view(t.shape) for t in skips]
         full_hw = hh * (2 ** self._levels[a]) if a else hh       # latent side length
         rs = self._row_stats(2 * n * full_hw * full_hw * max(c // 4 ** l for l, c in enumerate(s.block_out)) // 64)
         tb_all = self._prologue(t, key) if any(u[0] in ("res",) for u in units[a:b]) else None
@@ -310,7 +319,8 @@ class UNet:
                 record[i] = {"h": h, "skips": list(skips), "hw": (hh, ww), "n": n}
             if kind == "conv_in":
                 xp = K.copy_cols(x.view(n * hh * ww, s.in_channels), self.cin_pad)
-                h = K.gemm(xp, self.conv_in_w, bias=self.conv_in_b, conv=(n, hh, ww, self.cin_pad, 1))
+                h = K.gemm(xp, self.conv_in_w, bias=self.conv_in_b, conv=(n, hh, ww, self.cin_pad, 1),
+                           gn_hw=hh * ww)
                 skips.append(h)
             elif kind == "res":
                 _, where, lvl, j, push = u
@@ -327,7 +337,7 @@ class UNet:
                 if push:
                     skips.append(h)
             elif kind == "ds":
-                h = self.down[u[1]][2](h, n, hh, ww, stride=2)
+                h = self.down[u[1]][2](h, n, hh, ww, stride=2, gn_hw=(hh // 2) * (ww // 2))
                 hh, ww = hh // 2, ww // 2
                 skips.append(h)
             elif kind == "us":

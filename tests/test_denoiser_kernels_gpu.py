@@ -359,3 +359,70 @@ def test_upsample_conv_subpixel(n, h, w, c, co):
     xi = x.float().view(n, h, w, c).permute(0, 3, 1, 2)
     ref = F.conv2d(F.interpolate(xi, scale_factor=2, mode="nearest"), w3.permute(0, 3, 1, 2), bias, padding=1)
     close(out.view(n, 2 * h, 2 * w, co), ref.permute(0, 2, 3, 1))
+
+
+def _gn_ref(full, n, hw, C, g, b, silu):
+    ref = F.group_norm(full.view(n, hw, C).permute(0, 2, 1), 32, g, b, eps=1e-5).permute(0, 2, 1).reshape(n * hw, C)
+    return F.silu(ref) if silu else ref
+
+
+# GroupNorm statistics from the producing GEMM's epilogue (gemm(gn_hw=), hp_group_norm_parts):
+# plain (with residual and per-image bias), split-K (K >= 4096 at N = 1280), 3x3 conv
+# (pair 160 / 320 wide), against torch GroupNorm of the GEMM's own output
+@pytest.mark.parametrize("kind,n,hw,Kd,N", [("plain", 2, 1024, 1280, 1280), ("splitk", 2, 1024, 5120, 1280),
+                                            ("plain", 1, 4096, 640, 640), ("conv", 2, 1024, 640, 1280),
+                                            ("conv", 2, 4096, 320, 640), ("conv", 1, 16384, 320, 320)])
+def test_gemm_groupnorm_partials(kind, n, hw, Kd, N):
+    torch.manual_seed(hw + N + Kd)
+    side = int(math.isqrt(hw))
+    if kind == "conv":
+        x = rnd(n * hw, Kd)
+        w = rnd(N, 9 * Kd, s=(9 * Kd) ** -0.5)
+        kw = dict(conv=(n, side, side, Kd, 1))
+    else:
+        x = rnd(n * hw, Kd)
+        w = rnd(N, Kd, s=Kd ** -0.5)
+        kw = dict(residual=rnd(n * hw, N, s=0.5) + 0.25)
+    bias, b2 = torch.randn(N, device="cuda"), torch.randn(n, N, device="cuda")
+    y = K.gemm(x, w, bias=bias, bias2=b2, bias2_div=hw, gn_hw=hw, **kw)
+    assert getattr(y, "hp_gn", None) is not None
+    g, b = torch.randn(N, device="cuda"), torch.randn(N, device="cuda")
+    out = K.group_norm(y, n, hw, N, g, b, silu=True)
+    close(out, _gn_ref(y.float(), n, hw, N, g, b, True))
+    y.hp_gn = None                                   # the two-pass path on the same tensor
+    close(out, K.group_norm(y, n, hw, N, g, b, silu=True).float(), tol=8e-3)
+
+
+def test_gemm_groupnorm_partials_batch_invariant():
+    """Image 1's partials and normalised output from a B=2 GEMM equal a B=1 GEMM on image 1
+    bit for bit, although M changes (and with it the tile width the GEMM picks)."""
+    torch.manual_seed(7)
+    hw, Kd, N = 1024, 1280, 1280
+    x, w = rnd(2 * hw, Kd), rnd(N, Kd, s=Kd ** -0.5)
+    res = rnd(2 * hw, N)
+    g, b = torch.randn(N, device="cuda"), torch.randn(N, device="cuda")
+    y2 = K.gemm(x, w, residual=res, gn_hw=hw)
+    y1 = K.gemm(x[hw:].contiguous(), w, residual=res[hw:].contiguous(), gn_hw=hw)
+    assert torch.equal(y2[hw:], y1)
+    half = y2.hp_gn.buf.numel() // 2
+    assert torch.equal(y2.hp_gn.buf[half:], y1.hp_gn.buf)
+    assert torch.equal(K.group_norm(y2, 2, hw, N, g, b, silu=True)[hw:], K.group_norm(y1, 1, hw, N, g, b, silu=True))
+
+
+@pytest.mark.parametrize("n,h,w,c,co,c2", [(2, 32, 32, 1280, 1280, 640), (2, 64, 64, 640, 640, 320)])
+def test_groupnorm_partials_upconv_concat(n, h, w, c, co, c2):
+    """Upsampler output (phase-major partials) concatenated with a skip that carries its own
+    partials: one GroupNorm over the concat (groups straddle the two inputs) vs torch."""
+    torch.manual_seed(h + c)
+    x = rnd(n * h * w, c)
+    w3 = torch.randn(co, 3, 3, c, device="cuda") * (9 * c) ** -0.5
+    up = K.upsample_conv(x, n, h, w, c, K.upconv_weights(w3), torch.randn(co, device="cuda"), gn=True)
+    hw = 4 * h * w
+    sk = K.gemm(rnd(n * hw, 320), rnd(c2, 320, s=320 ** -0.5), gn_hw=hw)
+    assert up.hp_gn is not None and sk.hp_gn is not None
+    cat = K.concat_channels(up, co, sk, c2, n * hw)
+    assert cat.hp_gn.parts2 is not None
+    C = co + c2
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda")
+    out = K.group_norm(cat, n, hw, C, g, b, silu=True)
+    close(out, _gn_ref(cat.float(), n, hw, C, g, b, True))
