@@ -1366,8 +1366,9 @@ int pick_bn(int64_t M, int64_t N, int64_t K, int act, int batch = 1, int mode = 
   const int cands[5] = {320, 256, 160, 128, 64};
   int best = 0;
   double best_cost = 1e30;
+  // M = rows per batch slice: every slice rounds up to whole row tiles on its own
   const bool pair = pair_enabled() && M > BM;
-  const int64_t mt = pair ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM;
+  const int64_t mt = (int64_t)(batch > 1 ? batch : 1) * (pair ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM);
   const int sms = (g_num_sms ? g_num_sms : 148) / (pair ? 2 : 1);
   const double kb = (double)((K + BK - 1) / BK);
   // measured main-loop rate per SM relative to block_n 256 (pair kernel, B200): every MMA
@@ -1411,7 +1412,7 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
   const bool upconv = d->a_mode == HP_A_UPCONV;
   const int nbatch = upconv ? 4 : (d->batch > 1 ? d->batch : 1);
   const bool gn = d->gn_part != nullptr;
-  const int bn = d->block_n ? d->block_n : pick_bn(d->M * nbatch, d->N, d->K, d->act, nbatch, d->a_mode, gn);
+  const int bn = d->block_n ? d->block_n : pick_bn(d->M, d->N, d->K, d->act, nbatch, d->a_mode, gn);
   if (bn == 0 || d->N % bn) return HP_ERR_UNSUPPORTED;
   // GroupNorm partials: CTA-pair or split-K kernel, whole 128-row blocks of one image,
   // 160-multiple tiles (segments never straddle a tile), plain epilogue values
