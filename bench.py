@@ -91,7 +91,7 @@ class Workload:
 def _forward_traffic():
     """DRAM bytes of one forward from the committed ncu launch list (profiles/):
     dram__bytes_read.sum + dram__bytes_write.sum summed over the forward's kernels."""
-    path = os.path.join(ROOT, "profiles", "r02", "forward_r2c_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02", "bench_r2d_traffic.json")   # ncu pass over bench.py itself
     try:
         with open(path) as fh:
             t = json.load(fh)
