@@ -341,7 +341,7 @@ attn_single_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 // TMEM (512 cols): S_q [128 q, +128), O_q [256 + 64 q, +64), P_q [384 + 64 q, +64)
 // (P as bf16 pairs, the A operand of the TS-MMA O_q += P_q V).
 // Softmax per block: one TMEM load of the 128-score row, s_free arrive, a depth-10
-// FMNMX3 tree for the row max, exp2 (5/8 MUFU, 3/8 FMA polynomial) with four
+// FMNMX3 tree for the row max, exp2 (6/8 MUFU, 2/8 FMA polynomial) with four
 // partial sums, then the O rescale (lazy, > 2^8 only) once PV(i-1) is done, P
 // stored to TMEM, p_full arrive.
 // Persistent: one CTA per SM walks work units (PAIR: 256 queries of one (head,
