@@ -15,3 +15,4 @@ run attn_s1024 attn_stream 2 python tools/prof_attn.py 1024 20 3
 run attn_s4096 attn_stream 2 python tools/prof_attn.py 4096 10 3
 run attn_sd3 attn_stream 2 python tools/prof_attn.py 4429 24 3
 run attn_cross attn_single 2 python tools/prof_attn.py 1024 20 3 77
+run gn_parts gn_parts 0 python tools/gn_parts_time.py
