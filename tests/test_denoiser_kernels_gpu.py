@@ -451,3 +451,16 @@ def test_gemm_geglu_halfwidth_tail(M):
     if M == 1024:
         full = K.gemm(h, fold.w, bias=fold.bias, act=K.ACT_GEGLU, block_n=256, ln_fold=(rs, fold))
         assert torch.equal(full[:1024], out)
+
+
+def test_groupnorm_partials_dropped_when_overwritten():
+    """A GEMM that writes in place into a tensor carrying GroupNorm partials without
+    recording new ones drops them (stale statistics must never be folded)."""
+    torch.manual_seed(5)
+    hw, C = 1024, 640
+    y = K.gemm(rnd(2 * hw, 320), rnd(C, 320, s=320 ** -0.5), gn_hw=hw)
+    assert y.hp_gn is not None
+    K.gemm(rnd(2 * hw, 320), rnd(C, 320, s=320 ** -0.5), out=y)        # no gn_hw: partials now stale
+    assert getattr(y, "hp_gn", None) is None
+    g, b = torch.randn(C, device="cuda"), torch.randn(C, device="cuda")
+    close(K.group_norm(y, 2, hw, C, g, b), _gn_ref(y.float(), 2, hw, C, g, b, False))
