@@ -618,7 +618,7 @@ def main():
                        "predicted_pair_latency_s": pair_pred,
                        "predicted_pair_speedup_vs_batched": (value / pair_pred) if mode == "single" else None,
                        "predicted_pair_speedup_vs_sequential": seq_rho2 / pair_pred,
-                       "model": "50 x (B=1 forward + exchange (numel*2 B / 770 GB/s + 5 us) + sampler kernel)"},
+                       "model": f"{wl.T} x (B=1 forward + exchange (numel*2 B / 770 GB/s + 5 us) + sampler kernel)"},
         "sampler_roofline": {"bound": "hbm", "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_src,
                              "sizes": list(samp.values())},
         "clocks": clocks.summary(),
