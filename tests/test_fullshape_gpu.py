@@ -276,3 +276,50 @@ def test_sd3_28step_euler_generation_vs_oracle_loop():
     assert [t for t, _ in res.series] == [t for t, _ in series]
     assert mx <= YARD_MAX * ymx and mean <= YARD_MEAN * ymean, (mx, ymx, mean, ymean)
     assert rel.max() <= 2e-2
+
+
+def test_sd3_hybrid_stage_split_switch_vs_oracle():
+    """BASELINE config 3 at full shape: the SD3 hybrid plan (flow-matching Euler, CFG)
+    with the switch calibrated from the network's own discrepancy curves (L=15,
+    g=1e-4, k=5, tau_cap=22: profiles/r02/calibration/calibration_sd3.json) and the
+    stage-split window, against oracle.loop.run_staged(update="euler",
+    pipeline="stage_split") over the fp32 MMDiT: the switch schedule (tau1, tau2,
+    every step's label, the recorded series keys) must match exactly."""
+    from dataclasses import replace
+    from oracle import loop as oloop
+    from oracle.mmdit_ref import MMDiTRef
+    from oracle.stage_ref import StagedNet
+    from paper_2602_21760_b200.stages import network_fractions, stage_cuts
+    T, seed, w = 28, 0, 5.0
+    sw = dict(L=15, g_slope=1e-4, tau_cap=22, k=5)
+    s = SD3
+    W = init_weights(mmdit_param_specs(s), seed=0, device="cuda")
+    cond = synthetic_conditioning(1, s.ctx_len, s.ctx_dim, s.pooled_dim, device="cuda")
+    den = pipelines.build_sd3_denoiser(s, n_prompts=1, steps=T, weights=W, conditioning=cond)
+    plan = pipelines.sd3_plan(s, variant="hybrid", steps=T, seed=seed, guidance=w, denoiser=den, clock="model",
+                              switch=sw)
+    plan = replace(plan, pipeline_numerics="stage_split")
+    res = hp.run_plan(plan)
+    cuts = stage_cuts(den.net.unit_flops, network_fractions(plan.segment_fractions))
+    x_T = hp.initial_latents(plan)
+    fr = plan.segment_fractions
+    del den, plan
+    torch.cuda.empty_cache()
+    sch = pipelines.sd3_schedule(T)
+    net = StagedNet(MMDiTRef(s, W), "mmdit", cond, s, T, cuts, device="cuda", timestep=lambda t, T_: 1000.0 * t / T_)
+    xo, series, t1, t2, labels = oloop.run_staged(net, x_T, T, w, sch.alpha_bars, sch.sigmas, sw["L"],
+                                                  sw["g_slope"], sw["tau_cap"], sw["k"], fr, update="euler",
+                                                  pipeline="stage_split")
+    assert t1 is not None
+    assert (res.tau1, res.tau2) == (t1, t2), ((res.tau1, res.tau2), (t1, t2))
+    assert [s_.value for s_ in res.stages] == labels
+    assert [t for t, _ in res.series] == [t for t, _ in series]
+    m_gpu = np.array([m for _, m in res.series])
+    m_ref = np.array([m for _, m in series])
+    rel = np.abs(m_gpu - m_ref) / np.abs(m_ref)
+    mx, mean, _, _ = _report(f"sd3 hybrid stage_split x0 (tau1={t1}, tau2={t2}, "
+                             f"{'natural' if t1 < sw['tau_cap'] else 'cap'})", torch.from_numpy(res.x0),
+                             torch.from_numpy(xo))
+    print(f"PARITY sd3 hybrid: M_t max rel err {rel.max():.3g}")
+    assert rel.max() <= 2e-2
+    assert mx <= 8e-2 and mean <= 1.5e-2, (mx, mean)
